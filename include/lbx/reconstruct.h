@@ -1,0 +1,123 @@
+/*
+ * lbx/reconstruct.h -- C ABI of the B200-native decode-on-miss reconstruction path.
+ *
+ * What this replaces.  In the reference, a cache miss that needs pixels becomes a GPU job whose
+ * service time is the constant LatencyModel::decode_ms = 40 (proj/include/latentbox/sim.hpp:19):
+ *   Engine::on_job_ready  (proj/src/sim.cpp:409-429)  least-loaded GPU, start = max(t, free_at),
+ *                                                      free_at = start + decode_ms   (:414)
+ *   Engine::on_job_done   (proj/src/sim.cpp:431-442)  depth--, observe_latency(Decode, queue+decode)
+ *   observe_latency       (proj/include/latentbox/tuner.hpp:57-58, proj/src/tuner.cpp:48-59)
+ * called for LatentHit / FullMiss from Engine::on_arrival (proj/src/sim.cpp:364-405) and for the
+ * off-path promotion decode (:376-377).  There is no callable decode function in the reference
+ * (SPEC.md:8 scopes real decoding out); this header is the callable boundary those call sites get:
+ * lbx_reconstruct() is the "decode" of on_job_ready, its measured duration is the sample that
+ * on_job_done feeds to observe_latency, and lbx_batcher_* replaces least_loaded_gpu (sim.cpp:238-243)
+ * with real per-GPU queues.  INTEGRATION.md shows the call-site binding.
+ *
+ * Conventions mirrored from the reference:
+ *   - status codes instead of exceptions; LBX_E_CONFIG plays the role of ConfigError naming the bad
+ *     field (proj/include/latentbox/error.hpp:8-11), LBX_E_RUNTIME of std::runtime_error; the
+ *     message is available from lbx_last_error() (thread-local).
+ *   - single-owner state: one lbx_decoder per GPU, calls on it serialised by its owner thread
+ *     (proj/include/latentbox/dual_cache.hpp:46; the paper serialises each device behind
+ *     a lock).  Different decoders run concurrently from different threads.
+ *   - the caller owns inputs and outputs; the decoder owns weights, activation arena and CUDA graphs.
+ * No exceptions cross this boundary; no torch types appear in it.
+ */
+#ifndef LBX_RECONSTRUCT_H
+#define LBX_RECONSTRUCT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "lbx/lblp.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LBX_OK = 0,
+  LBX_E_RUNTIME = 1, /* runtime failure (std::runtime_error in the reference) */
+  LBX_E_CONFIG = 2,  /* invalid descriptor / argument (ConfigError, error.hpp:8-11) */
+  LBX_E_CUDA = 3,    /* CUDA error or no sm_100 device */
+  LBX_E_FORMAT = 4   /* malformed LBLP blob */
+} lbx_status;
+
+typedef enum { LBX_FAMILY_SD15 = 0, LBX_FAMILY_SD3 = 1, LBX_FAMILY_FLUX = 2 } lbx_family;
+
+/* Decoder descriptor.  Latent shapes: 4x64x64 (-> 512^2), 4x128x128 / 16x128x128 (-> 1024^2). */
+typedef struct {
+  int family;                 /* lbx_family: sets latent channels, scaling/shift, post_quant_conv */
+  uint32_t latent_h, latent_w; /* latent spatial size; output is 8x larger */
+  uint64_t weight_seed;       /* used when weights == NULL (deterministic generator) */
+  const float* weights;       /* optional: all parameters, fp32, canonical order (lbx_param_count) */
+  size_t weights_count;       /* number of floats in `weights` */
+  int device;                 /* CUDA device ordinal */
+  uint32_t max_batch;         /* largest n passed to decode/reconstruct (arena is sized for it) */
+} lbx_decoder_desc;
+
+typedef struct lbx_decoder lbx_decoder;
+typedef void* lbx_stream; /* cudaStream_t; NULL = the decoder's own stream */
+
+/* Number of fp32 parameters of a family's decoder (49,490,199 for SD1.5, 49,545,475 for SD3/FLUX). */
+size_t lbx_param_count(int family);
+
+/* The deterministic parameters a seed selects (fp32, canonical order; `out` holds count floats). */
+lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t count);
+
+lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out);
+lbx_status lbx_decoder_destroy(lbx_decoder* dec);
+
+/* Packed LBLP blobs (HOST memory) -> fp16 NCHW latents on the device, bit-exact.  Blob shapes must
+ * equal the decoder's (C, latent_h, latent_w).  Asynchronous on `stream`; a malformed blob is
+ * reported as LBX_E_FORMAT (host-side header validation) or at the next synchronising call. */
+lbx_status lbx_unpack(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                      void* latents_dev, lbx_stream stream);
+
+/* fp16 NCHW latents (device) -> uint8 RGB NHWC (device), n x 8h x 8w x 3.  Asynchronous. */
+lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uint8_t* rgb_dev,
+                      lbx_stream stream);
+
+/* The call the cache tiers make on a miss: host blobs -> H2D -> unpack -> decode (CUDA graph) ->
+ * D2H into rgb_host (n x 8h x 8w x 3).  Synchronous: returns when rgb_host is filled. */
+lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                           uint8_t* rgb_host, lbx_stream stream);
+
+/* Same path from fp16 NCHW latents in HOST memory (no codec): H2D -> decode -> D2H.  Synchronous. */
+lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
+                                   lbx_stream stream);
+
+/* Host-side LBLP packer (the write path).  `latent` is one fp16 NCHW latent (c*h*w values).
+ * Returns the blob size; writes it when out != NULL and cap is large enough. */
+lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, uint32_t w, uint8_t* out,
+                    size_t cap, size_t* out_bytes);
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char* lbx_last_error(void);
+
+/* ------------------------------------------------------------------ diagnostics / op-level entry
+ * Individual kernels of the path, for op-level parity tests and benchmarks.  Device pointers,
+ * fp16 = uint16 storage.  All asynchronous on `stream`. */
+
+/* tcgen05 GEMM / conv: out[m, n] = alpha*rs[m]*sum_k A[m,k]*B[n,k] + bias[n] + resid[m,n].
+ * mode 0 plain (A [M][K], row stride lda); mode 1 conv3x3 pad 1 (A NHWC [b][h][w][c], K = 9c);
+ * mode 2 nearest-2x upsample + conv3x3 as 4 sub-pixel 2x2 convs (B = [4][N][4c], out 2h x 2w).
+ * gn_stats (optional, double [b][32][2], accumulated) gets GroupNorm-32 partial sums of out.
+ * cta_group/bn: 0 = auto, else force 1|2 and 128|256. */
+lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
+                       const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
+                       const float* row_scale, float alpha, double* gn_stats, int cta_group, int bn,
+                       lbx_stream stream);
+/* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
+lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
+/* GroupNorm finalize + apply (SiLU when silu != 0); y may alias x. */
+lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta,
+                            int b, int hw, int c, int silu, float eps, lbx_stream stream);
+/* GroupNorm-32 statistics of x ([b][hw][c] fp16) into stats (double [b][32][2], zeroed here). */
+lbx_status lbx_op_gn_stats(const void* x, double* stats, int b, int hw, int c, lbx_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBX_RECONSTRUCT_H */

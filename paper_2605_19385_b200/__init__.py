@@ -1,0 +1,215 @@
+"""paper_2605_19385_b200 -- B200-native decode-on-miss reconstruction for LatentBox.
+
+Thin ctypes binding over the C ABI in include/lbx/reconstruct.h (liblbx.so, built in-tree by
+build.py).  The product path is the C++/CUDA library; this module only marshals pointers.  There is
+no CPU fallback: if liblbx.so is missing or no sm_100 device is present, calls fail loudly.
+
+Reference interface mirrored: the GPU job of the simulator (proj/src/sim.cpp:409-442), see
+include/lbx/reconstruct.h for the mapping.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblbx.so")
+
+FAMILY = {"sd15": 0, "sd3": 1, "flux": 2}
+LATENT_CHANNELS = {"sd15": 4, "sd3": 16, "flux": 16}
+
+OK, E_RUNTIME, E_CONFIG, E_CUDA, E_FORMAT = 0, 1, 2, 3, 4
+_STATUS = {1: "LBX_E_RUNTIME", 2: "LBX_E_CONFIG", 3: "LBX_E_CUDA", 4: "LBX_E_FORMAT"}
+
+# exported symbols (checked against include/lbx/reconstruct.h by tests/test_abi_cpu.py)
+SYMBOLS = [
+    "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
+    "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
+    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats",
+]
+
+
+class LbxError(RuntimeError):
+    """Raised on a non-zero lbx_status; .status holds the code (LBX_E_CONFIG ~ ConfigError)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int),
+        ("latent_h", ctypes.c_uint32),
+        ("latent_w", ctypes.c_uint32),
+        ("weight_seed", ctypes.c_uint64),
+        ("weights", ctypes.c_void_p),
+        ("weights_count", ctypes.c_size_t),
+        ("device", ctypes.c_int),
+        ("max_batch", ctypes.c_uint32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblbx.so (building it first when nvcc is available and the .so is missing)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _b
+        _b.build()
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u32, i32, sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_size_t
+    L.lbx_param_count.restype = sz
+    L.lbx_param_count.argtypes = [i32]
+    L.lbx_last_error.restype = ctypes.c_char_p
+    L.lbx_generate_params.argtypes = [i32, ctypes.c_uint64, vp, sz]
+    L.lbx_decoder_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(vp)]
+    L.lbx_decoder_destroy.argtypes = [vp]
+    L.lbx_unpack.argtypes = [vp, vp, vp, u32, vp, vp]
+    L.lbx_decode.argtypes = [vp, vp, u32, vp, vp]
+    L.lbx_reconstruct.argtypes = [vp, vp, vp, u32, vp, vp]
+    L.lbx_reconstruct_latents.argtypes = [vp, vp, u32, vp, vp]
+    L.lbx_pack.argtypes = [vp, i32, u32, u32, u32, vp, sz, ctypes.POINTER(sz)]
+    L.lbx_op_gemm.argtypes = [i32, i32, i32, i32, vp, i32, i32, i32, i32, i32, vp, i32, vp, i32, vp, vp, i32, vp,
+                              ctypes.c_float, vp, i32, i32, vp]
+    L.lbx_subpixel_weights.argtypes = [vp, i32, i32, vp]
+    L.lbx_op_groupnorm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, vp]
+    L.lbx_op_gn_stats.argtypes = [vp, vp, i32, i32, i32, vp]
+    for name in SYMBOLS:
+        if name not in ("lbx_param_count", "lbx_last_error"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != OK:
+        raise LbxError(status, lib().lbx_last_error().decode(errors="replace"))
+
+
+def param_count(family: str) -> int:
+    return int(lib().lbx_param_count(FAMILY[family]))
+
+
+def generate_params(family: str, seed: int) -> np.ndarray:
+    """The fp32 parameters (canonical order) the C++ generator produces for `seed`."""
+    n = param_count(family)
+    out = np.empty(n, dtype=np.float32)
+    check(lib().lbx_generate_params(FAMILY[family], seed, out.ctypes.data, n))
+    return out
+
+
+def pack(latent: np.ndarray, mode: int) -> bytes:
+    """Host LBLP packer (write path): one fp16 (C,H,W) latent -> blob."""
+    a = np.ascontiguousarray(latent.astype(np.float16)).view(np.uint16)
+    c, h, w = a.shape
+    n = ctypes.c_size_t(0)
+    check(lib().lbx_pack(a.ctypes.data, mode, c, h, w, None, 0, ctypes.byref(n)))
+    out = np.empty(n.value, dtype=np.uint8)
+    check(lib().lbx_pack(a.ctypes.data, mode, c, h, w, out.ctypes.data, n.value, ctypes.byref(n)))
+    return out.tobytes()
+
+
+class Decoder:
+    """One decoder per GPU (single owner; calls serialised by the owning thread)."""
+
+    def __init__(self, family: str = "sd15", latent_hw=(64, 64), seed: int = 0, device: int = 0,
+                 max_batch: int = 1, weights: np.ndarray | None = None):
+        self.family = family
+        self.h, self.w = latent_hw
+        self.c = LATENT_CHANNELS[family]
+        self.max_batch = max_batch
+        d = _Desc()
+        d.family = FAMILY[family]
+        d.latent_h, d.latent_w = self.h, self.w
+        d.weight_seed = seed
+        self._weights = None
+        if weights is not None:
+            self._weights = np.ascontiguousarray(weights, dtype=np.float32)
+            d.weights = self._weights.ctypes.data
+            d.weights_count = self._weights.size
+        d.device = device
+        d.max_batch = max_batch
+        h = ctypes.c_void_p()
+        check(lib().lbx_decoder_create(ctypes.byref(d), ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lbx_decoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def out_hw(self):
+        return 8 * self.h, 8 * self.w
+
+    # -- device-pointer entry points (pointers are ints, e.g. torch.Tensor.data_ptr()) --------
+    def decode_ptr(self, latents_dev: int, n: int, rgb_dev: int, stream: int = 0) -> None:
+        check(lib().lbx_decode(self._h, latents_dev, n, rgb_dev, stream or None))
+
+    def unpack_ptr(self, blobs, latents_dev: int, stream: int = 0) -> None:
+        arr, sizes, keep = _blob_arrays(blobs)
+        check(lib().lbx_unpack(self._h, arr, sizes, len(blobs), latents_dev, stream or None))
+
+    # -- host entry points ---------------------------------------------------------------------
+    def reconstruct(self, blobs, out: np.ndarray | None = None) -> np.ndarray:
+        """Packed LBLP blobs (host) -> uint8 RGB (n, 8h, 8w, 3)."""
+        n = len(blobs)
+        if out is None:
+            out = np.empty((n, 8 * self.h, 8 * self.w, 3), dtype=np.uint8)
+        arr, sizes, keep = _blob_arrays(blobs)
+        check(lib().lbx_reconstruct(self._h, arr, sizes, n, out.ctypes.data, None))
+        return out
+
+    def reconstruct_latents(self, latents: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """fp16 NCHW latents (host) -> uint8 RGB (n, 8h, 8w, 3)."""
+        lat = np.ascontiguousarray(latents.astype(np.float16))
+        n = lat.shape[0]
+        if out is None:
+            out = np.empty((n, 8 * self.h, 8 * self.w, 3), dtype=np.uint8)
+        check(lib().lbx_reconstruct_latents(self._h, lat.ctypes.data, n, out.ctypes.data, None))
+        return out
+
+
+def _blob_arrays(blobs):
+    bufs = [np.frombuffer(b, dtype=np.uint8) for b in blobs]
+    ptrs = (ctypes.c_void_p * len(bufs))(*[b.ctypes.data for b in bufs])
+    sizes = (ctypes.c_size_t * len(bufs))(*[b.size for b in bufs])
+    return ptrs, sizes, bufs
+
+
+def op_gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, *, b=0, h=0, w=0, c=0, bias=0, resid=0, ldr=0, row_scale=0,
+            alpha=1.0, gn_stats=0, cta_group=0, bn=0, stream=0):
+    """Diagnostic entry to the tcgen05 GEMM/conv kernel (device pointers as ints)."""
+    check(lib().lbx_op_gemm(mode, M, N, K, A, lda, b, h, w, c, B, ldb, out, ldo, bias or None, resid or None, ldr,
+                            row_scale or None, ctypes.c_float(alpha), gn_stats or None, cta_group, bn,
+                            stream or None))
+
+
+def subpixel_weights(w3x3: np.ndarray) -> np.ndarray:
+    """[N][3][3][C] fp32 conv weight -> [4][N][2][2][C] fp16 sub-pixel kernels."""
+    w = np.ascontiguousarray(w3x3, dtype=np.float32)
+    n, _, _, c = w.shape
+    out = np.empty((4, n, 2, 2, c), dtype=np.uint16)
+    check(lib().lbx_subpixel_weights(w.ctypes.data, n, c, out.ctypes.data))
+    return out.view(np.float16)
+
+
+def op_groupnorm(x, y, stats, gamma, beta, b, hw, c, silu=True, eps=1e-6, stream=0):
+    check(lib().lbx_op_groupnorm(x, y, stats, gamma, beta, b, hw, c, int(silu), ctypes.c_float(eps), stream or None))
+
+
+def op_gn_stats(x, stats, b, hw, c, stream=0):
+    check(lib().lbx_op_gn_stats(x, stats, b, hw, c, stream or None))

@@ -1,0 +1,803 @@
+// Decoder runtime + C ABI (include/lbx/reconstruct.h).
+//
+// One lbx_decoder per GPU owns: device weights in GEMM-ready layouts (fp16 K-major, conv taps
+// (ky,kx,ci) innermost-ci, upsample convs pre-folded into 4 sub-pixel 2x2 kernels), an activation
+// arena sized for max_batch (NHWC fp16), and a cache of CUDA graphs keyed by (n, in, out) -- the
+// paper wraps its TensorRT engine in a CUDA graph the same way.
+//
+// Layer plan per micro-batch, buffers X (residual stream), A (normalised
+// activations / shortcut / upsample output), H (conv1 output, normalised in place; attention QKV):
+//   prep(latents) -> A ; conv_in(A) -> X
+//   Res: A = SiLU(GN1(X)); H = conv1(A); H = SiLU(GN2(H)); [A = shortcut(X)]; X = conv2(H) + X|A
+//   Attn: A = GN(X); H = A Wqkv^T; per image: S = QK^T/sqrt(d); P = exp(S - max); O = P V / sum
+//         -> A; X = A Wo^T + bo + X
+//   Up:   A = subpixel_conv(X) (nearest-2x + conv3x3 in 4 phases); swap(X, A)
+//   tail: rgb = u8(conv_out(SiLU(GN(X))))
+// Every conv epilogue accumulates the GroupNorm-32 statistics its consumer needs.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "codec.h"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+#include "lbx/reconstruct.h"
+#include "model.h"
+
+namespace lbx {
+
+static thread_local std::string g_err;
+static lbx_status set_err(lbx_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+#define LBX_CUDA_TRY(expr)                                                                      \
+  do {                                                                                          \
+    cudaError_t _e = (expr);                                                                    \
+    if (_e != cudaSuccess)                                                                      \
+      return set_err(LBX_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+struct ConvW {
+  __half* w = nullptr;
+  float* b = nullptr;
+};
+struct NormW {
+  float* g = nullptr;
+  float* b = nullptr;
+};
+struct ResW {
+  int cin = 0, cout = 0;
+  NormW n1, n2;
+  ConvW c1, c2, sc;
+};
+
+class Decoder {
+ public:
+  lbx_decoder_desc desc{};
+  FamilyInfo fi{};
+  int h = 0, w = 0, cl = 0, max_batch = 0;
+  cudaStream_t stream = nullptr;
+
+  // weights
+  void* wblock = nullptr;
+  float *pq_w = nullptr, *pq_b = nullptr;
+  ConvW conv_in;
+  ResW res[14];
+  NormW attn_gn;
+  __half* wqkv = nullptr;
+  float* bqkv = nullptr;
+  __half* wo = nullptr;
+  float* bo = nullptr;
+  ConvW up[3];
+  NormW norm_out;
+  float *wout = nullptr, *bout = nullptr;
+
+  // arena
+  void* arena = nullptr;
+  __half *X = nullptr, *A = nullptr, *Hb = nullptr, *S = nullptr, *Vt = nullptr, *lat = nullptr;
+  float* rowscale = nullptr;
+  double* stats = nullptr;
+  float2* ss = nullptr;
+  uint8_t* rgb = nullptr;
+  int* err = nullptr;
+  static constexpr int kMaxSites = 64;
+
+  // blob staging
+  uint8_t* blob_dev = nullptr;
+  size_t blob_dev_cap = 0;
+  uint8_t* blob_host = nullptr;  // pinned
+  size_t blob_host_cap = 0;
+  unsigned long long* offs_dev = nullptr;
+  unsigned int* sizes_dev = nullptr;
+  unsigned long long* offs_host = nullptr;  // pinned [max_batch] offsets + sizes
+  int* err_host = nullptr;
+
+  std::map<std::tuple<int, const void*, const void*>, cudaGraphExec_t> graphs;
+  int launches_per_decode = 0;
+
+  ~Decoder() { release(); }
+
+  void release() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(desc.device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    graphs.clear();
+    if (wblock) cudaFree(wblock);
+    if (arena) cudaFree(arena);
+    if (blob_dev) cudaFree(blob_dev);
+    if (blob_host) cudaFreeHost(blob_host);
+    if (offs_host) cudaFreeHost(offs_host);
+    if (stream) cudaStreamDestroy(stream);
+    wblock = arena = nullptr;
+    blob_dev = blob_host = nullptr;
+    offs_host = nullptr;
+    stream = nullptr;
+    cudaSetDevice(cur);
+  }
+
+  size_t lat_elems(int n) const { return (size_t)n * cl * h * w; }
+  size_t rgb_bytes(int n) const { return (size_t)n * 64 * h * w * 3; }
+
+  lbx_status init(const lbx_decoder_desc& d);
+  lbx_status upload_weights(const std::vector<float>& p);
+  lbx_status alloc_arena();
+  lbx_status plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, bool counting);
+  lbx_status run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s);
+  lbx_status stage_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, cudaStream_t s);
+};
+
+// --------------------------------------------------------------------------- weights
+namespace {
+struct Bump {
+  uint8_t* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+}  // namespace
+
+lbx_status Decoder::upload_weights(const std::vector<float>& p) {
+  const auto specs = param_specs(fi.latent_channels, fi.post_quant);
+  std::unordered_map<std::string, const float*> by_name;
+  size_t pos = 0;
+  for (const auto& s : specs) {
+    by_name[s.name] = p.data() + pos;
+    pos += s.count();
+  }
+  auto get = [&](const std::string& n) { return by_name.at(n); };
+
+  // host staging buffer mirrors the device block
+  std::vector<uint8_t> host(160u << 20, 0);
+  Bump hb{host.data()};
+  std::vector<std::pair<size_t, size_t>> dummy;
+  struct Fix {
+    size_t off;
+    void** dst;
+  };
+  std::vector<Fix> fixes;
+  auto f32 = [&](const float* src, size_t n, float** dst) {
+    float* q = hb.take<float>(n);
+    std::memcpy(q, src, n * 4);
+    fixes.push_back({(size_t)((uint8_t*)q - host.data()), (void**)dst});
+  };
+  auto h16 = [&](size_t n, __half** dst) -> uint16_t* {
+    uint16_t* q = hb.take<uint16_t>(n);
+    fixes.push_back({(size_t)((uint8_t*)q - host.data()), (void**)dst});
+    return q;
+  };
+  // conv3x3 [cout][cin][3][3] -> [cout][ky][kx][cin_pad]
+  auto conv3 = [&](const std::string& n, int cin, int cout, int cin_pad, ConvW* cw) {
+    const float* W = get(n + ".weight");
+    uint16_t* q = h16((size_t)cout * 9 * cin_pad, &cw->w);
+    for (int o = 0; o < cout; ++o)
+      for (int t = 0; t < 9; ++t)
+        for (int c = 0; c < cin; ++c) q[((size_t)o * 9 + t) * cin_pad + c] = f32_to_f16_bits(W[((size_t)o * cin + c) * 9 + t]);
+    f32(get(n + ".bias"), cout, &cw->b);
+  };
+  auto norm = [&](const std::string& n, int c, NormW* nw) {
+    f32(get(n + ".weight"), c, &nw->g);
+    f32(get(n + ".bias"), c, &nw->b);
+  };
+  auto lin = [&](const float* W, int cout, int cin, uint16_t* q) {
+    for (size_t i = 0; i < (size_t)cout * cin; ++i) q[i] = f32_to_f16_bits(W[i]);
+  };
+
+  if (fi.post_quant) {
+    f32(get("post_quant_conv.weight"), (size_t)cl * cl, &pq_w);
+    f32(get("post_quant_conv.bias"), cl, &pq_b);
+  }
+  conv3("decoder.conv_in", cl, 512, 64, &conv_in);
+  const int chans[4] = {512, 512, 256, 128};
+  std::vector<std::string> rnames = {"decoder.mid_block.resnets.0", "decoder.mid_block.resnets.1"};
+  std::vector<std::pair<int, int>> rio = {{512, 512}, {512, 512}};
+  int prev = 512;
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 3; ++j) {
+      rnames.push_back("decoder.up_blocks." + std::to_string(i) + ".resnets." + std::to_string(j));
+      rio.push_back({j == 0 ? prev : chans[i], chans[i]});
+      if (j == 2) prev = chans[i];
+    }
+  for (int r = 0; r < 14; ++r) {
+    ResW& R = res[r];
+    R.cin = rio[r].first;
+    R.cout = rio[r].second;
+    norm(rnames[r] + ".norm1", R.cin, &R.n1);
+    conv3(rnames[r] + ".conv1", R.cin, R.cout, R.cin, &R.c1);
+    norm(rnames[r] + ".norm2", R.cout, &R.n2);
+    conv3(rnames[r] + ".conv2", R.cout, R.cout, R.cout, &R.c2);
+    if (R.cin != R.cout) {
+      uint16_t* q = h16((size_t)R.cout * R.cin, &R.sc.w);
+      lin(get(rnames[r] + ".conv_shortcut.weight"), R.cout, R.cin, q);
+      f32(get(rnames[r] + ".conv_shortcut.bias"), R.cout, &R.sc.b);
+    }
+  }
+  const std::string an = "decoder.mid_block.attentions.0";
+  norm(an + ".group_norm", 512, &attn_gn);
+  {
+    uint16_t* q = h16((size_t)1536 * 512, &wqkv);
+    lin(get(an + ".to_q.weight"), 512, 512, q);
+    lin(get(an + ".to_k.weight"), 512, 512, q + 512 * 512);
+    lin(get(an + ".to_v.weight"), 512, 512, q + 2 * 512 * 512);
+    float* bq = hb.take<float>(1536);
+    std::memcpy(bq, get(an + ".to_q.bias"), 512 * 4);
+    std::memcpy(bq + 512, get(an + ".to_k.bias"), 512 * 4);
+    std::memcpy(bq + 1024, get(an + ".to_v.bias"), 512 * 4);
+    fixes.push_back({(size_t)((uint8_t*)bq - host.data()), (void**)&bqkv});
+    uint16_t* qo = h16((size_t)512 * 512, &wo);
+    lin(get(an + ".to_out.0.weight"), 512, 512, qo);
+    f32(get(an + ".to_out.0.bias"), 512, &bo);
+  }
+  for (int i = 0; i < 3; ++i) {
+    const std::string n = "decoder.up_blocks." + std::to_string(i) + ".upsamplers.0.conv";
+    const int c = chans[i];
+    const float* W = get(n + ".weight");  // [c][c][3][3]
+    uint16_t* q = h16((size_t)4 * c * 4 * c, &up[i].w);
+    // phase (a,b): 2x2 taps (r,s); row r gathers original ky in S_a[r], S_0 = {{0},{1,2}}, S_1 = {{0,1},{2}}
+    static const int kset[2][2][2] = {{{0, -1}, {1, 2}}, {{0, 1}, {2, -1}}};
+    for (int ph = 0; ph < 4; ++ph) {
+      const int a = ph >> 1, bb = ph & 1;
+      for (int o = 0; o < c; ++o)
+        for (int t = 0; t < 4; ++t) {
+          const int r = t >> 1, s = t & 1;
+          for (int ci = 0; ci < c; ++ci) {
+            float acc = 0.f;
+            for (int u = 0; u < 2; ++u) {
+              const int ky = kset[a][r][u];
+              if (ky < 0) continue;
+              for (int v = 0; v < 2; ++v) {
+                const int kx = kset[bb][s][v];
+                if (kx < 0) continue;
+                acc += W[(((size_t)o * c + ci) * 3 + ky) * 3 + kx];
+              }
+            }
+            q[(((size_t)ph * c + o) * 4 + t) * c + ci] = f32_to_f16_bits(acc);
+          }
+        }
+    }
+    f32(get(n + ".bias"), c, &up[i].b);
+  }
+  norm("decoder.conv_norm_out", 128, &norm_out);
+  {
+    const float* W = get("decoder.conv_out.weight");  // [3][128][3][3] -> [3][ky][kx][128]
+    float* q = hb.take<float>(3 * 9 * 128);
+    for (int o = 0; o < 3; ++o)
+      for (int t = 0; t < 9; ++t)
+        for (int c = 0; c < 128; ++c) q[(o * 9 + t) * 128 + c] = W[(o * 128 + c) * 9 + t];
+    fixes.push_back({(size_t)((uint8_t*)q - host.data()), (void**)&wout});
+    f32(get("decoder.conv_out.bias"), 3, &bout);
+  }
+  const size_t bytes = (hb.off + 255) & ~size_t(255);
+  if (bytes > host.size()) return set_err(LBX_E_RUNTIME, "weight staging overflow");
+  LBX_CUDA_TRY(cudaMalloc(&wblock, bytes));
+  LBX_CUDA_TRY(cudaMemcpy(wblock, host.data(), bytes, cudaMemcpyHostToDevice));
+  for (const auto& f : fixes) *f.dst = (uint8_t*)wblock + f.off;
+  return LBX_OK;
+}
+
+// --------------------------------------------------------------------------- arena
+lbx_status Decoder::alloc_arena() {
+  const size_t hw = (size_t)h * w;
+  const size_t nb = (size_t)max_batch;
+  const size_t x_el = nb * hw * 64 * 256;  // max residual-stream tensor: 8h x 8w x 256
+  const size_t h_el = nb * hw * 64 * 128;  // max conv1 output: 8h x 8w x 128 (>= QKV hw x 1536)
+  const size_t s_el = hw * hw;             // one image's attention scores
+  const size_t vt_el = 512 * hw;
+  size_t off = 0;
+  auto slot = [&](size_t bytes) {
+    size_t o = (off + 1023) & ~size_t(1023);
+    off = o + bytes;
+    return o;
+  };
+  const size_t oX = slot(x_el * 2), oA = slot(x_el * 2), oH = slot(h_el * 2), oS = slot(s_el * 2),
+               oVt = slot(vt_el * 2), oR = slot(hw * 4), oSt = slot((size_t)kMaxSites * nb * 64 * 8),
+               oSs = slot(nb * 512 * 8), oLat = slot(nb * cl * hw * 2), oRgb = slot(nb * hw * 64 * 3),
+               oErr = slot(64);
+  LBX_CUDA_TRY(cudaMalloc(&arena, off));
+  uint8_t* b = (uint8_t*)arena;
+  X = (__half*)(b + oX);
+  A = (__half*)(b + oA);
+  Hb = (__half*)(b + oH);
+  S = (__half*)(b + oS);
+  Vt = (__half*)(b + oVt);
+  rowscale = (float*)(b + oR);
+  stats = (double*)(b + oSt);
+  ss = (float2*)(b + oSs);
+  lat = (__half*)(b + oLat);
+  rgb = b + oRgb;
+  err = (int*)(b + oErr);
+  LBX_CUDA_TRY(cudaMemset(err, 0, 64));
+  LBX_CUDA_TRY(cudaMallocHost(&offs_host, nb * 16 + 64));
+  err_host = reinterpret_cast<int*>(offs_host + 2 * nb);
+  return LBX_OK;
+}
+
+lbx_status Decoder::init(const lbx_decoder_desc& d) {
+  desc = d;
+  if (!family_info(d.family, &fi)) return set_err(LBX_E_CONFIG, "desc.family: unknown family");
+  cl = fi.latent_channels;
+  h = (int)d.latent_h;
+  w = (int)d.latent_w;
+  max_batch = (int)d.max_batch;
+  if (max_batch <= 0 || max_batch > 4096) return set_err(LBX_E_CONFIG, "desc.max_batch: must be in [1, 4096]");
+  if (h < 8 || w < 8 || h > 512 || w > 512) return set_err(LBX_E_CONFIG, "desc.latent_h/latent_w: out of range");
+  // tile geometry: every resolution's width must be 64 or a multiple of 128, heights even
+  if (!((w == 64) || (w % 128 == 0)) || h % 2) return set_err(LBX_E_CONFIG, "desc.latent_w: must be 64 or a multiple of 128 (latent_h even)");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return set_err(LBX_E_CUDA, "no CUDA device");
+  if (d.device < 0 || d.device >= ndev) return set_err(LBX_E_CONFIG, "desc.device: no such device");
+  LBX_CUDA_TRY(cudaSetDevice(d.device));
+  cudaDeviceProp prop;
+  LBX_CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+  if (prop.major != 10) return set_err(LBX_E_CUDA, "device is not sm_100 (B200); this build has no other code path");
+  if (!gemm_tc_prepare()) return set_err(LBX_E_CUDA, "tcgen05 GEMM setup failed (cuTensorMapEncodeTiled / smem attribute)");
+  LBX_CUDA_TRY(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  std::vector<float> params;
+  const size_t expect = param_specs(fi.latent_channels, fi.post_quant).size();
+  (void)expect;
+  size_t count = 0;
+  for (const auto& s : param_specs(fi.latent_channels, fi.post_quant)) count += s.count();
+  if (d.weights) {
+    if (d.weights_count != count) return set_err(LBX_E_CONFIG, "desc.weights_count: != lbx_param_count(family)");
+    params.assign(d.weights, d.weights + count);
+  } else {
+    params = generate_params(d.family, d.weight_seed);
+  }
+  lbx_status st = upload_weights(params);
+  if (st != LBX_OK) return st;
+  return alloc_arena();
+}
+
+// --------------------------------------------------------------------------- plan
+lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, bool counting) {
+  int launches = 0;
+  int site = 0;
+  const size_t site_stride = (size_t)max_batch * 64;
+  auto site_ptr = [&](int i) { return stats + (size_t)i * site_stride; };
+  auto chk = [&](cudaError_t e, const char* what) -> lbx_status {
+    if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return LBX_OK;
+  };
+#define LBX_STEP(expr, what)                       \
+  do {                                             \
+    lbx_status _s = chk((expr), what);             \
+    if (_s != LBX_OK) return _s;                   \
+  } while (0)
+#define LBX_LAUNCH(stmt, what)                     \
+  do {                                             \
+    stmt;                                          \
+    ++launches;                                    \
+    LBX_STEP(cudaPeekAtLastError(), what);         \
+  } while (0)
+
+  __half* X_ = X;
+  __half* A_ = A;
+  LBX_STEP(cudaMemsetAsync(stats, 0, (size_t)kMaxSites * site_stride * 8, s), "memset stats");
+
+  auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
+    ++launches;
+    return chk(gemm_tc_launch(ga, s), what);
+  };
+  auto gn = [&](int st_site, const NormW& nw, const __half* x, __half* y, int C, int hw, bool silu) -> lbx_status {
+    LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)hw * (C / 32), 1e-6f, s), "gn_finalize");
+    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, s), "gn_apply");
+    return LBX_OK;
+  };
+  auto conv3 = [&](const __half* in, int H, int W, int C, const ConvW& cw, int N, __half* out, const __half* resid,
+                   int out_site, const char* what) -> lbx_status {
+    GemmArgs g;
+    g.mode = GEMM_CONV3X3;
+    g.M = n * H * W; g.N = N; g.K = 9 * C;
+    g.A = in; g.B_img = n; g.H = H; g.W = W; g.C = C;
+    g.Bw = cw.w; g.ldb = 9 * C;
+    g.out = out; g.ldo = N; g.bias = cw.b;
+    g.resid = resid; g.ldr = N;
+    g.gn_stats = out_site >= 0 ? site_ptr(out_site) : nullptr;
+    g.gn_cpg = N / 32; g.rows_per_img = H * W;
+    return gemm(g, what);
+  };
+  lbx_status st;
+
+  // prep + conv_in
+  LBX_LAUNCH(launch_latent_prep(lat_in, A_, n, cl, h, w, fi.scaling, fi.shift, pq_w, pq_b, s), "latent_prep");
+  int x_site = site++;
+  if ((st = conv3(A_, h, w, 64, conv_in, 512, X_, nullptr, x_site, "conv_in")) != LBX_OK) return st;
+
+  auto resnet = [&](const ResW& R, int H, int W) -> lbx_status {
+    const int hw = H * W;
+    lbx_status e;
+    if ((e = gn(x_site, R.n1, X_, A_, R.cin, hw, true)) != LBX_OK) return e;
+    const int mid = site++;
+    if ((e = conv3(A_, H, W, R.cin, R.c1, R.cout, Hb, nullptr, mid, "resnet.conv1")) != LBX_OK) return e;
+    if ((e = gn(mid, R.n2, Hb, Hb, R.cout, hw, true)) != LBX_OK) return e;
+    const __half* resid = X_;
+    if (R.cin != R.cout) {
+      GemmArgs g;
+      g.mode = GEMM_PLAIN;
+      g.M = n * hw; g.N = R.cout; g.K = R.cin;
+      g.A = X_; g.lda = R.cin;
+      g.Bw = R.sc.w; g.ldb = R.cin;
+      g.out = A_; g.ldo = R.cout; g.bias = R.sc.b;
+      if ((e = gemm(g, "resnet.shortcut")) != LBX_OK) return e;
+      resid = A_;
+    }
+    const int out_site = site++;
+    if ((e = conv3(Hb, H, W, R.cout, R.c2, R.cout, X_, resid, out_site, "resnet.conv2")) != LBX_OK) return e;
+    x_site = out_site;
+    return LBX_OK;
+  };
+
+  // mid block
+  if ((st = resnet(res[0], h, w)) != LBX_OK) return st;
+  {
+    const int L = h * w;
+    if ((st = gn(x_site, attn_gn, X_, A_, 512, L, false)) != LBX_OK) return st;
+    GemmArgs g;
+    g.mode = GEMM_PLAIN;
+    g.M = n * L; g.N = 1536; g.K = 512;
+    g.A = A_; g.lda = 512; g.Bw = wqkv; g.ldb = 512;
+    g.out = Hb; g.ldo = 1536; g.bias = bqkv;
+    if ((st = gemm(g, "attn.qkv")) != LBX_OK) return st;
+    for (int i = 0; i < n; ++i) {
+      const __half* base = Hb + (size_t)i * L * 1536;
+      GemmArgs sq;
+      sq.mode = GEMM_PLAIN;
+      sq.M = L; sq.N = L; sq.K = 512;
+      sq.A = base; sq.lda = 1536;
+      sq.Bw = base + 512; sq.ldb = 1536;
+      sq.out = S; sq.ldo = L;
+      sq.alpha = 1.0f / std::sqrt(512.0f);
+      if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
+      LBX_LAUNCH(launch_softmax_rows(S, rowscale, L, L, s), "attn.softmax");
+      LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose");
+      GemmArgs pv;
+      pv.mode = GEMM_PLAIN;
+      pv.M = L; pv.N = 512; pv.K = L;
+      pv.A = S; pv.lda = L;
+      pv.Bw = Vt; pv.ldb = L;
+      pv.out = A_ + (size_t)i * L * 512; pv.ldo = 512;
+      pv.row_scale = rowscale;
+      if ((st = gemm(pv, "attn.pv")) != LBX_OK) return st;
+    }
+    GemmArgs o;
+    o.mode = GEMM_PLAIN;
+    o.M = n * L; o.N = 512; o.K = 512;
+    o.A = A_; o.lda = 512; o.Bw = wo; o.ldb = 512;
+    o.out = X_; o.ldo = 512; o.bias = bo; o.resid = X_; o.ldr = 512;
+    const int out_site = site++;
+    o.gn_stats = site_ptr(out_site); o.gn_cpg = 16; o.rows_per_img = L;
+    if ((st = gemm(o, "attn.out")) != LBX_OK) return st;
+    x_site = out_site;
+  }
+  if ((st = resnet(res[1], h, w)) != LBX_OK) return st;
+
+  // up blocks
+  int H = h, W = w;
+  const int chans[4] = {512, 512, 256, 128};
+  for (int i = 0; i < 4; ++i) {
+    for (int j = 0; j < 3; ++j)
+      if ((st = resnet(res[2 + 3 * i + j], H, W)) != LBX_OK) return st;
+    if (i < 3) {
+      const int c = chans[i];
+      GemmArgs g;
+      g.mode = GEMM_SUBPIX;
+      g.M = n * H * W; g.N = c; g.K = 4 * c;
+      g.A = X_; g.B_img = n; g.H = H; g.W = W; g.C = c;
+      g.Bw = up[i].w; g.ldb = 4 * c;
+      g.out = A_; g.ldo = c; g.bias = up[i].b;
+      const int out_site = site++;
+      g.gn_stats = site_ptr(out_site); g.gn_cpg = c / 32; g.rows_per_img = H * W;
+      if ((st = gemm(g, "upsample.subpixel_conv")) != LBX_OK) return st;
+      x_site = out_site;
+      std::swap(X_, A_);
+      H *= 2;
+      W *= 2;
+    }
+  }
+  // tail
+  LBX_LAUNCH(launch_gn_finalize(site_ptr(x_site), norm_out.g, norm_out.b, ss, n, 128, (double)H * W * 4, 1e-6f, s),
+             "norm_out.finalize");
+  LBX_LAUNCH(launch_conv_out_u8(X_, ss, wout, bout, rgb_out, n, H, W, s), "conv_out_u8");
+  if (site > kMaxSites) return set_err(LBX_E_RUNTIME, "too many GroupNorm sites");
+  if (counting) launches_per_decode = launches;
+  return LBX_OK;
+#undef LBX_STEP
+#undef LBX_LAUNCH
+}
+
+lbx_status Decoder::run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s) {
+  auto key = std::make_tuple(n, (const void*)lat_in, (const void*)rgb_out);
+  auto it = graphs.find(key);
+  if (it == graphs.end()) {
+    if (graphs.size() >= 16) {
+      for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+      graphs.clear();
+    }
+    cudaGraph_t g = nullptr;
+    LBX_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    lbx_status st = plan(n, lat_in, rgb_out, s, true);
+    cudaError_t ce = cudaStreamEndCapture(s, &g);
+    if (st != LBX_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (ce != cudaSuccess) return set_err(LBX_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t ex = nullptr;
+    ce = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return set_err(LBX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    it = graphs.emplace(key, ex).first;
+  }
+  LBX_CUDA_TRY(cudaGraphLaunch(it->second, s));
+  return LBX_OK;
+}
+
+lbx_status Decoder::stage_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, cudaStream_t s) {
+  size_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    std::string why;
+    if (!blobs || !nbytes || !blobs[i]) return set_err(LBX_E_CONFIG, "blobs: null pointer");
+    if (!lblp_validate(blobs[i], nbytes[i], cl, h, w, &why))
+      return set_err(LBX_E_FORMAT, "blob " + std::to_string(i) + ": " + why);
+    total += (nbytes[i] + 15) & ~size_t(15);
+  }
+  if (total > blob_host_cap) {
+    // the previous H2D from the pinned buffer must be complete before it is replaced
+    LBX_CUDA_TRY(cudaStreamSynchronize(s));
+    if (blob_host) cudaFreeHost(blob_host);
+    if (blob_dev) cudaFree(blob_dev);
+    blob_host_cap = blob_dev_cap = (total + (total >> 2) + 4096 + 255) & ~size_t(255);  // offs_dev follows: keep 8B+ alignment
+    LBX_CUDA_TRY(cudaMallocHost(&blob_host, blob_host_cap));
+    LBX_CUDA_TRY(cudaMalloc(&blob_dev, blob_dev_cap + (size_t)max_batch * 16));
+    offs_dev = reinterpret_cast<unsigned long long*>(blob_dev + blob_dev_cap);
+    sizes_dev = reinterpret_cast<unsigned int*>(offs_dev + max_batch);
+  } else {
+    LBX_CUDA_TRY(cudaStreamSynchronize(s));  // pinned staging is reused
+  }
+  size_t off = 0;
+  unsigned int* sizes_host = reinterpret_cast<unsigned int*>(offs_host + max_batch);
+  for (uint32_t i = 0; i < n; ++i) {
+    std::memcpy(blob_host + off, blobs[i], nbytes[i]);
+    offs_host[i] = off;
+    sizes_host[i] = (unsigned int)nbytes[i];
+    off += (nbytes[i] + 15) & ~size_t(15);
+  }
+  LBX_CUDA_TRY(cudaMemcpyAsync(blob_dev, blob_host, off, cudaMemcpyHostToDevice, s));
+  LBX_CUDA_TRY(cudaMemcpyAsync(offs_dev, offs_host, (size_t)max_batch * 12, cudaMemcpyHostToDevice, s));
+  launch_lblp_unpack(blob_dev, offs_dev, sizes_dev, (int)n, cl, h, w, lat, err, s);
+  LBX_CUDA_TRY(cudaPeekAtLastError());
+  return LBX_OK;
+}
+
+}  // namespace lbx
+
+// =========================================================================== C ABI
+using lbx::Decoder;
+using lbx::set_err;
+
+struct lbx_decoder {
+  Decoder d;
+  std::mutex mu;  // defensive: the contract is single-owner per decoder
+};
+
+static cudaStream_t pick(lbx_decoder* dec, lbx_stream s) {
+  return s ? reinterpret_cast<cudaStream_t>(s) : dec->d.stream;
+}
+
+extern "C" {
+
+const char* lbx_last_error(void) { return lbx::g_err.c_str(); }
+
+size_t lbx_param_count(int family) {
+  lbx::FamilyInfo fi;
+  if (!lbx::family_info(family, &fi)) return 0;
+  size_t n = 0;
+  for (const auto& s : lbx::param_specs(fi.latent_channels, fi.post_quant)) n += s.count();
+  return n;
+}
+
+lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t count) {
+  if (!out || count != lbx_param_count(family) || count == 0)
+    return set_err(LBX_E_CONFIG, "lbx_generate_params: count != lbx_param_count(family)");
+  const std::vector<float> p = lbx::generate_params(family, seed);
+  std::memcpy(out, p.data(), count * sizeof(float));
+  return LBX_OK;
+}
+
+lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out) {
+  if (!desc || !out) return set_err(LBX_E_CONFIG, "lbx_decoder_create: null argument");
+  *out = nullptr;
+  auto* dec = new (std::nothrow) lbx_decoder;
+  if (!dec) return set_err(LBX_E_RUNTIME, "out of host memory");
+  lbx_status st = dec->d.init(*desc);
+  if (st != LBX_OK) {
+    delete dec;
+    return st;
+  }
+  *out = dec;
+  lbx::g_err.clear();
+  return LBX_OK;
+}
+
+lbx_status lbx_decoder_destroy(lbx_decoder* dec) {
+  if (!dec) return set_err(LBX_E_CONFIG, "lbx_decoder_destroy: null decoder");
+  delete dec;
+  return LBX_OK;
+}
+
+lbx_status lbx_unpack(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                      void* latents_dev, lbx_stream stream) {
+  if (!dec || !latents_dev) return set_err(LBX_E_CONFIG, "lbx_unpack: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  cudaStream_t s = pick(dec, stream);
+  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  if (st != LBX_OK) return st;
+  if (cudaMemcpyAsync(latents_dev, d.lat, d.lat_elems(n) * 2, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "lbx_unpack: copy out failed");
+  return LBX_OK;
+}
+
+lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uint8_t* rgb_dev, lbx_stream stream) {
+  if (!dec || !latents_dev || !rgb_dev) return set_err(LBX_E_CONFIG, "lbx_decode: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  return d.run((int)n, reinterpret_cast<const __half*>(latents_dev), rgb_dev, pick(dec, stream));
+}
+
+static lbx_status finish_reconstruct(Decoder& d, uint32_t n, uint8_t* rgb_host, cudaStream_t s) {
+  lbx_status st = d.run((int)n, d.lat, d.rgb, s);
+  if (st != LBX_OK) return st;
+  if (cudaMemcpyAsync(rgb_host, d.rgb, d.rgb_bytes(n), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "D2H of rgb failed");
+  if (cudaMemcpyAsync(d.err_host, d.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "D2H of status failed");
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("reconstruct: ") + cudaGetErrorString(e));
+  if (*d.err_host) {
+    cudaMemset(d.err, 0, 4);
+    return set_err(LBX_E_FORMAT, "device unpack reported a malformed blob (code " + std::to_string(*d.err_host) + ")");
+  }
+  return LBX_OK;
+}
+
+lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                           uint8_t* rgb_host, lbx_stream stream) {
+  if (!dec || !rgb_host) return set_err(LBX_E_CONFIG, "lbx_reconstruct: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  cudaStream_t s = pick(dec, stream);
+  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  if (st != LBX_OK) return st;
+  return finish_reconstruct(d, n, rgb_host, s);
+}
+
+lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
+                                   lbx_stream stream) {
+  if (!dec || !latents_host || !rgb_host) return set_err(LBX_E_CONFIG, "lbx_reconstruct_latents: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  cudaStream_t s = pick(dec, stream);
+  if (cudaMemcpyAsync(d.lat, latents_host, d.lat_elems(n) * 2, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "H2D of latents failed");
+  return finish_reconstruct(d, n, rgb_host, s);
+}
+
+lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, uint32_t w, uint8_t* out, size_t cap,
+                    size_t* out_bytes) {
+  std::vector<uint8_t> blob;
+  std::string why;
+  if (!lbx::lblp_pack(latent, mode, c, h, w, &blob, &why)) return set_err(LBX_E_CONFIG, why);
+  if (out_bytes) *out_bytes = blob.size();
+  if (out) {
+    if (cap < blob.size()) return set_err(LBX_E_CONFIG, "cap: smaller than the encoded blob");
+    std::memcpy(out, blob.data(), blob.size());
+  }
+  return LBX_OK;
+}
+
+// ------------------------------------------------------------------ op-level entry points
+lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
+                       const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
+                       const float* row_scale, float alpha, double* gn_stats, int cta_group, int bn,
+                       lbx_stream stream) {
+  lbx::GemmArgs g;
+  g.mode = mode;
+  g.M = M; g.N = N; g.K = K;
+  g.A = reinterpret_cast<const __half*>(A); g.lda = lda;
+  g.B_img = b; g.H = h; g.W = w; g.C = c;
+  g.Bw = reinterpret_cast<const __half*>(Bw); g.ldb = ldb;
+  g.out = reinterpret_cast<__half*>(out); g.ldo = ldo;
+  g.bias = bias;
+  g.resid = reinterpret_cast<const __half*>(resid); g.ldr = ldr;
+  g.row_scale = row_scale; g.alpha = alpha;
+  g.gn_stats = gn_stats; g.gn_cpg = N / 32; g.rows_per_img = (mode == 0) ? (b > 0 ? M / b : M) : h * w;
+  cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), cta_group, bn);
+  if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
+                                       std::string("lbx_op_gemm: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+lbx_status lbx_subpixel_weights(const float* w3, int N, int C, uint16_t* out) {
+  if (!w3 || !out || N <= 0 || C <= 0) return set_err(LBX_E_CONFIG, "lbx_subpixel_weights: bad argument");
+  static const int kset[2][2][2] = {{{0, -1}, {1, 2}}, {{0, 1}, {2, -1}}};
+  for (int ph = 0; ph < 4; ++ph) {
+    const int a = ph >> 1, bb = ph & 1;
+    for (int o = 0; o < N; ++o)
+      for (int t = 0; t < 4; ++t)
+        for (int ci = 0; ci < C; ++ci) {
+          float acc = 0.f;
+          for (int u = 0; u < 2; ++u) {
+            const int ky = kset[a][t >> 1][u];
+            if (ky < 0) continue;
+            for (int v = 0; v < 2; ++v) {
+              const int kx = kset[bb][t & 1][v];
+              if (kx < 0) continue;
+              acc += w3[(((size_t)o * 3 + ky) * 3 + kx) * C + ci];
+            }
+          }
+          out[(((size_t)ph * N + o) * 4 + t) * C + ci] = lbx::f32_to_f16_bits(acc);
+        }
+  }
+  return LBX_OK;
+}
+
+lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta, int b,
+                            int hw, int c, int silu, float eps, lbx_stream stream) {
+  if (!x || !y || !stats || !gamma || !beta || c % 32 || c > 4096)
+    return set_err(LBX_E_CONFIG, "lbx_op_groupnorm: bad argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  float2* ss = nullptr;
+  if (cudaMallocAsync(&ss, (size_t)b * c * sizeof(float2), s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "cudaMallocAsync");
+  lbx::launch_gn_finalize(stats, gamma, beta, ss, b, c, (double)hw * (c / 32), eps, s);
+  lbx::launch_gn_apply(reinterpret_cast<const __half*>(x), reinterpret_cast<__half*>(y), ss, (long long)b * hw, hw, c,
+                       silu != 0, s);
+  cudaFreeAsync(ss, s);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+lbx_status lbx_op_gn_stats(const void* x, double* stats, int b, int hw, int c, lbx_stream stream) {
+  if (!x || !stats || c % 32 || c > 512 || b <= 0 || hw <= 0) return set_err(LBX_E_CONFIG, "lbx_op_gn_stats: bad argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(stats, 0, (size_t)b * 64 * sizeof(double), s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "memset");
+  lbx::launch_gn_stats(reinterpret_cast<const __half*>(x), stats, b, hw, c, s);
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+}  // extern "C"

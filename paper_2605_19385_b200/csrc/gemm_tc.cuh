@@ -1,0 +1,51 @@
+// Host-visible description of one tcgen05 implicit-GEMM launch (conv3x3 / conv1x1 / plain GEMM).
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lbx {
+
+enum GemmMode : int {
+  GEMM_PLAIN = 0,    // A = 2-D [M][K] (row stride lda), K-major
+  GEMM_CONV3X3 = 1,  // A = NHWC activation, 3x3 taps, pad 1 (TMA OOB zero-fill supplies the halo)
+  GEMM_SUBPIX = 2,   // nearest-2x upsample fused with 3x3 conv: 4 output phases, 2x2 taps each
+};
+
+// C[m, n] = alpha * row_scale[m] * sum_k A[m, k] B[n, k] + bias[n] + resid[m, n]     (fp32 math,
+// one rounding to fp16), optional GroupNorm(32) partial sums of the stored fp16 values.
+struct GemmArgs {
+  int mode = GEMM_PLAIN;
+  int M = 0, N = 0, K = 0;
+  // A operand
+  const __half* A = nullptr;
+  int lda = 0;                    // plain: row stride (elements)
+  int B_img = 0, H = 0, W = 0, C = 0;  // conv: NHWC input geometry (M = B_img*H*W, K = 9*C)
+  // B operand: weights [N][K] K-major (conv: K index = (ky*3+kx)*C + ci)
+  const __half* Bw = nullptr;
+  int ldb = 0;
+  // epilogue
+  __half* out = nullptr;
+  int ldo = 0;
+  const float* bias = nullptr;
+  const __half* resid = nullptr;
+  int ldr = 0;
+  const float* row_scale = nullptr;
+  float alpha = 1.f;
+  double* gn_stats = nullptr;     // [img][32][2] (sum, sumsq); zeroed by the caller
+  int gn_cpg = 0;                 // channels per group = N / 32
+  int rows_per_img = 0;           // M rows per image (GN image index = m / rows_per_img)
+};
+
+// Launch on `stream`.  Returns cudaSuccess or the launch error.  Chooses tile / CTA-pair config.
+cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg = 0, int force_bn = 0);
+
+// Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
+bool gemm_tc_prepare();
+
+// Number of SMs (cached) and the driver entry point used to encode TMA descriptors.
+int num_sms();
+bool tma_available();
+
+}  // namespace lbx

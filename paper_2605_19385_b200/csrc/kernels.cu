@@ -1,0 +1,336 @@
+// HBM-bound kernels of the reconstruction path (SURVEY.md 2.4 K1/K5/K7 and the attention glue).
+// All are vectorised (16-byte global accesses), grid-stride, sized in multiples of the SM count.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace lbx {
+
+static inline int grid_for(long long work, int threads, int per_sm = 8) {
+  long long g = (work + threads - 1) / threads;
+  long long cap = (long long)num_sms() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ----------------------------------------------------------------------------- latent prep
+__global__ void latent_prep_kernel(const __half* __restrict__ lat, __half* __restrict__ out, int n, int cl, int h,
+                                   int w, float scaling, float shift, const float* __restrict__ pq_w,
+                                   const float* __restrict__ pq_b) {
+  const long long pix = (long long)n * h * w;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < pix; p += (long long)gridDim.x * blockDim.x) {
+    const long long img = p / (h * w);
+    const int rem = (int)(p - img * h * w);
+    float z[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      if (c < cl) {
+        const float v = __half2float(lat[(img * cl + c) * h * w + rem]);
+        z[c] = __fadd_rn(__fdiv_rn(v, scaling), shift);
+      } else {
+        z[c] = 0.f;
+      }
+    }
+    if (pq_w) {
+      float y[16];
+#pragma unroll
+      for (int o = 0; o < 16; ++o) {
+        if (o < cl) {
+          float a = pq_b[o];
+          for (int c = 0; c < cl; ++c) a = fmaf(pq_w[o * cl + c], z[c], a);
+          y[o] = a;
+        } else {
+          y[o] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 16; ++o) z[o] = y[o];
+    }
+    uint4 pk[8];
+    __half2* h2 = reinterpret_cast<__half2*>(pk);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) h2[i] = __floats2half2_rn(z[2 * i], z[2 * i + 1]);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) pk[i] = make_uint4(0, 0, 0, 0);
+    uint4* o4 = reinterpret_cast<uint4*>(out + p * 64);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o4[i] = pk[i];
+  }
+}
+
+void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, int w, float scaling, float shift,
+                        const float* pq_w, const float* pq_b, cudaStream_t s) {
+  const long long pix = (long long)n * h * w;
+  latent_prep_kernel<<<grid_for(pix, 256), 256, 0, s>>>(lat, out, n, cl, h, w, scaling, shift, pq_w, pq_b);
+}
+
+// ----------------------------------------------------------------------------- GroupNorm
+__global__ void gn_finalize_kernel(const double* __restrict__ stats, const float* __restrict__ gamma,
+                                   const float* __restrict__ beta, float2* __restrict__ ss, int n, int C,
+                                   double count, float eps) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * C) return;
+  const int img = i / C, c = i - img * C;
+  const int g = c / (C / 32);
+  const double s = stats[(img * 32 + g) * 2], s2 = stats[(img * 32 + g) * 2 + 1];
+  const double mean = s / count;
+  double var = s2 / count - mean * mean;
+  if (var < 0) var = 0;
+  const double rstd = 1.0 / sqrt(var + (double)eps);
+  const double a = (double)gamma[c] * rstd;
+  ss[i] = make_float2((float)a, (float)((double)beta[c] - mean * a));
+}
+
+void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
+                        double count, float eps, cudaStream_t s) {
+  gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, count, eps);
+}
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+template <bool SILU>
+__global__ void gn_apply_kernel(const __half* x, __half* y, const float2* __restrict__ ss, long long vecs, int hw,
+                                int C) {
+  const int cv = C / 8;  // 16-byte vectors per pixel
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < vecs;
+       v += (long long)gridDim.x * blockDim.x) {
+    const long long pixel = v / cv;
+    const int c0 = (int)(v - pixel * cv) * 8;
+    const int img = (int)(pixel / hw);
+    const float2* sp = ss + (size_t)img * C + c0;
+    uint4 u = reinterpret_cast<const uint4*>(x)[v];
+    __half2* h2 = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __half22float2(h2[j]);
+      const float2 a = sp[2 * j], b = sp[2 * j + 1];
+      float y0 = fmaf(f.x, a.x, a.y), y1 = fmaf(f.y, b.x, b.y);
+      if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
+      h2[j] = __floats2half2_rn(y0, y1);
+    }
+    reinterpret_cast<uint4*>(y)[v] = u;
+  }
+}
+
+void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
+                     cudaStream_t s) {
+  const long long vecs = rows * (C / 8);
+  const int g = grid_for(vecs, 256, 16);
+  if (silu) gn_apply_kernel<true><<<g, 256, 0, s>>>(x, y, ss, vecs, hw, C);
+  else gn_apply_kernel<false><<<g, 256, 0, s>>>(x, y, ss, vecs, hw, C);
+}
+
+__global__ void gn_stats_kernel(const __half* __restrict__ x, double* stats, int hw, int C) {
+  __shared__ float acc[64];
+  const int img = blockIdx.y;
+  const int cpg = C / 32;
+  if (threadIdx.x < 64) acc[threadIdx.x] = 0.f;
+  __syncthreads();
+  const int cv = C / 8;
+  const long long vecs = (long long)hw * cv;
+  const uint4* xv = reinterpret_cast<const uint4*>(x + (size_t)img * hw * C);
+  float s[8], s2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) { s[j] = 0.f; s2[j] = 0.f; }
+  // each thread keeps a fixed channel octet so its partial sums stay per channel
+  const int stride = gridDim.x * blockDim.x;
+  int first = blockIdx.x * blockDim.x + threadIdx.x;
+  if (stride % cv == 0) {
+    const int c0 = (first % cv) * 8;
+    for (long long v = first; v < vecs; v += stride) {
+      uint4 u = xv[v];
+      const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __half22float2(h2[j]);
+        s[2 * j] += f.x; s2[2 * j] += f.x * f.x;
+        s[2 * j + 1] += f.y; s2[2 * j + 1] += f.y * f.y;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int g = (c0 + j) / cpg;
+      atomicAdd(&acc[2 * g], s[j]);
+      atomicAdd(&acc[2 * g + 1], s2[j]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 64) atomicAdd(&stats[(size_t)img * 64 + threadIdx.x], (double)acc[threadIdx.x]);
+}
+
+void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaStream_t s) {
+  // 256 threads x 64 blocks per image: stride 16384 vectors, a multiple of C/8 for C <= 512
+  dim3 grid(64, n);
+  gn_stats_kernel<<<grid, 256, 0, s>>>(x, stats, hw, C);
+}
+
+// ----------------------------------------------------------------------------- softmax
+// One 256-thread block per row; the row (<= 16384 fp16 = 32 KiB) is held in registers.
+template <int VPT>  // 16-byte vectors per thread
+__global__ void __launch_bounds__(256) softmax_rows_kernel(__half* S, float* row_scale, int cols) {
+  __shared__ float red[8];
+  __half* row = S + (size_t)blockIdx.x * cols;
+  const int nvec = cols / 8;
+  uint4 u[VPT];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = threadIdx.x + i * 256;
+    if (v < nvec) {
+      u[i] = reinterpret_cast<const uint4*>(row)[v];
+      const __half2* h2 = reinterpret_cast<const __half2*>(&u[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __half22float2(h2[j]);
+        mx = fmaxf(mx, fmaxf(f.x, f.y));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  __syncthreads();
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int v = threadIdx.x + i * 256;
+    if (v < nvec) {
+      __half2* h2 = reinterpret_cast<__half2*>(&u[i]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __half22float2(h2[j]);
+        const float e0 = __expf(f.x - mx), e1 = __expf(f.y - mx);
+        const __half2 e = __floats2half2_rn(e0, e1);
+        const float2 er = __half22float2(e);
+        sum += er.x + er.y;  // sum the values actually used by P*V
+        h2[j] = e;
+      }
+      reinterpret_cast<uint4*>(row)[v] = u[i];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    row_scale[blockIdx.x] = 1.0f / t;
+  }
+}
+
+void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s) {
+  const int nvec = cols / 8;
+  if (nvec <= 256 * 2) softmax_rows_kernel<2><<<rows, 256, 0, s>>>(S, row_scale, cols);
+  else if (nvec <= 256 * 4) softmax_rows_kernel<4><<<rows, 256, 0, s>>>(S, row_scale, cols);
+  else softmax_rows_kernel<8><<<rows, 256, 0, s>>>(S, row_scale, cols);
+}
+
+// ----------------------------------------------------------------------------- transpose
+__global__ void transpose_kernel(const __half* __restrict__ in, int ldi, __half* __restrict__ out, int ldo, int R,
+                                 int Cc) {
+  __shared__ __half tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < R && c < Cc) tile[i][threadIdx.x] = in[(size_t)r * ldi + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < R && c < Cc) out[(size_t)c * ldo + r] = tile[threadIdx.x][i];
+  }
+}
+
+void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, int Cc, cudaStream_t s) {
+  dim3 grid((Cc + 31) / 32, (R + 31) / 32);
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, ldi, out, ldo, R, Cc);
+}
+
+// ----------------------------------------------------------------------------- conv_out -> uint8
+// Tile: 8 rows x 32 columns of output pixels per 256-thread block (one pixel per thread).
+// Channels are streamed in chunks of 16 through a GN+SiLU-transformed halo tile in smem.
+constexpr int CO_TH = 8, CO_TW = 32, CO_CC = 16;
+
+__global__ void __launch_bounds__(256) conv_out_u8_kernel(const __half* __restrict__ x, const float2* __restrict__ ss,
+                                                          const float* __restrict__ w, const float* __restrict__ b,
+                                                          uint8_t* __restrict__ rgb, int H, int W) {
+  __shared__ float tile[CO_CC][CO_TH + 2][CO_TW + 2];
+  __shared__ float wsm[3][9][CO_CC];
+  const int img = blockIdx.z;
+  const int y0 = blockIdx.y * CO_TH, x0 = blockIdx.x * CO_TW;
+  const int ty = threadIdx.x / CO_TW, tx = threadIdx.x % CO_TW;
+  float acc0 = b[0], acc1 = b[1], acc2 = b[2];
+  const float2* ssi = ss + (size_t)img * 128;
+  for (int c0 = 0; c0 < 128; c0 += CO_CC) {
+    __syncthreads();
+    // halo tile (CO_TH+2) x (CO_TW+2) pixels x 16 channels; zero outside the image (conv padding
+    // applies after GN+SiLU, so padded taps contribute exactly 0)
+    for (int i = threadIdx.x; i < (CO_TH + 2) * (CO_TW + 2) * 2; i += 256) {
+      const int half_sel = i & 1;  // which 8-channel half of the chunk
+      const int pix = i >> 1;
+      const int py = pix / (CO_TW + 2), px = pix % (CO_TW + 2);
+      const int gy = y0 + py - 1, gx = x0 + px - 1;
+      float v[8];
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+        const uint4 u = *reinterpret_cast<const uint4*>(x + (((size_t)img * H + gy) * W + gx) * 128 + c0 + half_sel * 8);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __half22float2(h2[j]);
+          const int c = c0 + half_sel * 8 + 2 * j;
+          const float2 a = ssi[c], bb = ssi[c + 1];
+          v[2 * j] = silu_f(fmaf(f.x, a.x, a.y));
+          v[2 * j + 1] = silu_f(fmaf(f.y, bb.x, bb.y));
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) tile[half_sel * 8 + j][py][px] = v[j];
+    }
+    for (int i = threadIdx.x; i < 3 * 9 * CO_CC; i += 256) {
+      const int co = i / (9 * CO_CC), rem = i % (9 * CO_CC), tap = rem / CO_CC, ci = rem % CO_CC;
+      wsm[co][tap][ci] = w[(co * 9 + tap) * 128 + c0 + ci];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx)
+#pragma unroll
+        for (int ci = 0; ci < CO_CC; ++ci) {
+          const float v = tile[ci][ty + ky][tx + kx];
+          acc0 = fmaf(v, wsm[0][ky * 3 + kx][ci], acc0);
+          acc1 = fmaf(v, wsm[1][ky * 3 + kx][ci], acc1);
+          acc2 = fmaf(v, wsm[2][ky * 3 + kx][ci], acc2);
+        }
+  }
+  const int gy = y0 + ty, gx = x0 + tx;
+  if (gy < H && gx < W) {
+    float a[3] = {acc0, acc1, acc2};
+    uint8_t* o = rgb + (((size_t)img * H + gy) * W + gx) * 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      float t = __fadd_rn(__fmul_rn(a[k], 0.5f), 0.5f);
+      t = fminf(fmaxf(t, 0.f), 1.f);
+      o[k] = (uint8_t)__float2int_rn(__fmul_rn(t, 255.f));  // round-half-even
+    }
+  }
+}
+
+void launch_conv_out_u8(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb, int n,
+                        int H, int W, cudaStream_t s) {
+  dim3 grid((W + CO_TW - 1) / CO_TW, (H + CO_TH - 1) / CO_TH, n);
+  conv_out_u8_kernel<<<grid, 256, 0, s>>>(x, ss, w, b, rgb, H, W);
+}
+
+}  // namespace lbx

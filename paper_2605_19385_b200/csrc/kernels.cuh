@@ -1,0 +1,44 @@
+// Launch wrappers for the HBM-bound kernels of the reconstruction path.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace lbx {
+
+// fp16 NCHW latents -> prescale z/scaling + shift -> [post_quant 1x1, fp32] -> fp16 NHWC, channels
+// zero-padded to 64 (conv_in then runs as an ordinary tcgen05 conv with C = 64).
+void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, int w, float scaling, float shift,
+                        const float* pq_w, const float* pq_b, cudaStream_t s);
+
+// GroupNorm-32 finalize: stats [n][32][2] (sum, sumsq of `count` values per group) -> per-channel
+// affine ss[n][C] = (gamma*rstd, beta - mean*gamma*rstd).
+void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
+                        double count, float eps, cudaStream_t s);
+
+// y = act(x * ss.x + ss.y), x/y fp16 [n*hw][C] (y may alias x), act = SiLU if silu else identity.
+void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
+                     cudaStream_t s);
+
+// Row softmax numerator in place: P = exp(S - rowmax(S)) (fp16), row_scale = 1 / sum(P) (fp32).
+void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s);
+
+// out[c][r] = in[r][c] for an R x Cc block with input row stride ldi and output row stride ldo.
+void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, int Cc, cudaStream_t s);
+
+// Fused tail: GroupNorm(128) + SiLU -> conv3x3 128->3 (+bias) -> (x/2+0.5).clamp(0,1)*255 ->
+// round-half-even -> uint8 HWC.  x fp16 NHWC [n][H][W][128]; w fp32 [3][3][3][128]; rgb [n][H][W][3].
+void launch_conv_out_u8(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb, int n,
+                        int H, int W, cudaStream_t s);
+
+// GroupNorm-32 statistics (sum, sumsq per image and group) of x [n][hw][C] fp16 into stats
+// [n][32][2] (accumulated; zero it first).  Standalone form of what the conv epilogue fuses.
+void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaStream_t s);
+
+// LBLP v1 device unpack (include/lbx/lblp.h).  `blobs` is one device buffer holding n blobs at
+// byte offsets `offs[i]` (device array); output fp16 NCHW [n][C][H][W].  Any malformed blob sets
+// *err (device int) to a nonzero code; the output of that latent is then unspecified (zeros).
+void launch_lblp_unpack(const uint8_t* blobs, const unsigned long long* offs, const unsigned int* sizes, int n,
+                        int C, int H, int W, __half* out, int* err, cudaStream_t s);
+
+}  // namespace lbx

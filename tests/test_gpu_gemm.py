@@ -1,0 +1,140 @@
+"""Op-level parity of the tcgen05 implicit-GEMM kernel (csrc/gemm_tc.cu) through the C ABI
+(lbx_op_gemm), against plain PyTorch fp32 references of the same op (TF32 off).
+
+Tolerance: outputs are fp16 (relative precision 2^-11); fp32 accumulation.  We require
+|got - ref| <= 2e-3 * max|ref| + 1e-3 elementwise (written per test below).
+"""
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+torch.backends.cuda.matmul.allow_tf32 = False
+torch.backends.cudnn.allow_tf32 = False
+
+
+def _close(got, ref, rel=2e-3, abs_=1e-3):
+    got = got.float()
+    ref = ref.float()
+    tol = rel * ref.abs().max().item() + abs_
+    err = (got - ref).abs().max().item()
+    assert err <= tol, f"max err {err} > tol {tol}"
+
+
+def _rand(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return (torch.randn(*shape, generator=g) * scale).half().cuda()
+
+
+@pytest.mark.parametrize("cg,bn", [(1, 128), (1, 256), (2, 128), (2, 256)])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 512, 512), (1024, 256, 1152)])
+def test_plain_gemm(lbx, cg, bn, M, N, K):
+    if N % bn:
+        pytest.skip("N not a multiple of the tile")
+    A = _rand(M, K, seed=1)
+    B = _rand(N, K, scale=K ** -0.5, seed=2)
+    out = torch.empty(M, N, dtype=torch.half, device="cuda")
+    lbx.op_gemm(0, M, N, K, A.data_ptr(), K, B.data_ptr(), K, out.data_ptr(), N, cta_group=cg, bn=bn)
+    torch.cuda.synchronize()
+    _close(out, A.float() @ B.float().t())
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_gemm_epilogue(lbx, cg):
+    M, N, K = 512, 256, 256
+    A = _rand(M, K, seed=3)
+    B = _rand(N, K, scale=K ** -0.5, seed=4)
+    bias = torch.randn(N, device="cuda")
+    resid = _rand(M, N, seed=5)
+    rs = torch.rand(M, device="cuda") + 0.5
+    out = torch.empty(M, N, dtype=torch.half, device="cuda")
+    lbx.op_gemm(0, M, N, K, A.data_ptr(), K, B.data_ptr(), K, out.data_ptr(), N, bias=bias.data_ptr(),
+                resid=resid.data_ptr(), ldr=N, row_scale=rs.data_ptr(), alpha=0.5, cta_group=cg)
+    torch.cuda.synchronize()
+    ref = 0.5 * rs[:, None] * (A.float() @ B.float().t()) + bias[None, :] + resid.float()
+    _close(out, ref)
+
+
+def test_gemm_strided_views(lbx):
+    """Q K^T on column views of a [L, 1536] QKV buffer (row stride 1536), as the attention uses."""
+    L = 512
+    qkv = _rand(L, 1536, seed=6)
+    S = torch.empty(L, L, dtype=torch.half, device="cuda")
+    q, k = qkv[:, :512], qkv[:, 512:1024]
+    lbx.op_gemm(0, L, L, 512, q.data_ptr(), 1536, k.data_ptr(), 1536, S.data_ptr(), L, alpha=512 ** -0.5)
+    torch.cuda.synchronize()
+    _close(S, (q.float() @ k.float().t()) * 512 ** -0.5)
+
+
+def _conv_ref(x_nhwc, w_oihw, bias):
+    x = x_nhwc.permute(0, 3, 1, 2).float()
+    y = F.conv2d(x, w_oihw.float(), bias, padding=1)
+    return y.permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("b,h,w,c,n", [(1, 64, 64, 64, 128), (2, 64, 64, 128, 256), (1, 128, 128, 64, 256),
+                                       (1, 16, 256, 64, 128)])
+def test_conv3x3(lbx, cg, b, h, w, c, n):
+    x = _rand(b, h, w, c, seed=7)
+    wt = _rand(n, c, 3, 3, scale=(9 * c) ** -0.5, seed=8)
+    bias = torch.randn(n, device="cuda")
+    wk = wt.permute(0, 2, 3, 1).contiguous()  # [N][ky][kx][C]
+    out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
+    lbx.op_gemm(1, b * h * w, n, 9 * c, x.data_ptr(), 0, wk.data_ptr(), 9 * c, out.data_ptr(), n, b=b, h=h, w=w,
+                c=c, bias=bias.data_ptr(), cta_group=cg)
+    torch.cuda.synchronize()
+    _close(out, _conv_ref(x, wt, bias))
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_conv3x3_resid_gnstats(lbx, cg):
+    b, h, w, c, n = 2, 64, 64, 128, 128
+    x = _rand(b, h, w, c, seed=9)
+    wt = _rand(n, c, 3, 3, scale=(9 * c) ** -0.5, seed=10)
+    wk = wt.permute(0, 2, 3, 1).contiguous()
+    resid = _rand(b, h, w, n, seed=11)
+    out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
+    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    lbx.op_gemm(1, b * h * w, n, 9 * c, x.data_ptr(), 0, wk.data_ptr(), 9 * c, out.data_ptr(), n, b=b, h=h, w=w,
+                c=c, resid=resid.data_ptr(), ldr=n, gn_stats=stats.data_ptr(), cta_group=cg)
+    torch.cuda.synchronize()
+    _close(out, _conv_ref(x, wt, None) + resid.float())
+    # GN partial sums are of the stored fp16 values: compare with a float64 reduction of `out`
+    o = out.double().reshape(b, h * w, 32, n // 32)
+    ref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
+    torch.testing.assert_close(stats, ref, rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("b,h,w,c", [(1, 64, 64, 128), (2, 32, 128, 128), (1, 16, 256, 256)])
+def test_subpixel_upsample_conv(lbx, cg, b, h, w, c):
+    """nearest-2x upsample + conv3x3 == 4 sub-pixel 2x2 convs on the low-res grid."""
+    x = _rand(b, h, w, c, seed=12)
+    wt = _rand(c, c, 3, 3, scale=(9 * c) ** -0.5, seed=13)
+    bias = torch.randn(c, device="cuda")
+    w4 = torch.from_numpy(lbx.subpixel_weights(wt.float().permute(0, 2, 3, 1).cpu().numpy()).copy()).cuda()
+    out = torch.empty(b, 2 * h, 2 * w, c, dtype=torch.half, device="cuda")
+    lbx.op_gemm(2, b * h * w, c, 4 * c, x.data_ptr(), 0, w4.data_ptr(), 4 * c, out.data_ptr(), c, b=b, h=h, w=w,
+                c=c, bias=bias.data_ptr(), cta_group=cg)
+    torch.cuda.synchronize()
+    up = F.interpolate(x.permute(0, 3, 1, 2).float(), scale_factor=2.0, mode="nearest")
+    ref = F.conv2d(up, wt.float(), bias, padding=1).permute(0, 2, 3, 1)
+    # folded weights are re-rounded to fp16: allow a slightly wider band
+    _close(out, ref, rel=4e-3)
+
+
+def test_gn_stats_and_apply(lbx):
+    b, hw, c = 2, 4096, 256
+    x = _rand(b, hw, c, seed=14) * 2 + 0.5
+    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    lbx.op_gn_stats(x.data_ptr(), stats.data_ptr(), b, hw, c)
+    gamma = torch.rand(c, device="cuda") + 0.5
+    beta = torch.randn(c, device="cuda") * 0.1
+    y = torch.empty_like(x)
+    lbx.op_groupnorm(x.data_ptr(), y.data_ptr(), stats.data_ptr(), gamma.data_ptr(), beta.data_ptr(), b, hw, c)
+    torch.cuda.synchronize()
+    ref = F.silu(F.group_norm(x.float().permute(0, 2, 1), 32, gamma, beta, 1e-6)).permute(0, 2, 1)
+    _close(y, ref, rel=2e-3, abs_=2e-3)

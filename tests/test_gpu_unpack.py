@@ -1,0 +1,82 @@
+"""K1 parity: GPU LBLP unpack (csrc/unpack.cu) bit-exact against the C oracle (oracle/lblp_ref.c),
+through the C ABI (lbx_unpack / lbx_reconstruct).  Edge cases: +-0, subnormals, +-inf, NaN payloads,
+all-equal rows (width 0), maximum deltas (width 16), malformed blobs."""
+import numpy as np
+import pytest
+
+import lblp
+import weights_ref
+
+pytestmark = pytest.mark.gpu
+
+SPECIAL = np.array([0x0000, 0x8000, 0x0001, 0x8001, 0x03FF, 0x83FF, 0x0400, 0x7BFF, 0xFBFF, 0x7C00, 0xFC00,
+                    0x7E00, 0x7C01, 0xFE01, 0x3C00, 0xBC00], dtype=np.uint16)
+
+
+def _gpu_unpack(lbx, dec, blobs):
+    import torch
+    n = len(blobs)
+    out = torch.zeros((n, dec.c, dec.h, dec.w), dtype=torch.int16, device="cuda")
+    dec.unpack_ptr(blobs, out.data_ptr())
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint16)
+
+
+def _latents_with_specials(seed):
+    z = weights_ref.make_latents("sd3", 3, 64, 64, seed=seed).view(np.uint16).copy()
+    z[0, 0, 0, :] = np.resize(SPECIAL, 64)                     # special values
+    z[0, 1, :, :] = 0x3C00                                     # constant plane -> width-0 mini-blocks
+    z[0, 2, 0, :] = np.where(np.arange(64) % 2, 0xFC00, 0x7C00)  # alternating +-inf -> width-16
+    z[1, 3, 5, :] = np.random.default_rng(seed).integers(0, 65536, 64, dtype=np.uint16)  # random bit patterns
+    return z.view(np.float16)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_unpack_bit_exact_vs_oracle(lbx, mode):
+    z = _latents_with_specials(21)
+    if mode == 2:  # q8 is lossy: specials would blow the per-channel range; use finite data
+        z = weights_ref.make_latents("sd3", 3, 64, 64, seed=22)
+    dec = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=3)
+    blobs = [lblp.encode(z[i], mode) for i in range(3)]
+    got = _gpu_unpack(lbx, dec, blobs)
+    ref = np.stack([lblp.decode(b, 16, 64, 64).view(np.uint16) for b in blobs])
+    assert np.array_equal(got, ref)
+    if mode in (0, 1):
+        assert np.array_equal(got, z.view(np.uint16))  # lossless round trip
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_unpack_product_packer_blobs(lbx, mode):
+    """Product packer (lbx_pack) -> GPU unpack == oracle decode of the same bytes, at config-3 shape."""
+    z = weights_ref.make_latents("sd3", 4, 128, 128, seed=3, smooth=True)
+    dec = lbx.Decoder("sd3", (128, 128), seed=0, max_batch=4)
+    blobs = [lbx.pack(z[i], mode) for i in range(4)]
+    got = _gpu_unpack(lbx, dec, blobs)
+    ref = np.stack([lblp.decode(b, 16, 128, 128).view(np.uint16) for b in blobs])
+    assert np.array_equal(got, ref)
+
+
+def test_malformed_blob_rejected(lbx):
+    z = weights_ref.make_latents("sd3", 1, 64, 64, seed=1)
+    dec = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=1)
+    good = lblp.encode(z[0], 1)
+    bad = bytearray(good)
+    bad[0] = ord("X")
+    with pytest.raises(lbx.LbxError) as e:
+        dec.reconstruct([bytes(bad)])
+    assert e.value.status == lbx.E_FORMAT
+    trunc = good[:-8]
+    with pytest.raises(lbx.LbxError) as e:
+        dec.reconstruct([trunc])
+    assert e.value.status == lbx.E_FORMAT
+    # the decoder stays usable after a rejected call
+    rgb = dec.reconstruct([good])
+    assert rgb.shape == (1, 512, 512, 3)
+
+
+def test_reconstruct_from_blobs_equals_from_latents(lbx):
+    z = weights_ref.make_latents("sd3", 2, 64, 64, seed=4)
+    dec = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=2)
+    a = dec.reconstruct([lbx.pack(z[i], 1) for i in range(2)])
+    b = dec.reconstruct_latents(z)
+    assert np.array_equal(a, b)
