@@ -96,6 +96,23 @@ lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, ui
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* lbx_last_error(void);
 
+/* ------------------------------------------------------------------ profiling
+ * Run one decode of n latents (internal buffers) eagerly with a CUDA event after every launch and
+ * report per-launch device time.  flops = executed tensor FLOPs, algo_flops = the standard
+ * algorithmic FLOPs the launch stands for (a sub-pixel launch stands for nearest-2x + conv3x3),
+ * bytes = algorithmic HBM bytes.  Fills up to cap entries, *count = entries written. */
+typedef struct {
+  char name[96];
+  double ms;
+  double flops;
+  double algo_flops;
+  double bytes;
+} lbx_prof_entry;
+lbx_status lbx_profile(lbx_decoder* dec, uint32_t n, lbx_prof_entry* out, int cap, int* count);
+
+/* Kernel launches in one decode of batch n (after the first lbx_decode/reconstruct of that n), or -1. */
+int lbx_launch_count(lbx_decoder* dec, uint32_t n);
+
 /* ------------------------------------------------------------------ diagnostics / op-level entry
  * Individual kernels of the path, for op-level parity tests and benchmarks.  Device pointers,
  * fp16 = uint16 storage.  All asynchronous on `stream`. */

@@ -27,7 +27,7 @@ _STATUS = {1: "LBX_E_RUNTIME", 2: "LBX_E_CONFIG", 3: "LBX_E_CUDA", 4: "LBX_E_FOR
 SYMBOLS = [
     "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
-    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats",
+    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count",
 ]
 
 
@@ -37,6 +37,11 @@ class LbxError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{_STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 96), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
+                ("algo_flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
 class _Desc(ctypes.Structure):
@@ -81,6 +86,8 @@ def lib() -> ctypes.CDLL:
     L.lbx_subpixel_weights.argtypes = [vp, i32, i32, vp]
     L.lbx_op_groupnorm.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, ctypes.c_float, vp]
     L.lbx_op_gn_stats.argtypes = [vp, vp, i32, i32, i32, vp]
+    L.lbx_profile.argtypes = [vp, u32, ctypes.POINTER(ProfEntry), i32, ctypes.POINTER(i32)]
+    L.lbx_launch_count.argtypes = [vp, u32]
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -163,14 +170,26 @@ class Decoder:
         arr, sizes, keep = _blob_arrays(blobs)
         check(lib().lbx_unpack(self._h, arr, sizes, len(blobs), latents_dev, stream or None))
 
+    def profile(self, n: int):
+        """Per-launch device times of one eager decode of n latents: list of dicts."""
+        cap = 4096
+        arr = (ProfEntry * cap)()
+        cnt = ctypes.c_int(0)
+        check(lib().lbx_profile(self._h, n, arr, cap, ctypes.byref(cnt)))
+        return [{"name": arr[i].name.decode(), "ms": arr[i].ms, "flops": arr[i].flops,
+                 "algo_flops": arr[i].algo_flops, "bytes": arr[i].bytes} for i in range(cnt.value)]
+
+    def launch_count(self, n: int) -> int:
+        return int(lib().lbx_launch_count(self._h, n))
+
     # -- host entry points ---------------------------------------------------------------------
-    def reconstruct(self, blobs, out: np.ndarray | None = None) -> np.ndarray:
-        """Packed LBLP blobs (host) -> uint8 RGB (n, 8h, 8w, 3)."""
+    def reconstruct(self, blobs, out: np.ndarray | None = None, stream: int = 0) -> np.ndarray:
+        """Packed LBLP blobs (host) -> uint8 RGB (n, 8h, 8w, 3).  Synchronous."""
         n = len(blobs)
         if out is None:
             out = np.empty((n, 8 * self.h, 8 * self.w, 3), dtype=np.uint8)
         arr, sizes, keep = _blob_arrays(blobs)
-        check(lib().lbx_reconstruct(self._h, arr, sizes, n, out.ctypes.data, None))
+        check(lib().lbx_reconstruct(self._h, arr, sizes, n, out.ctypes.data, stream or None))
         return out
 
     def reconstruct_latents(self, latents: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:

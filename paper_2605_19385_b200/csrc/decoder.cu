@@ -106,7 +106,13 @@ class Decoder {
   int* err_host = nullptr;
 
   std::map<std::tuple<int, const void*, const void*>, cudaGraphExec_t> graphs;
-  int launches_per_decode = 0;
+  std::map<int, int> launch_counts;
+  struct ProfRec {
+    std::string name;
+    double flops, algo_flops, bytes;
+    cudaEvent_t ev;
+  };
+  std::vector<ProfRec>* prof = nullptr;
 
   ~Decoder() { release(); }
 
@@ -372,8 +378,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   int site = 0;
   const size_t site_stride = (size_t)max_batch * 64;
   auto site_ptr = [&](int i) { return stats + (size_t)i * site_stride; };
-  auto chk = [&](cudaError_t e, const char* what) -> lbx_status {
-    if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  auto chk = [&](cudaError_t e, const std::string& what) -> lbx_status {
+    if (e != cudaSuccess) return set_err(LBX_E_CUDA, what + ": " + cudaGetErrorString(e));
     return LBX_OK;
   };
 #define LBX_STEP(expr, what)                       \
@@ -381,24 +387,51 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     lbx_status _s = chk((expr), what);             \
     if (_s != LBX_OK) return _s;                   \
   } while (0)
-#define LBX_LAUNCH(stmt, what)                     \
+  auto mark = [&](const std::string& name, double flops, double algo, double bytes) {
+    if (!prof) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    prof->push_back({name, flops, algo, bytes, e});
+  };
+#define LBX_LAUNCH(stmt, what, bytes)              \
   do {                                             \
     stmt;                                          \
     ++launches;                                    \
     LBX_STEP(cudaPeekAtLastError(), what);         \
+    mark(what, 0.0, 0.0, (double)(bytes));         \
   } while (0)
 
   __half* X_ = X;
   __half* A_ = A;
+  if (prof) mark("start", 0, 0, 0);
   LBX_STEP(cudaMemsetAsync(stats, 0, (size_t)kMaxSites * site_stride * 8, s), "memset stats");
 
   auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
     ++launches;
-    return chk(gemm_tc_launch(ga, s), what);
+    lbx_status e = chk(gemm_tc_launch(ga, s), what);
+    if (e == LBX_OK && prof) {
+      const double fl = 2.0 * ga.M * (double)ga.N * ga.K;
+      // algorithmic (standard) FLOPs: the sub-pixel form stands for nearest-2x + a full 3x3 conv
+      const double algo = ga.mode == GEMM_SUBPIX ? 2.0 * 4.0 * ga.M * (double)ga.N * 9.0 * ga.C : fl;
+      char nm[160];
+      if (ga.mode == GEMM_PLAIN)
+        snprintf(nm, sizeof nm, "%s gemm M%d N%d K%d", what, ga.M, ga.N, ga.K);
+      else
+        snprintf(nm, sizeof nm, "%s %s c%d->%d @%dx%d", what, ga.mode == GEMM_CONV3X3 ? "conv3x3" : "subpix2x2",
+                 ga.C, ga.N, ga.mode == GEMM_SUBPIX ? 2 * ga.H : ga.H, ga.mode == GEMM_SUBPIX ? 2 * ga.W : ga.W);
+      const double by = 2.0 * ((double)ga.M * ga.K / (ga.mode == GEMM_PLAIN ? 1 : (ga.mode == GEMM_CONV3X3 ? 9 : 4)) +
+                               (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1) +
+                               (double)ga.M * ga.N * (ga.mode == GEMM_SUBPIX ? 4 : 1) * (ga.resid ? 2 : 1));
+      mark(nm, fl, algo, by);
+    }
+    return e;
   };
   auto gn = [&](int st_site, const NormW& nw, const __half* x, __half* y, int C, int hw, bool silu) -> lbx_status {
-    LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)hw * (C / 32), 1e-6f, s), "gn_finalize");
-    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, s), "gn_apply");
+    LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)hw * (C / 32), 1e-6f, s), "gn_finalize", n * C * 8.0);
+    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, s),
+               std::string(silu ? "gn_apply_silu c" : "gn_apply c") + std::to_string(C) + " hw" + std::to_string(hw),
+               4.0 * n * (double)hw * C);
     return LBX_OK;
   };
   auto conv3 = [&](const __half* in, int H, int W, int C, const ConvW& cw, int N, __half* out, const __half* resid,
@@ -417,7 +450,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   lbx_status st;
 
   // prep + conv_in
-  LBX_LAUNCH(launch_latent_prep(lat_in, A_, n, cl, h, w, fi.scaling, fi.shift, pq_w, pq_b, s), "latent_prep");
+  LBX_LAUNCH(launch_latent_prep(lat_in, A_, n, cl, h, w, fi.scaling, fi.shift, pq_w, pq_b, s), "latent_prep",
+             2.0 * n * h * w * (cl + 64));
   int x_site = site++;
   if ((st = conv3(A_, h, w, 64, conv_in, 512, X_, nullptr, x_site, "conv_in")) != LBX_OK) return st;
 
@@ -466,8 +500,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       sq.out = S; sq.ldo = L;
       sq.alpha = 1.0f / std::sqrt(512.0f);
       if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
-      LBX_LAUNCH(launch_softmax_rows(S, rowscale, L, L, s), "attn.softmax");
-      LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose");
+      LBX_LAUNCH(launch_softmax_rows(S, rowscale, L, L, s), "attn.softmax", 4.0 * L * (double)L);
+      LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose", 4.0 * L * 512.0);
       GemmArgs pv;
       pv.mode = GEMM_PLAIN;
       pv.M = L; pv.N = 512; pv.K = L;
@@ -514,10 +548,11 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   }
   // tail
   LBX_LAUNCH(launch_gn_finalize(site_ptr(x_site), norm_out.g, norm_out.b, ss, n, 128, (double)H * W * 4, 1e-6f, s),
-             "norm_out.finalize");
-  LBX_LAUNCH(launch_conv_out_u8(X_, ss, wout, bout, rgb_out, n, H, W, s), "conv_out_u8");
+             "norm_out.finalize", n * 128 * 8.0);
+  LBX_LAUNCH(launch_conv_out_u8(X_, ss, wout, bout, rgb_out, n, H, W, s), "conv_out_u8",
+             (double)n * H * W * (128 * 2 + 3));
   if (site > kMaxSites) return set_err(LBX_E_RUNTIME, "too many GroupNorm sites");
-  if (counting) launches_per_decode = launches;
+  if (counting) launch_counts[n] = launches;
   return LBX_OK;
 #undef LBX_STEP
 #undef LBX_LAUNCH
@@ -774,7 +809,7 @@ lbx_status lbx_subpixel_weights(const float* w3, int N, int C, uint16_t* out) {
 
 lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta, int b,
                             int hw, int c, int silu, float eps, lbx_stream stream) {
-  if (!x || !y || !stats || !gamma || !beta || c % 32 || c > 4096)
+  if (!x || !y || !stats || !gamma || !beta || !(c == 128 || c == 256 || c == 512))
     return set_err(LBX_E_CONFIG, "lbx_op_groupnorm: bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   float2* ss = nullptr;
@@ -798,6 +833,44 @@ lbx_status lbx_op_gn_stats(const void* x, double* stats, int b, int hw, int c, l
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));
   return LBX_OK;
+}
+
+lbx_status lbx_profile(lbx_decoder* dec, uint32_t n, lbx_prof_entry* out, int cap, int* count) {
+  if (!dec || !out || !count) return set_err(LBX_E_CONFIG, "lbx_profile: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0 || (int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: must be in [1, desc.max_batch]");
+  cudaSetDevice(d.desc.device);
+  std::vector<Decoder::ProfRec> recs;
+  d.prof = &recs;
+  lbx_status st = d.plan((int)n, d.lat, d.rgb, d.stream, false);
+  d.prof = nullptr;
+  cudaError_t e = cudaStreamSynchronize(d.stream);
+  int k = 0;
+  for (size_t i = 1; i < recs.size(); ++i) {
+    if (st == LBX_OK && e == cudaSuccess && k < cap) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, recs[i - 1].ev, recs[i].ev);
+      lbx_prof_entry& o = out[k++];
+      std::memset(&o, 0, sizeof o);
+      std::snprintf(o.name, sizeof o.name, "%s", recs[i].name.c_str());
+      o.ms = ms;
+      o.flops = recs[i].flops;
+      o.algo_flops = recs[i].algo_flops;
+      o.bytes = recs[i].bytes;
+    }
+  }
+  for (auto& r : recs) cudaEventDestroy(r.ev);
+  *count = k;
+  if (st != LBX_OK) return st;
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("lbx_profile: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+int lbx_launch_count(lbx_decoder* dec, uint32_t n) {
+  if (!dec) return -1;
+  auto it = dec->d.launch_counts.find((int)n);
+  return it == dec->d.launch_counts.end() ? -1 : it->second;
 }
 
 }  // extern "C"

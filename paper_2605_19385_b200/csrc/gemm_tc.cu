@@ -53,7 +53,7 @@ struct Cfg {
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;           // double-buffered fp32 accumulator
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
-  static constexpr int THREADS = 192;
+  static constexpr int THREADS = 320;  // 2 non-epilogue + 8 epilogue warps
   static constexpr uint32_t IDESC = ptx::idesc_f16(128 * CG, BN);
   static constexpr uint32_t TX_BYTES = CG * STAGE_BYTES;  // bytes landing per stage per tile (pair)
 };
@@ -70,8 +70,48 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile
   }
 }
 
+// Per-chunk GroupNorm partials.  pk holds this lane's 32 stored fp16 values (one pixel, 32
+// consecutive channels) as half2 pairs.  NV = 2 * groups-per-chunk values per lane (group sums,
+// then group sums of squares) are reduce-scattered across the warp with NV + log2(32/NV)
+// shuffles (instead of 5 * NV for a butterfly per value): lane L ends up owning the warp total
+// of value index (L >> (5 - log2 NV)) & (NV - 1).
+template <int NV>
+__device__ __forceinline__ float chunk_group_stats(const uint32_t (&pk)[16], uint32_t lane) {
+  constexpr int G = NV / 2, H2 = 16 / G;  // half2 words per group
+  constexpr int LG = NV == 16 ? 4 : (NV == 8 ? 3 : 2);
+  float v[NV];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float s = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < H2; ++i) {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&pk[g * H2 + i]));
+      s += f.x + f.y;
+      s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+    }
+    v[g] = s;
+    v[G + g] = s2;
+  }
+#pragma unroll
+  for (int lvl = 0; lvl < LG; ++lvl) {
+    const int cnt = NV >> lvl;
+    const int o = 16 >> lvl;
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < cnt / 2; ++i) {
+      const float send = upper ? v[i] : v[i + cnt / 2];
+      const float keep = upper ? v[i + cnt / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  float x = v[0];
+#pragma unroll
+  for (int o = 16 >> LG; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
 template <int BN, int CG>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const KParams p) {
   using C = Cfg<BN, CG>;
@@ -101,7 +141,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4 * CG);
+      ptx::mbar_init(&tempty[i], 8 * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -187,9 +227,39 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    // Two warps per TMEM lane quarter; warp half `hsel` takes the even/odd 32-column chunks.
+    const uint32_t q = warp & 3;
+    const int hsel = (int)(warp - 2) >> 2;
     const int row = q * 32 + lane;
+    constexpr int NCH = BN / 64;  // chunks per warp per tile
+    // GroupNorm partials: after the per-chunk reduce-scatter each lane owns one (group, sum|sumsq)
+    // value per chunk; lanes accumulate those across tiles in fp64 registers and flush with one
+    // atomic per owned value only when the (image, n-tile) changes -- not once per tile.
+    double gacc[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) gacc[j] = 0.0;
+    int g_img = -1, g_ntile = -1;
+    const int nv = p.gn_stats ? 64 / p.gn_cpg : 0;  // values per chunk: 2 * groups-per-chunk
+    const int lg = nv == 16 ? 4 : (nv == 8 ? 3 : 2);
+    const int own = nv ? (int)(lane >> (5 - lg)) & (nv - 1) : 0;
+    const bool rep = nv ? (lane & ((1u << (5 - lg)) - 1u)) == 0 : false;
+    auto flush = [&]() {
+      if (g_img < 0) return;
+      if (rep) {
+        const int gpc = nv >> 1;  // groups per chunk
+        const int kind = own >= gpc;
+        const int g_in = own - kind * gpc;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          const int c = hsel + 2 * j;
+          const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + g_in;
+          atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, gacc[j]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) gacc[j] = 0.0;
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster_id; t < p.tiles; t += nclusters) {
@@ -197,7 +267,6 @@ __global__ void __launch_bounds__(192, 1)
       tile_coords(p, t, m_tile, n_tile, ph);
       const int m = m_tile * (128 * CG) + rank * 128 + row;
       const int n0 = n_tile * BN;
-      // destination row for this pixel
       long long orow = m;
       if (p.mode == GEMM_SUBPIX) {
         const int hw = p.H * p.W;
@@ -207,80 +276,68 @@ __global__ void __launch_bounds__(192, 1)
         orow = ((long long)img * (2 * p.H) + (2 * i + (ph >> 1))) * (2 * p.W) + (2 * j + (ph & 1));
       }
       const float rs = p.alpha * (p.row_scale ? p.row_scale[m] : 1.f);
-      const int img_idx = p.gn_stats ? m / p.rows_per_img : 0;
+      if (p.gn_stats) {
+        const int img = m / p.rows_per_img;  // warp-uniform: 32-row slices never straddle images
+        if (img != g_img || n_tile != g_ntile) {
+          flush();
+          g_img = img;
+          g_ntile = n_tile;
+        }
+      }
 
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) {
+        const int c = hsel + 2 * j;
+        const int n = n0 + c * 32;
         uint32_t r[32];
         ptx::tmem_ld32(t_row + c * 32, r);
+        uint4 rr[4];
+        if (p.resid) {  // in flight while the TMEM load completes
+          const uint4* rp = reinterpret_cast<const uint4*>(p.resid + orow * p.ldr + n);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rr[i] = rp[i];
+        }
         ptx::tmem_ld_wait();
-        const int n = n0 + c * 32;
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * rs;
         if (p.bias) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = *reinterpret_cast<const float4*>(p.bias + n + i);
+            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n + i));
             v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
           }
         }
         if (p.resid) {
-          const uint4* rp = reinterpret_cast<const uint4*>(p.resid + orow * p.ldr + n);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            uint4 u = rp[i];
-            const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+            const uint32_t w4[4] = {rr[i].x, rr[i].y, rr[i].z, rr[i].w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              float2 f = __half22float2(h2[j]);
-              v[i * 8 + 2 * j] += f.x;
-              v[i * 8 + 2 * j + 1] += f.y;
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
+              v[i * 8 + 2 * k] += f.x;
+              v[i * 8 + 2 * k + 1] += f.y;
             }
           }
         }
-        uint4 packed[4];
-        __half2* ph2 = reinterpret_cast<__half2*>(packed);
+        uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) ph2[i] = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+        for (int i = 0; i < 16; ++i) {
+          const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          pk[i] = *reinterpret_cast<const uint32_t*>(&h);
+        }
         uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) op[i] = packed[i];
+        for (int i = 0; i < 4; ++i) op[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
         if (p.gn_stats) {
-          // partial sums over 4-channel quads of the *stored* values, then combine per group
-          float s[8], s2[8];
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-            s[g] = 0.f; s2[g] = 0.f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float x = __half2float(reinterpret_cast<__half*>(packed)[g * 4 + i]);
-              s[g] += x;
-              s2[g] += x * x;
-            }
-          }
-#pragma unroll
-          for (int g = 0; g < 8; ++g) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-              s[g] += __shfl_xor_sync(0xffffffffu, s[g], o);
-              s2[g] += __shfl_xor_sync(0xffffffffu, s2[g], o);
-            }
-          }
-          if (lane == 0) {
-            const int quads = p.gn_cpg >> 2;  // 1, 2 or 4 quads per group
-            double* st = p.gn_stats + ((size_t)img_idx * 32 + n / p.gn_cpg) * 2;
-            for (int g0 = 0; g0 < 8; g0 += quads) {
-              float a = 0.f, b = 0.f;
-              for (int j = 0; j < quads; ++j) { a += s[g0 + j]; b += s2[g0 + j]; }
-              atomicAdd(st, (double)a);
-              atomicAdd(st + 1, (double)b);
-              st += 2;
-            }
-          }
+          float val;
+          if (nv == 16) val = chunk_group_stats<16>(pk, lane);
+          else if (nv == 8) val = chunk_group_stats<8>(pk, lane);
+          else val = chunk_group_stats<4>(pk, lane);
+          gacc[j] += (double)val;
         }
       }
       ptx::tc_fence_before();
@@ -291,6 +348,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (p.gn_stats) flush();
   }
 
   ptx::tc_fence_before();
@@ -421,7 +479,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
-  if (a.gn_stats && (a.gn_cpg < 4 || a.gn_cpg > 32 || (a.gn_cpg & 3) || a.N != 32 * a.gn_cpg ||
+  if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
                      a.rows_per_img <= 0))
     return cudaErrorInvalidValue;
   if (a.mode == GEMM_SUBPIX && a.resid) return cudaErrorInvalidValue;
