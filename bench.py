@@ -178,6 +178,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2605_19385_b200 as lbx
+    from paper_2605_19385_b200.dist import reduce_max, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -197,8 +198,10 @@ def main():
 
     dec = lbx.Decoder(fam, (128, 128), seed=0, device=local, max_batch=batch)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    rng = np.random.default_rng(2 + rank)
-    lat_np = rng.standard_normal((batch, c, 128, 128), dtype=np.float32).astype(np.float16)
+    # this rank's shard of the global request stream (whole requests; weak scaling)
+    first, last = shard_range(world * batch, rank, world)
+    rng = np.random.default_rng(1_000_003 * 2 + first)
+    lat_np = rng.standard_normal((last - first, c, 128, 128), dtype=np.float32).astype(np.float16)
     lat = torch.from_numpy(lat_np.view(np.int16)).to(dev)
     rgb = torch.empty((batch, 1024, 1024, 3), dtype=torch.uint8, device=dev)
     # a dedicated non-default stream: handle 0 would mean "the decoder's own stream" at the C ABI
@@ -225,10 +228,7 @@ def main():
     barrier()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = reduce_max(ms, dev)
     value = world * batch * args.steps / (ms_max / 1e3)
     launches = dec.launch_count(batch)
 
@@ -247,10 +247,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * batch * args.steps / (float(t.item()) / 1e3), "unit": "img/s",
+        e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
+        e2e = {"value": world * batch * args.steps / (e2e_ms / 1e3), "unit": "img/s",
                "h2d_bytes_per_step": int(sum(len(b) for b in blobs) + 12 * batch),
                "d2h_bytes_per_step": int(out.nbytes), "path": "lbx_reconstruct: LBLP mode-1 blobs (host) -> "
                "H2D -> GPU unpack -> decode graph -> RGB D2H (pinned)"}

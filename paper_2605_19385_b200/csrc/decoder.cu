@@ -411,7 +411,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     ++launches;
     lbx_status e = chk(gemm_tc_launch(ga, s), what);
     if (e == LBX_OK && prof) {
-      const double fl = 2.0 * ga.M * (double)ga.N * ga.K;
+      const double fl = 2.0 * ga.M * (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1);  // 4 phases
       // algorithmic (standard) FLOPs: the sub-pixel form stands for nearest-2x + a full 3x3 conv
       const double algo = ga.mode == GEMM_SUBPIX ? 2.0 * 4.0 * ga.M * (double)ga.N * 9.0 * ga.C : fl;
       char nm[160];

@@ -285,6 +285,16 @@ __global__ void __launch_bounds__(320, 1)
         }
       }
 
+      // residual prefetch ring, two chunks deep, issued before waiting for the accumulator
+      constexpr int PF = NCH < 2 ? NCH : 2;
+      uint4 rr[PF][4];
+      const __half* rbase = p.resid ? p.resid + orow * p.ldr + n0 + hsel * 32 : nullptr;
+      if (p.resid) {
+#pragma unroll
+        for (int j = 0; j < PF; ++j)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rr[j][i] = __ldg(reinterpret_cast<const uint4*>(rbase + j * 64) + i);
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN;
@@ -294,12 +304,6 @@ __global__ void __launch_bounds__(320, 1)
         const int n = n0 + c * 32;
         uint32_t r[32];
         ptx::tmem_ld32(t_row + c * 32, r);
-        uint4 rr[4];
-        if (p.resid) {  // in flight while the TMEM load completes
-          const uint4* rp = reinterpret_cast<const uint4*>(p.resid + orow * p.ldr + n);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) rr[i] = rp[i];
-        }
         ptx::tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -314,13 +318,19 @@ __global__ void __launch_bounds__(320, 1)
         if (p.resid) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const uint32_t w4[4] = {rr[i].x, rr[i].y, rr[i].z, rr[i].w};
+            const uint4 q4 = rr[j % PF][i];
+            const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
               v[i * 8 + 2 * k] += f.x;
               v[i * 8 + 2 * k + 1] += f.y;
             }
+          }
+          if (j + PF < NCH) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              rr[j % PF][i] = __ldg(reinterpret_cast<const uint4*>(rbase + (j + PF) * 64) + i);
           }
         }
         uint32_t pk[16];
@@ -343,8 +353,8 @@ __global__ void __launch_bounds__(320, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 1) ptx::mbar_arrive(&tempty[acc]);
-        else ptx::mbar_arrive_cluster(&tempty[acc], 0);
+        if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty[acc]);
+        else ptx::mbar_arrive_cluster_relaxed(&tempty[acc], 0);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }

@@ -1,0 +1,90 @@
+#!/usr/bin/env python
+"""Run single kernels of the path through the C ABI at realistic sizes (for ncu captures and
+per-op timing).  Not part of the product; device buffers come from torch (plumbing only).
+
+  python scripts/op_bench.py conv --b 4 --hw 1024 --c 128 --n 128 --resid --stats
+  python scripts/op_bench.py subpix --b 4 --hw 512 --c 256
+  python scripts/op_bench.py gn --b 4 --hw 1024 --c 128
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_19385_b200 as lbx  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("op", choices=["conv", "subpix", "gemm", "gn"])
+    ap.add_argument("--b", type=int, default=4)
+    ap.add_argument("--hw", type=int, default=1024)
+    ap.add_argument("--c", type=int, default=128)
+    ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--resid", action="store_true")
+    ap.add_argument("--stats", action="store_true")
+    ap.add_argument("--cg", type=int, default=0)
+    ap.add_argument("--bn", type=int, default=0)
+    ap.add_argument("--iters", type=int, default=3)
+    a = ap.parse_args()
+    dev = torch.device("cuda")
+    b, hw, c = a.b, a.hw, a.c
+    n = a.n or c
+    x = (torch.randn(b, hw, hw, c, device=dev) * 0.5).half()
+    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device=dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    if a.op in ("conv", "subpix", "gemm"):
+        if a.op == "conv":
+            K = 9 * c
+            w = (torch.randn(n, K, device=dev) * K ** -0.5).half()
+            out = torch.empty(b, hw, hw, n, dtype=torch.half, device=dev)
+            M, mode, flops = b * hw * hw, 1, 2.0 * b * hw * hw * n * K
+        elif a.op == "subpix":
+            K = 4 * c
+            w = (torch.randn(4 * n, K, device=dev) * K ** -0.5).half()
+            out = torch.empty(b, 2 * hw, 2 * hw, n, dtype=torch.half, device=dev)
+            M, mode, flops = b * hw * hw, 2, 2.0 * 4 * b * hw * hw * n * 9 * c
+        else:
+            K = a.k or c
+            w = (torch.randn(n, K, device=dev) * K ** -0.5).half()
+            x = (torch.randn(b * hw * hw, K, device=dev)).half()
+            out = torch.empty(b * hw * hw, n, dtype=torch.half, device=dev)
+            M, mode, flops = b * hw * hw, 0, 2.0 * b * hw * hw * n * K
+        bias = torch.randn(n, device=dev)
+        resid = torch.randn_like(out) if a.resid else None
+
+        def run():
+            stats.zero_()
+            lbx.op_gemm(mode, M, n, K, x.data_ptr(), K, w.data_ptr(), K, out.data_ptr(), n, b=b, h=hw, w=hw, c=c,
+                        bias=bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
+                        gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn)
+    else:
+        gamma = torch.ones(c, device=dev)
+        beta = torch.zeros(c, device=dev)
+        y = torch.empty_like(x)
+        lbx.op_gn_stats(x.data_ptr(), stats.data_ptr(), b, hw * hw, c)
+        flops = 4.0 * x.numel()  # bytes
+
+        def run():
+            lbx.op_groupnorm(x.data_ptr(), y.data_ptr(), stats.data_ptr(), gamma.data_ptr(), beta.data_ptr(), b,
+                             hw * hw, c, True)
+
+    run()
+    torch.cuda.synchronize()
+    ev0.record()
+    for _ in range(a.iters):
+        run()
+    ev1.record()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / a.iters
+    unit = "GB/s" if a.op == "gn" else "TFLOP/s(algo)"
+    scale = 1e9 if a.op == "gn" else 1e12
+    print(f"{a.op} b{b} hw{hw} c{c} n{n}: {ms:.3f} ms  {flops / (ms / 1e3) / scale:.1f} {unit}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,60 @@
+"""CPU tests of the C-ABI library: it loads without a GPU, exports every symbol the public headers
+declare, and fails loudly (status + message, no crash, no CPU fallback) when no sm_100 device is
+present.  No compute calls."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    syms = set()
+    for hdr in ("reconstruct.h", "batcher.h"):
+        p = os.path.join(ROOT, "include", "lbx", hdr)
+        if not os.path.exists(p):
+            continue
+        src = open(p).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"\b(lbx_[a-z0-9_]+)\s*\(", src):
+            syms.add(m.group(1))
+    return syms
+
+
+def test_library_exports_every_declared_symbol(lbx):
+    L = ctypes.CDLL(lbx.LIB_PATH)
+    declared = _declared_symbols()
+    assert "lbx_reconstruct" in declared and "lbx_decode" in declared and "lbx_unpack" in declared
+    missing = [s for s in sorted(declared) if not hasattr(L, s)]
+    assert not missing, missing
+    assert set(lbx.SYMBOLS) <= declared | {"lbx_batcher_create"}
+
+
+def test_header_compiles_as_c(tmp_path):
+    src = tmp_path / "t.c"
+    src.write_text('#include "lbx/reconstruct.h"\nint main(void){ lbx_decoder_desc d; (void)d; return 0; }\n')
+    r = os.system(f"gcc -std=c99 -Wall -Werror -I {ROOT}/include -c {src} -o {tmp_path}/t.o")
+    assert r == 0
+
+
+def test_no_device_fails_loudly(lbx):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(lbx.LbxError) as e:
+        lbx.Decoder("sd15", (64, 64), max_batch=1)
+    assert e.value.status in (lbx.E_CUDA, lbx.E_CONFIG)
+    assert lbx.lib().lbx_last_error()  # message set
+
+
+def test_config_validation_before_device(lbx):
+    with pytest.raises(lbx.LbxError) as e:
+        lbx.Decoder("sd15", (64, 64), max_batch=0)
+    assert e.value.status == lbx.E_CONFIG
+    assert b"max_batch" in lbx.lib().lbx_last_error()
+
+
+def test_param_count_unknown_family(lbx):
+    assert lbx.lib().lbx_param_count(99) == 0
