@@ -126,6 +126,31 @@ lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, in
                        const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
                        const float* row_scale, float alpha, double* gn_stats, int cta_group, int bn,
                        lbx_stream stream);
+/* Same op with an optional extra K segment from a second plain operand A2 [M][K2] (row stride lda2):
+ * out += A2 . B[:, K:K+K2]^T inside the tensor-core accumulation (B then has K + K2 columns).  The
+ * decoder folds each resnet's residual (B = identity) or 1x1 shortcut (B = W_sc) into conv2 this way. */
+typedef struct {
+  int mode, M, N, K;
+  const void* A;
+  int lda, b, h, w, c;
+  const void* A2;
+  int lda2, K2;
+  const void* B;
+  int ldb;
+  void* out;
+  int ldo;
+  const float* bias;
+  const void* resid;
+  int ldr;
+  const float* row_scale;
+  float alpha;
+  double* gn_stats;
+  int cta_group, bn;
+} lbx_gemm_desc;
+lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
+/* Diagnostics: halo_policy 0 forces per-tap A staging in the conv kernel (1 = halo when possible);
+ * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
+lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
 /* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
 lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
 /* GroupNorm finalize + apply (SiLU when silu != 0); y may alias x. */

@@ -27,7 +27,7 @@ _STATUS = {1: "LBX_E_RUNTIME", 2: "LBX_E_CONFIG", 3: "LBX_E_CUDA", 4: "LBX_E_FOR
 SYMBOLS = [
     "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
-    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count",
+    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc",
 ]
 
 
@@ -42,6 +42,16 @@ class LbxError(RuntimeError):
 class ProfEntry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 96), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
                 ("algo_flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class GemmDesc(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int), ("M", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+                ("A", ctypes.c_void_p), ("lda", ctypes.c_int), ("b", ctypes.c_int), ("h", ctypes.c_int),
+                ("w", ctypes.c_int), ("c", ctypes.c_int), ("A2", ctypes.c_void_p), ("lda2", ctypes.c_int),
+                ("K2", ctypes.c_int), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int), ("out", ctypes.c_void_p),
+                ("ldo", ctypes.c_int), ("bias", ctypes.c_void_p), ("resid", ctypes.c_void_p), ("ldr", ctypes.c_int),
+                ("row_scale", ctypes.c_void_p), ("alpha", ctypes.c_float), ("gn_stats", ctypes.c_void_p),
+                ("cta_group", ctypes.c_int), ("bn", ctypes.c_int)]
 
 
 class _Desc(ctypes.Structure):
@@ -88,6 +98,8 @@ def lib() -> ctypes.CDLL:
     L.lbx_op_gn_stats.argtypes = [vp, vp, i32, i32, i32, vp]
     L.lbx_profile.argtypes = [vp, u32, ctypes.POINTER(ProfEntry), i32, ctypes.POINTER(i32)]
     L.lbx_launch_count.argtypes = [vp, u32]
+    L.lbx_op_set_debug.argtypes = [i32, i32]
+    L.lbx_op_gemm_desc.argtypes = [ctypes.POINTER(GemmDesc), vp]
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -210,8 +222,14 @@ def _blob_arrays(blobs):
 
 
 def op_gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, *, b=0, h=0, w=0, c=0, bias=0, resid=0, ldr=0, row_scale=0,
-            alpha=1.0, gn_stats=0, cta_group=0, bn=0, stream=0):
-    """Diagnostic entry to the tcgen05 GEMM/conv kernel (device pointers as ints)."""
+            alpha=1.0, gn_stats=0, cta_group=0, bn=0, stream=0, a2=0, lda2=0, k2=0):
+    """Diagnostic entry to the tcgen05 GEMM/conv kernel (device pointers as ints).  a2/lda2/k2 add
+    the extra K segment (lbx_op_gemm_desc)."""
+    if k2:
+        d = GemmDesc(mode, M, N, K, A, lda, b, h, w, c, a2, lda2, k2, B, ldb, out, ldo, bias or None, resid or None,
+                     ldr, row_scale or None, alpha, gn_stats or None, cta_group, bn)
+        check(lib().lbx_op_gemm_desc(ctypes.byref(d), stream or None))
+        return
     check(lib().lbx_op_gemm(mode, M, N, K, A, lda, b, h, w, c, B, ldb, out, ldo, bias or None, resid or None, ldr,
                             row_scale or None, ctypes.c_float(alpha), gn_stats or None, cta_group, bn,
                             stream or None))

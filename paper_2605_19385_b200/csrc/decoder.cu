@@ -229,11 +229,26 @@ lbx_status Decoder::upload_weights(const std::vector<float>& p) {
     norm(rnames[r] + ".norm1", R.cin, &R.n1);
     conv3(rnames[r] + ".conv1", R.cin, R.cout, R.cin, &R.c1);
     norm(rnames[r] + ".norm2", R.cout, &R.n2);
-    conv3(rnames[r] + ".conv2", R.cout, R.cout, R.cout, &R.c2);
-    if (R.cin != R.cout) {
-      uint16_t* q = h16((size_t)R.cout * R.cin, &R.sc.w);
-      lin(get(rnames[r] + ".conv_shortcut.weight"), R.cout, R.cin, q);
-      f32(get(rnames[r] + ".conv_shortcut.bias"), R.cout, &R.sc.b);
+    {
+      // conv2 with the residual folded into K: [Cout][9*Cout + Cin] = [W2 taps | W_sc or identity],
+      // bias b2 (+ b_sc); the tensor core adds x (or shortcut(x)) into the conv2 accumulator.
+      const int K = 9 * R.cout + R.cin;
+      const float* W = get(rnames[r] + ".conv2.weight");
+      uint16_t* q = h16((size_t)R.cout * K, &R.c2.w);
+      const float* Wsc = R.cin != R.cout ? get(rnames[r] + ".conv_shortcut.weight") : nullptr;
+      for (int o = 0; o < R.cout; ++o) {
+        for (int t = 0; t < 9; ++t)
+          for (int c = 0; c < R.cout; ++c)
+            q[(size_t)o * K + t * R.cout + c] = f32_to_f16_bits(W[((size_t)o * R.cout + c) * 9 + t]);
+        for (int c = 0; c < R.cin; ++c)
+          q[(size_t)o * K + 9 * R.cout + c] =
+              Wsc ? f32_to_f16_bits(Wsc[(size_t)o * R.cin + c]) : (uint16_t)(c == o ? 0x3C00 : 0);
+      }
+      float* bq = hb.take<float>(R.cout);
+      const float* b2 = get(rnames[r] + ".conv2.bias");
+      const float* bsc = R.cin != R.cout ? get(rnames[r] + ".conv_shortcut.bias") : nullptr;
+      for (int o = 0; o < R.cout; ++o) bq[o] = bsc ? b2[o] + bsc[o] : b2[o];
+      fixes.push_back({(size_t)((uint8_t*)bq - host.data()), (void**)&R.c2.b});
     }
   }
   const std::string an = "decoder.mid_block.attentions.0";
@@ -462,19 +477,23 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     const int mid = site++;
     if ((e = conv3(A_, H, W, R.cin, R.c1, R.cout, Hb, nullptr, mid, "resnet.conv1")) != LBX_OK) return e;
     if ((e = gn(mid, R.n2, Hb, Hb, R.cout, hw, true)) != LBX_OK) return e;
-    const __half* resid = X_;
-    if (R.cin != R.cout) {
-      GemmArgs g;
-      g.mode = GEMM_PLAIN;
-      g.M = n * hw; g.N = R.cout; g.K = R.cin;
-      g.A = X_; g.lda = R.cin;
-      g.Bw = R.sc.w; g.ldb = R.cin;
-      g.out = A_; g.ldo = R.cout; g.bias = R.sc.b;
-      if ((e = gemm(g, "resnet.shortcut")) != LBX_OK) return e;
-      resid = A_;
-    }
+    // conv2 + (x or shortcut(x)): the residual is an extra K segment of the same tcgen05 GEMM.
+    // Same width: the output overwrites X in place (each tile reads only its own X rows, via TMA,
+    // before its epilogue writes them).  Cin != Cout: row strides differ, so a tile's output rows
+    // would land on other tiles' unread input rows -- write to A (free after conv1) and swap.
     const int out_site = site++;
-    if ((e = conv3(Hb, H, W, R.cout, R.c2, R.cout, X_, resid, out_site, "resnet.conv2")) != LBX_OK) return e;
+    {
+      GemmArgs g;
+      g.mode = GEMM_CONV3X3;
+      g.M = n * hw; g.N = R.cout; g.K = 9 * R.cout;
+      g.A = Hb; g.B_img = n; g.H = H; g.W = W; g.C = R.cout;
+      g.A2 = X_; g.lda2 = R.cin; g.K2 = R.cin;
+      g.Bw = R.c2.w; g.ldb = 9 * R.cout + R.cin;
+      g.out = R.cin == R.cout ? X_ : A_; g.ldo = R.cout; g.bias = R.c2.b;
+      g.gn_stats = site_ptr(out_site); g.gn_cpg = R.cout / 32; g.rows_per_img = hw;
+      if ((e = gemm(g, "resnet.conv2+residual")) != LBX_OK) return e;
+      if (R.cin != R.cout) std::swap(X_, A_);
+    }
     x_site = out_site;
     return LBX_OK;
   };
@@ -780,6 +799,32 @@ lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, in
   cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), cta_group, bn);
   if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
                                        std::string("lbx_op_gemm: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
+  if (!d) return set_err(LBX_E_CONFIG, "lbx_op_gemm_desc: null descriptor");
+  lbx::GemmArgs g;
+  g.mode = d->mode;
+  g.M = d->M; g.N = d->N; g.K = d->K;
+  g.A = reinterpret_cast<const __half*>(d->A); g.lda = d->lda;
+  g.B_img = d->b; g.H = d->h; g.W = d->w; g.C = d->c;
+  g.A2 = reinterpret_cast<const __half*>(d->A2); g.lda2 = d->lda2; g.K2 = d->K2;
+  g.Bw = reinterpret_cast<const __half*>(d->B); g.ldb = d->ldb;
+  g.out = reinterpret_cast<__half*>(d->out); g.ldo = d->ldo;
+  g.bias = d->bias;
+  g.resid = reinterpret_cast<const __half*>(d->resid); g.ldr = d->ldr;
+  g.row_scale = d->row_scale; g.alpha = d->alpha;
+  g.gn_stats = d->gn_stats; g.gn_cpg = d->N / 32;
+  g.rows_per_img = (d->mode == 0) ? (d->b > 0 ? d->M / d->b : d->M) : d->h * d->w;
+  cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), d->cta_group, d->bn);
+  if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
+                                       std::string("lbx_op_gemm_desc: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
+lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
+  lbx::gemm_tc_set_debug(halo_policy, desc_base_mode);
   return LBX_OK;
 }
 

@@ -28,7 +28,7 @@ struct KParams {
   int M, N, K;
   int num_kb;          // K / 64
   int cblocks;         // conv: C / 64
-  int H, W, Wt, Ht;    // conv geometry (A box = 64 x Wt x Ht x 1)
+  int H, W, Wt, Ht;    // conv geometry (per-tap A box = 64 x Wt x Ht x 1)
   int m_tiles, n_tiles, tiles;
   __half* out;
   int ldo;
@@ -40,22 +40,32 @@ struct KParams {
   double* gn_stats;
   int gn_cpg;
   int rows_per_img;
+  // operand staging (host-computed, see stage_plan())
+  int halo;            // 1: one halo box per C-block feeds every tap (row-shifted UMMA descriptors)
+  int halo_rows;       // 3 (conv3x3) or 2 (sub-pixel)
+  int taps;            // 9 (conv3x3), 4 (sub-pixel)
+  int a_stage_bytes;   // smem bytes per A stage (1024-aligned)
+  int a_tx_bytes;      // bytes one CTA's A load lands per stage
+  int a_stages, b_stages;
+  int desc_base_mode;  // descriptor base-offset convention for row-shifted views (0 or 1)
+  int msub;            // 128-row M sub-tiles per CTA sharing every B tile (1 or 2)
+  int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
+  int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
+  int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
+  int k_main;          // K of the main segment (B columns of the extra segment start here)
 };
+
+constexpr int kHaloW = 130;      // 128 output pixels + 1-pixel halo on each side
+constexpr int kMaxStages = 16;   // barrier array capacity per ring
+constexpr int kSmemBudget = 220 * 1024;
 
 template <int BN, int CG>
 struct Cfg {
-  static constexpr int BM_CTA = 128;                 // A rows per CTA
-  static constexpr int BK = 64;                      // 128 bytes of fp16 (one SW128 row)
-  static constexpr int A_BYTES = BM_CTA * BK * 2;    // 16 KiB
   static constexpr int B_ROWS = BN / CG;             // B rows staged per CTA
-  static constexpr int B_BYTES = B_ROWS * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;           // double-buffered fp32 accumulator
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
-  static constexpr int THREADS = 320;  // 2 non-epilogue + 8 epilogue warps
+  static constexpr int B_BYTES = B_ROWS * 64 * 2;    // one 64-wide k-block
+  static constexpr int SMEM_MAX = 227 * 1024;
+  static constexpr int THREADS = 352;  // warp 0 A-producer, 1 MMA, 2..9 epilogue, 10 B-producer
   static constexpr uint32_t IDESC = ptx::idesc_f16(128 * CG, BN);
-  static constexpr uint32_t TX_BYTES = CG * STAGE_BYTES;  // bytes landing per stage per tile (pair)
 };
 
 __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile, int& n_tile, int& phase) {
@@ -111,17 +121,19 @@ __device__ __forceinline__ float chunk_group_stats(const uint32_t (&pk)[16], uin
 }
 
 template <int BN, int CG>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const KParams p) {
+                   const __grid_constant__ CUtensorMap tmA2, const KParams p) {
   using C = Cfg<BN, CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint8_t* sB = smem + p.a_stages * p.a_stage_bytes;
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + p.b_stages * C::B_BYTES);
+  uint64_t* a_empty = a_full + kMaxStages;
+  uint64_t* b_full = a_empty + kMaxStages;
+  uint64_t* b_empty = b_full + kMaxStages;
+  uint64_t* tfull = b_empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -131,13 +143,19 @@ __global__ void __launch_bounds__(320, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG;
   const int nclusters = gridDim.x / CG;
+  // A stages per tile and taps (B stages) per A stage
+  const int n_a = p.halo ? p.cblocks : p.num_kb;
+  const int per_a = p.halo ? p.taps : 1;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
-    for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+    if (p.n_extra) ptx::tma_prefetch(&tmA2);
+    for (int s = 0; s < kMaxStages; ++s) {
+      ptx::mbar_init(&a_full[s], 1);
+      ptx::mbar_init(&a_empty[s], 1);
+      ptx::mbar_init(&b_full[s], 1);
+      ptx::mbar_init(&b_empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
@@ -145,21 +163,22 @@ __global__ void __launch_bounds__(320, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, C::TMEM_COLS);
+  if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ A producer (TMA)
     if (ptx::elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
+      int st = 0;
+      uint32_t ph = 0;
       for (int t = cluster_id; t < p.tiles; t += nclusters) {
-        int m_tile, n_tile, ph;
-        tile_coords(p, t, m_tile, n_tile, ph);
-        const int m0 = m_tile * (128 * CG) + rank * 128;  // this CTA's first A row
+        int m_tile, n_tile, phs;
+        tile_coords(p, t, m_tile, n_tile, phs);
+        const int rows_cta = 128 * p.msub;
+        const int m0 = m_tile * (rows_cta * CG) + rank * rows_cta;  // this CTA's first A row
         int img = 0, y0 = 0, x0 = 0;
         if (p.mode != GEMM_PLAIN) {
           const int hw = p.H * p.W;
@@ -168,60 +187,149 @@ __global__ void __launch_bounds__(320, 1)
           y0 = rem / p.W;
           x0 = rem - y0 * p.W;
         }
-        const int b_row = (p.mode == GEMM_SUBPIX ? ph * p.N : 0) + n_tile * BN + rank * C::B_ROWS;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* a_dst = sA + stage * C::A_BYTES;
-          uint8_t* b_dst = sB + stage * C::B_BYTES;
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], C::TX_BYTES);
+        for (int j = 0; j < n_a; ++j) {
+          ptx::mbar_wait(&a_empty[st], ph ^ 1);
+          uint8_t* dst = sA + st * p.a_stage_bytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * p.a_tx_bytes);
+          int c0 = 0, c1 = 0, c2 = 0, c3 = img;
           if (p.mode == GEMM_PLAIN) {
-            if constexpr (CG == 1) ptx::tma_load_2d(&tmA, &full[stage], a_dst, kb * 64, m0);
-            else ptx::tma_load_2d_pair(&tmA, &full[stage], a_dst, kb * 64, m0);
+            c0 = j * 64;
+            c1 = m0;
+          } else if (p.halo) {  // per sub-tile: rows [y_top, y_top + halo_rows) x cols [x-1, x+129) x 64 ch
+            c0 = j * 64;
+            c1 = x0 - 1;
+            c2 = p.mode == GEMM_CONV3X3 ? y0 - 1 : y0 + (phs >> 1) - 1;
+            for (int sub = 1; sub < p.msub; ++sub) {
+              if constexpr (CG == 1) ptx::tma_load_4d(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
+              else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
+            }
           } else {
-            const int tap = kb / p.cblocks;
-            const int cb = kb - tap * p.cblocks;
+            const int tap = j / p.cblocks;
+            const int cb = j - tap * p.cblocks;
             int dx, dy;
             if (p.mode == GEMM_CONV3X3) {
               dy = tap / 3 - 1;
               dx = tap % 3 - 1;
-            } else {  // sub-pixel phase (a, b) = (ph >> 1, ph & 1): low-res offsets r + a - 1
-              dy = (tap >> 1) + (ph >> 1) - 1;
-              dx = (tap & 1) + (ph & 1) - 1;
+            } else {  // sub-pixel phase (a, b): low-res offsets r + a - 1
+              dy = (tap >> 1) + (phs >> 1) - 1;
+              dx = (tap & 1) + (phs & 1) - 1;
             }
-            if constexpr (CG == 1) ptx::tma_load_4d(&tmA, &full[stage], a_dst, cb * 64, x0 + dx, y0 + dy, img);
-            else ptx::tma_load_4d_pair(&tmA, &full[stage], a_dst, cb * 64, x0 + dx, y0 + dy, img);
+            c0 = cb * 64;
+            c1 = x0 + dx;
+            c2 = y0 + dy;
           }
-          if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &full[stage], b_dst, kb * 64, b_row);
-          else ptx::tma_load_2d_pair(&tmB, &full[stage], b_dst, kb * 64, b_row);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (p.mode == GEMM_PLAIN) {
+            if constexpr (CG == 1) ptx::tma_load_2d(&tmA, &a_full[st], dst, c0, c1);
+            else ptx::tma_load_2d_pair(&tmA, &a_full[st], dst, c0, c1);
+          } else {
+            if constexpr (CG == 1) ptx::tma_load_4d(&tmA, &a_full[st], dst, c0, c1, c2, c3);
+            else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst, c0, c1, c2, c3);
+          }
+          if (++st == p.a_stages) { st = 0; ph ^= 1; }
+        }
+        for (int e = 0; e < p.n_extra; ++e) {  // second operand: plain [M][K2] rows of this tile
+          ptx::mbar_wait(&a_empty[st], ph ^ 1);
+          uint8_t* dst = sA + st * p.a_stage_bytes;
+          if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * rows_cta * 64 * 2);
+          for (int sub = 0; sub < p.msub; ++sub) {
+            if constexpr (CG == 1) ptx::tma_load_2d(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
+            else ptx::tma_load_2d_pair(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
+          }
+          if (++st == p.a_stages) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ B producer (TMA, weights)
+    if (ptx::elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int t = cluster_id; t < p.tiles; t += nclusters) {
+        int m_tile, n_tile, phs;
+        tile_coords(p, t, m_tile, n_tile, phs);
+        const int b_row = (p.mode == GEMM_SUBPIX ? phs * p.N : 0) + n_tile * BN + rank * C::B_ROWS;
+        for (int j = 0; j < n_a; ++j) {
+          for (int tp = 0; tp < per_a; ++tp) {
+            ptx::mbar_wait(&b_empty[st], ph ^ 1);
+            if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
+            const int k0 = p.halo ? tp * (p.cblocks * 64) + j * 64 : j * 64;  // K = (tap, channel)
+            uint8_t* dst = sB + st * C::B_BYTES;
+            if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst, k0, b_row);
+            else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst, k0, b_row);
+            if (++st == p.b_stages) { st = 0; ph ^= 1; }
+          }
+        }
+        for (int e = 0; e < p.n_extra; ++e) {
+          ptx::mbar_wait(&b_empty[st], ph ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
+          uint8_t* dst = sB + st * C::B_BYTES;
+          if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst, p.k_main + e * 64, b_row);
+          else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst, p.k_main + e * 64, b_row);
+          if (++st == p.b_stages) { st = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (leader) {
-      int stage = 0;
-      uint32_t phase = 0;
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cluster_id; t < p.tiles; t += nclusters) {
+        int m_tile, n_tile, phs;
+        tile_coords(p, t, m_tile, n_tile, phs);
         ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+        const uint32_t d_tmem = tmem_base + acc * (p.msub * BN);
+        for (int j = 0; j < n_a; ++j) {
+          ptx::mbar_wait(&a_full[as], aph);
+          const uint32_t a_base = ptx::smem_u32(sA + as * p.a_stage_bytes);
+          for (int tp = 0; tp < per_a; ++tp) {
+            ptx::mbar_wait(&b_full[bs], bph);
+            ptx::tc_fence_after();
+            if (ptx::elect_one()) {
+              // halo: the tap's 128 A rows start `r0` rows into the halo box
+              int r0 = 0;
+              if (p.halo) r0 = p.mode == GEMM_CONV3X3 ? (tp / 3) * 130 + tp % 3 : (tp >> 1) * 130 + (tp & 1) + (phs & 1);
+              const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + bs * C::B_BYTES));
+              for (int sub = 0; sub < p.msub; ++sub) {  // sub-tiles share this B tile
+                uint64_t a_desc = ptx::sdesc_k_sw128(a_base + sub * p.halo_sub_bytes + r0 * 128);
+                if (p.desc_base_mode) a_desc |= (uint64_t)(r0 & 7) << 49;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide k-block; +32 B per step inside the swizzle atom
+                  ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, (j | tp | k) != 0);
+              }
+              ptx::mma_commit<CG>(&b_empty[bs]);
+              if (tp == per_a - 1) {
+                ptx::mma_commit<CG>(&a_empty[as]);
+                if (j == n_a - 1 && p.n_extra == 0) ptx::mma_commit<CG>(&tfull[acc]);
+              }
+            }
+            __syncwarp();
+            if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
+          }
+          if (++as == p.a_stages) { as = 0; aph ^= 1; }
+        }
+        for (int e = 0; e < p.n_extra; ++e) {
+          ptx::mbar_wait(&a_full[as], aph);
+          ptx::mbar_wait(&b_full[bs], bph);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
-            const uint64_t a_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + stage * C::A_BYTES));
-            const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + stage * C::B_BYTES));
+            const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + bs * C::B_BYTES));
+            for (int sub = 0; sub < p.msub; ++sub) {
+              const uint64_t a_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + as * p.a_stage_bytes + sub * 16384));
 #pragma unroll
-            for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide k-block; +32 B per step inside the swizzle atom
-              ptx::mma_f16_ss<CG>(d_tmem, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, (kb | k) != 0);
-            ptx::mma_commit<CG>(&empty[stage]);
-            if (kb == p.num_kb - 1) ptx::mma_commit<CG>(&tfull[acc]);
+              for (int k = 0; k < 4; ++k)
+                ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, 1u);
+            }
+            ptx::mma_commit<CG>(&b_empty[bs]);
+            ptx::mma_commit<CG>(&a_empty[as]);
+            if (e == p.n_extra - 1) ptx::mma_commit<CG>(&tfull[acc]);
           }
           __syncwarp();
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
+          if (++as == p.a_stages) { as = 0; aph ^= 1; }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
@@ -265,8 +373,11 @@ __global__ void __launch_bounds__(320, 1)
     for (int t = cluster_id; t < p.tiles; t += nclusters) {
       int m_tile, n_tile, ph;
       tile_coords(p, t, m_tile, n_tile, ph);
-      const int m = m_tile * (128 * CG) + rank * 128 + row;
       const int n0 = n_tile * BN;
+      ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
+      for (int sub = 0; sub < p.msub; ++sub) {
+      const int m = m_tile * (128 * p.msub * CG) + rank * (128 * p.msub) + sub * 128 + row;
       long long orow = m;
       if (p.mode == GEMM_SUBPIX) {
         const int hw = p.H * p.W;
@@ -295,9 +406,7 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
           for (int i = 0; i < 4; ++i) rr[j][i] = __ldg(reinterpret_cast<const uint4*>(rbase + j * 64) + i);
       }
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * (p.msub * BN) + sub * BN;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
         const int c = hsel + 2 * j;
@@ -350,6 +459,7 @@ __global__ void __launch_bounds__(320, 1)
           gacc[j] += (double)val;
         }
       }
+      }  // sub-tiles
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -365,7 +475,7 @@ __global__ void __launch_bounds__(320, 1)
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+    ptx::tmem_dealloc<CG>(tmem_base, p.tmem_cols);
   }
 }
 
@@ -412,8 +522,25 @@ static bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_
 }
 
 template <int BN, int CG>
-static cudaError_t launch_cfg(const GemmArgs& a, const KParams& kp, cudaStream_t stream) {
+static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
+  // ---- operand staging plan
+  if (kp.halo) {
+    kp.halo_sub_bytes = (64 * 130 * kp.halo_rows * 2 + 1023) & ~1023;
+    kp.a_tx_bytes = kp.msub * 64 * 130 * kp.halo_rows * 2;
+    kp.a_stage_bytes = kp.msub * kp.halo_sub_bytes;
+    kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
+    kp.b_stages = (kSmemBudget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
+  } else {
+    kp.a_tx_bytes = kp.a_stage_bytes = 128 * 64 * 2;
+    kp.a_stages = kp.b_stages = kSmemBudget / (kp.a_stage_bytes + Cf::B_BYTES);
+  }
+  if (kp.a_stages > kMaxStages) kp.a_stages = kMaxStages;
+  if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
+  if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
+  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (4 * kMaxStages + 4) * 8 + 16;
+  if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
+
   CUtensorMap tmA, tmB;
   if (a.mode == GEMM_PLAIN) {
     cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.M};
@@ -423,12 +550,21 @@ static cudaError_t launch_cfg(const GemmArgs& a, const KParams& kp, cudaStream_t
   } else {
     cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.B_img};
     cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)kp.Wt, (cuuint32_t)kp.Ht, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)(kp.halo ? 130 : kp.Wt), (cuuint32_t)(kp.halo ? kp.halo_rows : kp.Ht), 1};
     if (!make_map(&tmA, a.A, 4, dims, strides, box)) return cudaErrorInvalidValue;
+  }
+  CUtensorMap tmA2;
+  if (kp.n_extra) {
+    cuuint64_t dims[2] = {(cuuint64_t)a.K2, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)a.lda2 * 2};
+    cuuint32_t box[2] = {64, 128};
+    if (!make_map(&tmA2, a.A2, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
+    tmA2 = tmA;
   }
   {
     const int brows = a.mode == GEMM_SUBPIX ? 4 * a.N : a.N;
-    cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)brows};
+    cuuint64_t dims[2] = {(cuuint64_t)(a.K + a.K2), (cuuint64_t)brows};
     cuuint64_t strides[1] = {(cuuint64_t)a.ldb * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)Cf::B_ROWS};
     if (!make_map(&tmB, a.Bw, 2, dims, strides, box)) return cudaErrorInvalidValue;
@@ -440,7 +576,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, const KParams& kp, cudaStream_t
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG);
   cfg.blockDim = dim3(Cf::THREADS);
-  cfg.dynamicSmemBytes = Cf::SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -449,13 +585,13 @@ static cudaError_t launch_cfg(const GemmArgs& a, const KParams& kp, cudaStream_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, kp);
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA2, kp);
 }
 
 template <int BN, int CG>
 static bool set_attr() {
   return cudaFuncSetAttribute(gemm_tc_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<BN, CG>::SMEM_BYTES) == cudaSuccess;
+                              Cfg<BN, CG>::SMEM_MAX) == cudaSuccess;
 }
 
 bool gemm_tc_prepare() {
@@ -469,6 +605,15 @@ bool gemm_tc_prepare() {
   return ok == 1;
 }
 
+static int g_halo_policy = 1;      // 1: use halo staging whenever the geometry allows
+static int g_msub_policy = 1;      // 1: two M sub-tiles per CTA for BN = 128 halo convs
+static int g_desc_base_mode = 0;   // descriptor base-offset convention for row-shifted A views
+void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
+  g_halo_policy = halo_policy & 1;
+  g_msub_policy = (halo_policy >> 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
+  g_desc_base_mode = desc_base_mode;
+}
+
 cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg, int force_bn) {
   if (!gemm_tc_prepare()) return cudaErrorNotSupported;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0 || a.K % 64) return cudaErrorInvalidValue;
@@ -476,6 +621,11 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.mode = a.mode;
   kp.M = a.M; kp.N = a.N; kp.K = a.K;
   kp.num_kb = a.K / 64;
+  kp.k_main = a.K;
+  if (a.K2) {
+    if (a.K2 % 64 || !a.A2 || a.lda2 < a.K2 || a.mode == GEMM_SUBPIX) return cudaErrorInvalidValue;
+    kp.n_extra = a.K2 / 64;
+  }
   if (a.mode != GEMM_PLAIN) {
     if (a.C % 64 || a.M != a.B_img * a.H * a.W) return cudaErrorInvalidValue;
     if (a.K != (a.mode == GEMM_CONV3X3 ? 9 : 4) * a.C) return cudaErrorInvalidValue;
@@ -485,6 +635,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
     if (128 % kp.Wt || (a.W > 128 && a.W % 128)) return cudaErrorInvalidValue;
     kp.Ht = 128 / kp.Wt;
     if (a.H % kp.Ht) return cudaErrorInvalidValue;
+    kp.taps = a.mode == GEMM_CONV3X3 ? 9 : 4;
+    kp.halo_rows = a.mode == GEMM_CONV3X3 ? 3 : 2;
+    kp.halo = (g_halo_policy && kp.Ht == 1) ? 1 : 0;  // a tap's 128 rows must be contiguous in the halo
+    kp.desc_base_mode = g_desc_base_mode;
   }
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
@@ -498,7 +652,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   if (a.N % bn) return cudaErrorInvalidValue;
   int cg = force_cg ? force_cg : ((a.M % 256 == 0) ? 2 : 1);
   if (a.M % (128 * cg)) return cudaErrorInvalidValue;
-  kp.m_tiles = a.M / (128 * cg);
+  kp.msub = (kp.halo && g_msub_policy && bn == 128 && cg == 2 && a.mode == GEMM_CONV3X3 && a.W % 256 == 0 &&
+             a.M % (512 * cg) == 0) ? 2 : 1;
+  kp.tmem_cols = 2 * bn * kp.msub;
+  kp.m_tiles = a.M / (128 * cg * kp.msub);
   kp.n_tiles = a.N / bn;
   kp.tiles = kp.m_tiles * kp.n_tiles * (a.mode == GEMM_SUBPIX ? 4 : 1);
   if (bn == 256 && cg == 2) return launch_cfg<256, 2>(a, kp, stream);

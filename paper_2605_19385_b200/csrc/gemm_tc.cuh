@@ -22,7 +22,12 @@ struct GemmArgs {
   const __half* A = nullptr;
   int lda = 0;                    // plain: row stride (elements)
   int B_img = 0, H = 0, W = 0, C = 0;  // conv: NHWC input geometry (M = B_img*H*W, K = 9*C)
-  // B operand: weights [N][K] K-major (conv: K index = (ky*3+kx)*C + ci)
+  // optional extra K segment from a second, plain operand whose rows match the output rows:
+  // C += A2[m, :] . B[n, K : K + K2].  Used to fold a residual (B = identity) or a 1x1 shortcut
+  // conv (B = W_sc) into the tensor-core accumulation instead of the epilogue.
+  const __half* A2 = nullptr;
+  int lda2 = 0, K2 = 0;
+  // B operand: weights [N][K + K2] K-major (conv: K index = (ky*3+kx)*C + ci)
   const __half* Bw = nullptr;
   int ldb = 0;
   // epilogue
@@ -40,6 +45,10 @@ struct GemmArgs {
 
 // Launch on `stream`.  Returns cudaSuccess or the launch error.  Chooses tile / CTA-pair config.
 cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg = 0, int force_bn = 0);
+
+// Diagnostics: halo_policy 0 forces per-tap A staging; desc_base_mode selects the UMMA descriptor
+// base-offset convention for row-shifted (non-1024-aligned) halo views.
+void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();

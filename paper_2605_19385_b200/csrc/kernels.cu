@@ -89,61 +89,89 @@ void launch_gn_finalize(const double* stats, const float* gamma, const float* be
   gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, count, eps);
 }
 
-__device__ __forceinline__ float silu_f(float x) { return x * __frcp_rn(1.0f + __expf(-x)); }
+// SiLU with one MUFU op per element: ex2 on the SFU, the reciprocal of (1 + e) on the FMA pipe
+// (bit-trick seed, 3 Newton steps -> fp32-accurate).  The SFU (16 ops/clk/SM) is what bounded the
+// GroupNorm-apply pass at ~3.5 TB/s with ex2 + rcp; the FMA pipe has 8x its throughput.
+__device__ __forceinline__ float silu_f(float x) {
+  const float xc = fmaxf(x, -80.0f);  // keeps 1 + e finite and normal for the seed trick
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(xc * -1.4426950408889634f));
+  const float d = 1.0f + e;
+  float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+  r = r * fmaf(-d, r, 2.0f);
+  r = r * fmaf(-d, r, 2.0f);
+  r = r * fmaf(-d, r, 2.0f);
+  return x * r;
+}
 
-// y = act(x * a_c + b_c).  Block (bx, img) covers a contiguous pixel range of one image; thread t
-// owns channel octet t % (C/8) for every pixel it visits, so its 8 affine pairs are loaded once.
+// y = act(x * a_c + b_c).  The launch is exactly one resident wave; block b covers a contiguous
+// range of the flattened (image, pixel) space, split at image boundaries.  Thread t owns channel
+// octet t % (C/8) for every pixel it visits, so its 8 affine pairs are reloaded only per image.
 template <bool SILU, int CV>
 __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* y, const float2* __restrict__ ss,
-                                                       int hw, int pix_per_block) {
+                                                       int hw, long long total, long long pix_per_block) {
   constexpr int PSTEP = 256 / CV;  // pixels advanced per iteration of the block
-  const int img = blockIdx.y;
   const int cvec = threadIdx.x % CV;
-  const int p_first = blockIdx.x * pix_per_block + threadIdx.x / CV;
-  const int p_end = min(hw, (blockIdx.x + 1) * pix_per_block);
-  float a[8], b[8];
+  const long long end = min(total, (blockIdx.x + 1) * pix_per_block);
+  long long p = blockIdx.x * pix_per_block + threadIdx.x / CV;
+  const uint4* xv = reinterpret_cast<const uint4*>(x) + cvec;
+  uint4* yv = reinterpret_cast<uint4*>(y) + cvec;
+  while (p < end) {
+    const int img = (int)(p / hw);
+    const long long seg_end = min(end, (long long)(img + 1) * hw);
+    float a[8], b[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float2 t = ss[(size_t)img * CV * 8 + cvec * 8 + k];
-    a[k] = t.x;
-    b[k] = t.y;
-  }
-  const uint4* xv = reinterpret_cast<const uint4*>(x) + (size_t)img * hw * CV + cvec;
-  uint4* yv = reinterpret_cast<uint4*>(y) + (size_t)img * hw * CV + cvec;
-  auto apply = [&](uint4 u) {
-    uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-      float y0 = fmaf(f.x, a[2 * j], b[2 * j]), y1 = fmaf(f.y, a[2 * j + 1], b[2 * j + 1]);
-      if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
-      const __half2 h = __floats2half2_rn(y0, y1);
-      w[j] = *reinterpret_cast<const uint32_t*>(&h);
+    for (int k = 0; k < 8; ++k) {
+      const float2 t = ss[(size_t)img * CV * 8 + cvec * 8 + k];
+      a[k] = t.x;
+      b[k] = t.y;
     }
-    return make_uint4(w[0], w[1], w[2], w[3]);
-  };
-  int p = p_first;
-  for (; p + 3 * PSTEP < p_end; p += 4 * PSTEP) {
-    uint4 u[4];
+    auto apply = [&](uint4 u) {
+      uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) u[i] = xv[(size_t)(p + i * PSTEP) * CV];
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+        float y0 = fmaf(f.x, a[2 * j], b[2 * j]), y1 = fmaf(f.y, a[2 * j + 1], b[2 * j + 1]);
+        if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
+        const __half2 h = __floats2half2_rn(y0, y1);
+        w[j] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+    constexpr int U = 8;  // 16-byte loads in flight per thread (latency x bandwidth needs ~100 KB/SM)
+    for (; p + (U - 1) * PSTEP < seg_end; p += U * PSTEP) {
+      uint4 u[U];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) yv[(size_t)(p + i * PSTEP) * CV] = apply(u[i]);
+      for (int i = 0; i < U; ++i) u[i] = __ldcs(xv + (size_t)(p + i * PSTEP) * CV);
+#pragma unroll
+      for (int i = 0; i < U; ++i) __stcs(yv + (size_t)(p + i * PSTEP) * CV, apply(u[i]));
+    }
+    for (; p < seg_end; p += PSTEP) __stcs(yv + (size_t)p * CV, apply(__ldcs(xv + (size_t)p * CV)));
   }
-  for (; p < p_end; p += PSTEP) yv[(size_t)p * CV] = apply(xv[(size_t)p * CV]);
+}
+
+template <bool SILU, int CV>
+static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
+  static int occ = 0;
+  if (!occ) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel<SILU, CV>, 256, 0);
+    if (occ <= 0) occ = 4;
+  }
+  constexpr int PSTEP = 256 / CV;
+  const long long total = (long long)n * hw;
+  const long long blocks = (long long)num_sms() * occ;
+  long long ppb = (total + blocks - 1) / blocks;
+  ppb = (ppb + PSTEP - 1) / PSTEP * PSTEP;
+  const int grid = (int)((total + ppb - 1) / ppb);
+  gn_apply_kernel<SILU, CV><<<grid, 256, 0, s>>>(x, y, ss, hw, total, ppb);
 }
 
 template <bool SILU>
 static void gn_apply_dispatch(const __half* x, __half* y, const float2* ss, int n, int hw, int C, cudaStream_t s) {
-  // ~8 resident blocks per SM across the whole launch, pixel ranges a multiple of the pixel step
-  int per_img = (num_sms() * 8 + n - 1) / n;
-  int ppb = (hw + per_img - 1) / per_img;
-  ppb = (ppb + 31) & ~31;
-  dim3 grid((hw + ppb - 1) / ppb, n);
   switch (C / 8) {
-    case 16: gn_apply_kernel<SILU, 16><<<grid, 256, 0, s>>>(x, y, ss, hw, ppb); break;
-    case 32: gn_apply_kernel<SILU, 32><<<grid, 256, 0, s>>>(x, y, ss, hw, ppb); break;
-    case 64: gn_apply_kernel<SILU, 64><<<grid, 256, 0, s>>>(x, y, ss, hw, ppb); break;
+    case 16: gn_apply_launch<SILU, 16>(x, y, ss, n, hw, s); break;
+    case 32: gn_apply_launch<SILU, 32>(x, y, ss, n, hw, s); break;
+    case 64: gn_apply_launch<SILU, 64>(x, y, ss, n, hw, s); break;
     default: break;  // C validated by callers (128 / 256 / 512)
   }
 }
@@ -287,38 +315,41 @@ void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, in
 }
 
 // ----------------------------------------------------------------------------- conv_out -> uint8
-// Tile: 8 rows x 32 columns of output pixels per 256-thread block (one pixel per thread).
-// Channels are streamed in chunks of 16 through a GN+SiLU-transformed halo tile in smem.
-constexpr int CO_TH = 8, CO_TW = 32, CO_CC = 16;
+// Tile: 16 rows x 64 columns of output pixels per 256-thread block; each thread owns 4 horizontally
+// adjacent pixels, so one 6-wide input window per (row, channel) feeds all 3 taps x 4 pixels
+// (6 LDS + 9 broadcast LDS.128 of weights per 108 FMAs).  Channels stream in chunks of 8 through
+// a GN+SiLU-transformed fp32 halo tile; the padding taps are exact zeros (padding after SiLU).
+constexpr int CO_TH = 16, CO_TW = 64, CO_CC = 8, CO_PW = 68;  // halo row pitch (>= 66, float4-aligned)
 
 __global__ void __launch_bounds__(256) conv_out_u8_kernel(const __half* __restrict__ x, const float2* __restrict__ ss,
                                                           const float* __restrict__ w, const float* __restrict__ b,
                                                           uint8_t* __restrict__ rgb, int H, int W) {
-  __shared__ float tile[CO_CC][CO_TH + 2][CO_TW + 2];
-  __shared__ float wsm[3][9][CO_CC];
+  __shared__ __align__(16) float tile[CO_CC][CO_TH + 2][CO_PW];
+  __shared__ float4 wsm[9][CO_CC];  // (co0, co1, co2, 0) per tap and channel
   const int img = blockIdx.z;
   const int y0 = blockIdx.y * CO_TH, x0 = blockIdx.x * CO_TW;
-  const int ty = threadIdx.x / CO_TW, tx = threadIdx.x % CO_TW;
-  float acc0 = b[0], acc1 = b[1], acc2 = b[2];
+  const int ty = threadIdx.x >> 4, tx4 = (threadIdx.x & 15) * 4;
+  float acc[4][3];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    acc[p][0] = b[0];
+    acc[p][1] = b[1];
+    acc[p][2] = b[2];
+  }
   const float2* ssi = ss + (size_t)img * 128;
   for (int c0 = 0; c0 < 128; c0 += CO_CC) {
     __syncthreads();
-    // halo tile (CO_TH+2) x (CO_TW+2) pixels x 16 channels; zero outside the image (conv padding
-    // applies after GN+SiLU, so padded taps contribute exactly 0)
-    for (int i = threadIdx.x; i < (CO_TH + 2) * (CO_TW + 2) * 2; i += 256) {
-      const int half_sel = i & 1;  // which 8-channel half of the chunk
-      const int pix = i >> 1;
-      const int py = pix / (CO_TW + 2), px = pix % (CO_TW + 2);
+    for (int pix = threadIdx.x; pix < (CO_TH + 2) * (CO_TW + 2); pix += 256) {
+      const int py = pix / (CO_TW + 2), px = pix - py * (CO_TW + 2);
       const int gy = y0 + py - 1, gx = x0 + px - 1;
       float v[8];
       if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-        const uint4 u = *reinterpret_cast<const uint4*>(x + (((size_t)img * H + gy) * W + gx) * 128 + c0 + half_sel * 8);
-        const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + (((size_t)img * H + gy) * W + gx) * 128 + c0));
+        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float2 f = __half22float2(h2[j]);
-          const int c = c0 + half_sel * 8 + 2 * j;
-          const float2 a = ssi[c], bb = ssi[c + 1];
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&wd[j]));
+          const float2 a = ssi[c0 + 2 * j], bb = ssi[c0 + 2 * j + 1];
           v[2 * j] = silu_f(fmaf(f.x, a.x, a.y));
           v[2 * j + 1] = silu_f(fmaf(f.y, bb.x, bb.y));
         }
@@ -327,35 +358,52 @@ __global__ void __launch_bounds__(256) conv_out_u8_kernel(const __half* __restri
         for (int j = 0; j < 8; ++j) v[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) tile[half_sel * 8 + j][py][px] = v[j];
+      for (int j = 0; j < 8; ++j) tile[j][py][px] = v[j];
     }
-    for (int i = threadIdx.x; i < 3 * 9 * CO_CC; i += 256) {
-      const int co = i / (9 * CO_CC), rem = i % (9 * CO_CC), tap = rem / CO_CC, ci = rem % CO_CC;
-      wsm[co][tap][ci] = w[(co * 9 + tap) * 128 + c0 + ci];
+    if (threadIdx.x < 9 * CO_CC) {
+      const int tap = threadIdx.x / CO_CC, ci = threadIdx.x % CO_CC;
+      wsm[tap][ci] = make_float4(w[(0 * 9 + tap) * 128 + c0 + ci], w[(1 * 9 + tap) * 128 + c0 + ci],
+                                 w[(2 * 9 + tap) * 128 + c0 + ci], 0.f);
     }
     __syncthreads();
 #pragma unroll
-    for (int ky = 0; ky < 3; ++ky)
+    for (int ci = 0; ci < CO_CC; ++ci) {
 #pragma unroll
-      for (int kx = 0; kx < 3; ++kx)
+      for (int ky = 0; ky < 3; ++ky) {
+        const float* row = &tile[ci][ty + ky][tx4];
+        const float4 i4 = *reinterpret_cast<const float4*>(row);
+        const float2 i2 = *reinterpret_cast<const float2*>(row + 4);
+        const float in[6] = {i4.x, i4.y, i4.z, i4.w, i2.x, i2.y};
 #pragma unroll
-        for (int ci = 0; ci < CO_CC; ++ci) {
-          const float v = tile[ci][ty + ky][tx + kx];
-          acc0 = fmaf(v, wsm[0][ky * 3 + kx][ci], acc0);
-          acc1 = fmaf(v, wsm[1][ky * 3 + kx][ci], acc1);
-          acc2 = fmaf(v, wsm[2][ky * 3 + kx][ci], acc2);
+        for (int kx = 0; kx < 3; ++kx) {
+          const float4 wv = wsm[ky * 3 + kx][ci];
+#pragma unroll
+          for (int p = 0; p < 4; ++p) {
+            acc[p][0] = fmaf(in[p + kx], wv.x, acc[p][0]);
+            acc[p][1] = fmaf(in[p + kx], wv.y, acc[p][1]);
+            acc[p][2] = fmaf(in[p + kx], wv.z, acc[p][2]);
+          }
         }
-  }
-  const int gy = y0 + ty, gx = x0 + tx;
-  if (gy < H && gx < W) {
-    float a[3] = {acc0, acc1, acc2};
-    uint8_t* o = rgb + (((size_t)img * H + gy) * W + gx) * 3;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      float t = __fadd_rn(__fmul_rn(a[k], 0.5f), 0.5f);
-      t = fminf(fmaxf(t, 0.f), 1.f);
-      o[k] = (uint8_t)__float2int_rn(__fmul_rn(t, 255.f));  // round-half-even
+      }
     }
+  }
+  const int gy = y0 + ty, gx = x0 + tx4;
+  if (gy < H && gx + 3 < W) {
+    uint32_t q[3] = {0, 0, 0};
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float t = __fadd_rn(__fmul_rn(acc[p][k], 0.5f), 0.5f);
+        t = fminf(fmaxf(t, 0.f), 1.f);
+        const uint32_t u8 = (uint32_t)__float2int_rn(__fmul_rn(t, 255.f));  // round-half-even
+        const int byte = p * 3 + k;
+        q[byte >> 2] |= u8 << (8 * (byte & 3));
+      }
+    uint32_t* o = reinterpret_cast<uint32_t*>(rgb + (((size_t)img * H + gy) * W + gx) * 3);  // 4-byte aligned
+    o[0] = q[0];
+    o[1] = q[1];
+    o[2] = q[2];
   }
 }
 

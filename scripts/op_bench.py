@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--resid", action="store_true")
+    ap.add_argument("--fold", action="store_true", help="residual as an extra K segment (identity B)")
     ap.add_argument("--stats", action="store_true")
     ap.add_argument("--cg", type=int, default=0)
     ap.add_argument("--bn", type=int, default=0)
@@ -40,7 +41,7 @@ def main():
     if a.op in ("conv", "subpix", "gemm"):
         if a.op == "conv":
             K = 9 * c
-            w = (torch.randn(n, K, device=dev) * K ** -0.5).half()
+            w = (torch.randn(n, K + (n if a.fold else 0), device=dev) * K ** -0.5).half()
             out = torch.empty(b, hw, hw, n, dtype=torch.half, device=dev)
             M, mode, flops = b * hw * hw, 1, 2.0 * b * hw * hw * n * K
         elif a.op == "subpix":
@@ -57,9 +58,13 @@ def main():
         bias = torch.randn(n, device=dev)
         resid = torch.randn_like(out) if a.resid else None
 
+        fold = a.fold and a.op == "conv"
+        xr = torch.randn_like(out) if fold else None
+
         def run():
             stats.zero_()
-            lbx.op_gemm(mode, M, n, K, x.data_ptr(), K, w.data_ptr(), K, out.data_ptr(), n, b=b, h=hw, w=hw, c=c,
+            lbx.op_gemm(mode, M, n, K, x.data_ptr(), K, w.data_ptr(), K + (n if fold else 0), out.data_ptr(), n,
+                        b=b, h=hw, w=hw, c=c, a2=xr.data_ptr() if fold else 0, lda2=n, k2=n if fold else 0,
                         bias=bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
                         gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn)
     else:

@@ -25,4 +25,8 @@ def has_gpu() -> bool:
 def lbx():
     import paper_2605_19385_b200 as m
     m.lib()
+    dbg = os.environ.get("LBX_GEMM_DEBUG")  # "halo_policy,desc_base_mode" (diagnostic runs only)
+    if dbg:
+        h, d = (int(v) for v in dbg.split(","))
+        m.check(m.lib().lbx_op_set_debug(h, d))
     return m

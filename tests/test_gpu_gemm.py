@@ -138,3 +138,30 @@ def test_gn_stats_and_apply(lbx):
     torch.cuda.synchronize()
     ref = F.silu(F.group_norm(x.float().permute(0, 2, 1), 32, gamma, beta, 1e-6)).permute(0, 2, 1)
     _close(y, ref, rel=2e-3, abs_=2e-3)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("b,h,w,c,cin", [(2, 16, 256, 128, 128), (1, 16, 256, 128, 256), (1, 64, 64, 256, 512)])
+def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
+    """conv3x3(H) + X.W2^T as an extra K segment (identity -> residual, W_sc -> 1x1 shortcut)."""
+    n = c
+    hin = _rand(b, h, w, c, seed=21)
+    x = _rand(b, h, w, cin, seed=22)
+    wt = _rand(n, c, 3, 3, scale=(9 * c) ** -0.5, seed=23)
+    if cin == c:
+        wsc = torch.eye(c, device="cuda").half()
+    else:
+        wsc = _rand(n, cin, scale=cin ** -0.5, seed=24)
+    wk = torch.cat([wt.permute(0, 2, 3, 1).reshape(n, 9 * c), wsc], dim=1).contiguous()
+    bias = torch.randn(n, device="cuda")
+    out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
+    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    lbx.op_gemm(1, b * h * w, n, 9 * c, hin.data_ptr(), 0, wk.data_ptr(), 9 * c + cin, out.data_ptr(), n, b=b, h=h,
+                w=w, c=c, bias=bias.data_ptr(), gn_stats=stats.data_ptr(), cta_group=cg, a2=x.data_ptr(), lda2=cin,
+                k2=cin)
+    torch.cuda.synchronize()
+    ref = _conv_ref(hin, wt, bias) + (x.float().reshape(-1, cin) @ wsc.float().t()).reshape(b, h, w, n)
+    _close(out, ref)
+    o = out.double().reshape(b, h * w, 32, n // 32)
+    sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
+    torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
