@@ -1,0 +1,73 @@
+/*
+ * lbx/batcher.h -- multi-GPU decode-on-miss request batcher (north_star item 3).
+ *
+ * Replaces the simulator's GPU placement and FIFO service (proj/src/sim.cpp:238-243, 409-442) with
+ * real per-GPU queues.  One worker thread per device owns one lbx_decoder per latent shape class
+ * ("groups cache-miss decodes by latent shape").  An idle worker pulls the next batch, so a request
+ * goes to the least-loaded GPU, as least_loaded_gpu() picks the GPU with the smallest depth.  A batch
+ * closes when it reaches max_batch requests or its oldest request has waited max_wait_us.  Whole
+ * requests are never split across GPUs and there is no collective: one process drives all GPUs of a
+ * box, and requests are independent.
+ *
+ * Each completion carries the timestamps that Engine::on_job_done feeds to observe_latency:
+ * queue + batch wait = t_start - t_submit, and GPU = t_end - t_start (sim.cpp:438-440).
+ */
+#ifndef LBX_BATCHER_H
+#define LBX_BATCHER_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "lbx/reconstruct.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int family;                  /* lbx_family */
+  uint32_t latent_h, latent_w; /* latent shape of this class */
+} lbx_shape;
+
+typedef struct {
+  const int* devices;          /* CUDA ordinals, one worker per entry */
+  int n_devices;
+  const lbx_shape* shapes;     /* shape classes; a request names its class by index */
+  int n_shapes;
+  uint32_t max_batch;          /* per-launch batch cap (also the decoders' arena size) */
+  uint32_t max_wait_us;        /* close a partial batch once its oldest request waited this long */
+  uint64_t weight_seed;        /* decoder weights (deterministic generator) */
+} lbx_batcher_desc;
+
+typedef struct {
+  uint64_t request_id;
+  int status;                  /* lbx_status of the batch that carried the request */
+  int device;                  /* CUDA ordinal that decoded it */
+  uint32_t batch_size;         /* requests in that batch */
+  uint64_t t_submit_us, t_start_us, t_end_us; /* steady-clock microseconds */
+} lbx_completion;
+
+typedef struct lbx_batcher lbx_batcher;
+
+lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out);
+/* Stops the workers after draining queued requests, then frees everything. */
+lbx_status lbx_batcher_destroy(lbx_batcher* b);
+
+/* Enqueue one request.  The blob is copied.  rgb_out (8h x 8w x 3 bytes, host memory; pinned is
+ * fastest) must stay valid until the request's completion is returned by lbx_batcher_poll. */
+lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob, size_t nbytes,
+                              uint8_t* rgb_out);
+
+/* Up to cap completions.  Waits up to wait_us for the first one.  Returns the count (>= 0). */
+int lbx_batcher_poll(lbx_batcher* b, lbx_completion* out, int cap, uint32_t wait_us);
+
+/* Requests submitted but not yet returned by poll. */
+uint64_t lbx_batcher_pending(lbx_batcher* b);
+
+/* Steady-clock microseconds, the time base of lbx_completion. */
+uint64_t lbx_now_us(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBX_BATCHER_H */

@@ -84,6 +84,10 @@ lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uin
 lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                            uint8_t* rgb_host, lbx_stream stream);
 
+/* Vectored form: image i lands in rgb_hosts[i] (8h x 8w x 3 bytes each).  Synchronous. */
+lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                             uint8_t* const* rgb_hosts, lbx_stream stream);
+
 /* Same path from fp16 NCHW latents in HOST memory (no codec): H2D -> decode -> D2H.  Synchronous. */
 lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
                                    lbx_stream stream);

@@ -250,3 +250,88 @@ def op_groupnorm(x, y, stats, gamma, beta, b, hw, c, silu=True, eps=1e-6, stream
 
 def op_gn_stats(x, stats, b, hw, c, stream=0):
     check(lib().lbx_op_gn_stats(x, stats, b, hw, c, stream or None))
+
+
+# ---------------------------------------------------------------------------- batcher (batcher.h)
+class Shape(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int), ("latent_h", ctypes.c_uint32), ("latent_w", ctypes.c_uint32)]
+
+
+class BatcherDesc(ctypes.Structure):
+    _fields_ = [("devices", ctypes.POINTER(ctypes.c_int)), ("n_devices", ctypes.c_int),
+                ("shapes", ctypes.POINTER(Shape)), ("n_shapes", ctypes.c_int), ("max_batch", ctypes.c_uint32),
+                ("max_wait_us", ctypes.c_uint32), ("weight_seed", ctypes.c_uint64)]
+
+
+class Completion(ctypes.Structure):
+    _fields_ = [("request_id", ctypes.c_uint64), ("status", ctypes.c_int), ("device", ctypes.c_int),
+                ("batch_size", ctypes.c_uint32), ("t_submit_us", ctypes.c_uint64), ("t_start_us", ctypes.c_uint64),
+                ("t_end_us", ctypes.c_uint64)]
+
+
+def _batcher_lib():
+    L = lib()
+    if not getattr(L, "_batcher_ready", False):
+        vp = ctypes.c_void_p
+        L.lbx_batcher_create.argtypes = [ctypes.POINTER(BatcherDesc), ctypes.POINTER(vp)]
+        L.lbx_batcher_create.restype = ctypes.c_int
+        L.lbx_batcher_destroy.argtypes = [vp]
+        L.lbx_batcher_destroy.restype = ctypes.c_int
+        L.lbx_batcher_submit.argtypes = [vp, ctypes.c_uint64, ctypes.c_int, vp, ctypes.c_size_t, vp]
+        L.lbx_batcher_submit.restype = ctypes.c_int
+        L.lbx_batcher_poll.argtypes = [vp, ctypes.POINTER(Completion), ctypes.c_int, ctypes.c_uint32]
+        L.lbx_batcher_poll.restype = ctypes.c_int
+        L.lbx_batcher_pending.argtypes = [vp]
+        L.lbx_batcher_pending.restype = ctypes.c_uint64
+        L.lbx_now_us.restype = ctypes.c_uint64
+        L._batcher_ready = True
+    return L
+
+
+class Batcher:
+    """Multi-GPU request batcher: one worker + decoder per (device, shape class)."""
+
+    def __init__(self, devices, shapes, max_batch=32, max_wait_us=5000, seed=0):
+        L = _batcher_lib()
+        self._devs = (ctypes.c_int * len(devices))(*devices)
+        self._shapes = (Shape * len(shapes))(*[Shape(FAMILY[f], h, w) for f, h, w in shapes])
+        d = BatcherDesc(self._devs, len(devices), self._shapes, len(shapes), max_batch, max_wait_us, seed)
+        h = ctypes.c_void_p()
+        check(L.lbx_batcher_create(ctypes.byref(d), ctypes.byref(h)))
+        self._h = h
+        self._keep = {}
+
+    def submit(self, request_id: int, shape: int, blob: bytes, out: np.ndarray):
+        buf = np.frombuffer(blob, dtype=np.uint8)
+        self._keep[request_id] = out
+        check(_batcher_lib().lbx_batcher_submit(self._h, request_id, shape, buf.ctypes.data, buf.size,
+                                                out.ctypes.data))
+
+    def poll(self, cap=256, wait_us=1000):
+        arr = (Completion * cap)()
+        n = _batcher_lib().lbx_batcher_poll(self._h, arr, cap, wait_us)
+        res = []
+        for i in range(n):
+            c = arr[i]
+            self._keep.pop(c.request_id, None)
+            res.append({"id": c.request_id, "status": c.status, "device": c.device, "batch": c.batch_size,
+                        "t_submit": c.t_submit_us, "t_start": c.t_start_us, "t_end": c.t_end_us})
+        return res
+
+    def pending(self) -> int:
+        return int(_batcher_lib().lbx_batcher_pending(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _batcher_lib().lbx_batcher_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def now_us() -> int:
+    return int(_batcher_lib().lbx_now_us())

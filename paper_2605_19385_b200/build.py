@@ -68,5 +68,26 @@ def build(verbose: bool = False) -> str:
     return LIB
 
 
+
+
+def build_tools(verbose: bool = False) -> str:
+    """tools/c5_replay (config-5 trace replay harness), linked against the in-tree liblbx.so."""
+    tools = os.path.join(ROOT, "tools")
+    out = os.path.join(tools, "c5_replay")
+    srcs = [os.path.join(tools, f) for f in ("c5_replay.cpp", "lb_sim.cpp")]
+    deps = srcs + [os.path.join(tools, "lb_sim.hpp"), LIB]
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(p) for p in deps):
+        return out
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", tools] + srcs + [
+        "-L", HERE, "-llbx", "-Wl,-rpath,$ORIGIN/../paper_2605_19385_b200", "-lpthread", "-o", out]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"c5_replay build failed:\n{r.stderr}")
+    if verbose:
+        print(out)
+    return out
+
+
 if __name__ == "__main__":
     build(verbose=True)
+    build_tools(verbose=True)

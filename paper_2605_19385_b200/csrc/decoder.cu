@@ -42,6 +42,8 @@ static lbx_status set_err(lbx_status s, const std::string& m) {
   g_err = m;
   return s;
 }
+// For other translation units of the library (batcher.cpp): record an error on this thread.
+lbx_status set_last_error(lbx_status s, const std::string& m) { return set_err(s, m); }
 
 #define LBX_CUDA_TRY(expr)                                                                      \
   do {                                                                                          \
@@ -723,11 +725,18 @@ lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uin
   return d.run((int)n, reinterpret_cast<const __half*>(latents_dev), rgb_dev, pick(dec, stream));
 }
 
-static lbx_status finish_reconstruct(Decoder& d, uint32_t n, uint8_t* rgb_host, cudaStream_t s) {
+static lbx_status finish_reconstruct(Decoder& d, uint32_t n, uint8_t* rgb_host, cudaStream_t s,
+                                     uint8_t* const* rgb_hosts = nullptr) {
   lbx_status st = d.run((int)n, d.lat, d.rgb, s);
   if (st != LBX_OK) return st;
-  if (cudaMemcpyAsync(rgb_host, d.rgb, d.rgb_bytes(n), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+  if (rgb_hosts) {
+    const size_t per = d.rgb_bytes(1);
+    for (uint32_t i = 0; i < n; ++i)
+      if (cudaMemcpyAsync(rgb_hosts[i], d.rgb + i * per, per, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        return set_err(LBX_E_CUDA, "D2H of rgb failed");
+  } else if (cudaMemcpyAsync(rgb_host, d.rgb, d.rgb_bytes(n), cudaMemcpyDeviceToHost, s) != cudaSuccess) {
     return set_err(LBX_E_CUDA, "D2H of rgb failed");
+  }
   if (cudaMemcpyAsync(d.err_host, d.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return set_err(LBX_E_CUDA, "D2H of status failed");
   cudaError_t e = cudaStreamSynchronize(s);
@@ -751,6 +760,22 @@ lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const 
   lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
   if (st != LBX_OK) return st;
   return finish_reconstruct(d, n, rgb_host, s);
+}
+
+lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                             uint8_t* const* rgb_hosts, lbx_stream stream) {
+  if (!dec || !rgb_hosts) return set_err(LBX_E_CONFIG, "lbx_reconstruct_v: null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!rgb_hosts[i]) return set_err(LBX_E_CONFIG, "rgb_hosts: null entry");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  cudaStream_t s = pick(dec, stream);
+  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  if (st != LBX_OK) return st;
+  return finish_reconstruct(d, n, nullptr, s, rgb_hosts);
 }
 
 lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
