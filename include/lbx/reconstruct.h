@@ -68,6 +68,9 @@ lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t cou
 
 lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out);
 lbx_status lbx_decoder_destroy(lbx_decoder* dec);
+/* Capture (without running) the CUDA graphs of the host-buffer reconstruct path for every batch
+ * size 1..n_max, so the first request of each size does not pay graph capture (~tens of ms). */
+lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max);
 
 /* Packed LBLP blobs (HOST memory) -> fp16 NCHW latents on the device, bit-exact.  Blob shapes must
  * equal the decoder's (C, latent_h, latent_w).  Asynchronous on `stream`; a malformed blob is

@@ -27,7 +27,7 @@ _STATUS = {1: "LBX_E_RUNTIME", 2: "LBX_E_CONFIG", 3: "LBX_E_CUDA", 4: "LBX_E_FOR
 SYMBOLS = [
     "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
-    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc",
+    "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
 ]
 
 
@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_generate_params.argtypes = [i32, ctypes.c_uint64, vp, sz]
     L.lbx_decoder_create.argtypes = [ctypes.POINTER(_Desc), ctypes.POINTER(vp)]
     L.lbx_decoder_destroy.argtypes = [vp]
+    L.lbx_decoder_prepare.argtypes = [vp, u32]
     L.lbx_unpack.argtypes = [vp, vp, vp, u32, vp, vp]
     L.lbx_decode.argtypes = [vp, vp, u32, vp, vp]
     L.lbx_reconstruct.argtypes = [vp, vp, vp, u32, vp, vp]

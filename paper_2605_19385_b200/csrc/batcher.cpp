@@ -70,6 +70,7 @@ void lbx_batcher::worker(int di) {
     d.device = device;
     d.max_batch = desc.max_batch;
     st = lbx_decoder_create(&d, &decs[s]);
+    if (st == LBX_OK) st = lbx_decoder_prepare(decs[s], desc.max_batch);  // no capture on the request path
   }
   {
     std::lock_guard<std::mutex> g(mu);

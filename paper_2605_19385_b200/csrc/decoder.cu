@@ -145,6 +145,7 @@ class Decoder {
   lbx_status alloc_arena();
   lbx_status plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, bool counting);
   lbx_status run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s);
+  lbx_status graph_for(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, cudaGraphExec_t* out);
   lbx_status stage_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, cudaStream_t s);
 };
 
@@ -579,11 +580,12 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
 #undef LBX_LAUNCH
 }
 
-lbx_status Decoder::run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s) {
+lbx_status Decoder::graph_for(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, cudaGraphExec_t* out) {
   auto key = std::make_tuple(n, (const void*)lat_in, (const void*)rgb_out);
   auto it = graphs.find(key);
   if (it == graphs.end()) {
-    if (graphs.size() >= 16) {
+    // one graph per (batch size, buffers): the internal-buffer graphs of every n <= max_batch fit
+    if (graphs.size() >= (size_t)(2 * max_batch + 16)) {
       for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
       graphs.clear();
     }
@@ -602,7 +604,15 @@ lbx_status Decoder::run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStrea
     if (ce != cudaSuccess) return set_err(LBX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
     it = graphs.emplace(key, ex).first;
   }
-  LBX_CUDA_TRY(cudaGraphLaunch(it->second, s));
+  *out = it->second;
+  return LBX_OK;
+}
+
+lbx_status Decoder::run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s) {
+  cudaGraphExec_t ex = nullptr;
+  lbx_status st = graph_for(n, lat_in, rgb_out, s, &ex);
+  if (st != LBX_OK) return st;
+  LBX_CUDA_TRY(cudaGraphLaunch(ex, s));
   return LBX_OK;
 }
 
@@ -690,6 +700,20 @@ lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out) {
   }
   *out = dec;
   lbx::g_err.clear();
+  return LBX_OK;
+}
+
+lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max) {
+  if (!dec) return set_err(LBX_E_CONFIG, "lbx_decoder_prepare: null decoder");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n_max == 0 || (int)n_max > d.max_batch) return set_err(LBX_E_CONFIG, "n_max: must be in [1, desc.max_batch]");
+  cudaSetDevice(d.desc.device);
+  for (uint32_t n = 1; n <= n_max; ++n) {
+    cudaGraphExec_t ex = nullptr;
+    lbx_status st = d.graph_for((int)n, d.lat, d.rgb, d.stream, &ex);
+    if (st != LBX_OK) return st;
+  }
   return LBX_OK;
 }
 

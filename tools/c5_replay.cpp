@@ -36,8 +36,8 @@ struct Opts {
 };
 
 // Batch service curve measured on one B200 for 16x128x128 -> 1024^2 (lbx_reconstruct, host blobs,
-// r1 build); sizes 1,2,4,8,16,32.  Used by sim mode unless --service or live measurement overrides.
-const double kDefaultService[6] = {15.0, 26.0, 47.0, 88.0, 170.0, 335.0};
+// round-1 build, gpurun_out/c5_live_10x.err); sizes 1,2,4,8,16,32.  Used by sim mode unless --service or live measurement overrides.
+const double kDefaultService[6] = {9.40, 19.33, 40.27, 80.49, 165.76, 334.71};
 const int kSizes[6] = {1, 2, 4, 8, 16, 32};
 
 std::vector<double> curve_from(const double* pts, int maxb) {
