@@ -279,8 +279,10 @@ def main():
         with open(tp) as f:
             roof["traffic"] = json.load(f).get(dom_name)
     flop_img = FLOP_PER_IMG_1024[fam]
-    step_roof = {"algo_tflop_per_img": flop_img / 1e12, "achieved_tflops": value / world * flop_img / 1e12,
-                 "frac_of_peak": value / world * flop_img / 1e12 / peak, "tensor_kernel_share": tensor_ms / total_ms}
+    ach = value / world * flop_img / 1e12
+    step_roof = {"algo_tflop_per_img": flop_img / 1e12, "achieved_tflops": ach, "frac_of_peak": ach / peak,
+                 "frac_of_sustained_peak": ach / peak_sus, "tensor_kernel_share": tensor_ms / total_ms,
+                 "note": "whole decode (all kernels incl. GroupNorm/softmax/u8), per GPU, vs measured cuBLAS bf16"}
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
             json.dump({"groups": groups, "launches": prof}, f, indent=1)

@@ -153,6 +153,7 @@ typedef struct {
   float alpha;
   double* gn_stats;
   int cta_group, bn;
+  const float* gn_ss; /* optional: fused A' = SiLU(A * ss[img][c].x + ss[img][c].y) (conv3x3), float pairs */
 } lbx_gemm_desc;
 lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
 /* Diagnostics: halo_policy 0 forces per-tap A staging in the conv kernel (1 = halo when possible);

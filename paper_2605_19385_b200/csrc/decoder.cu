@@ -429,9 +429,12 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     ++launches;
     lbx_status e = chk(gemm_tc_launch(ga, s), what);
     if (e == LBX_OK && prof) {
-      const double fl = 2.0 * ga.M * (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1);  // 4 phases
+      const double fl_main = 2.0 * ga.M * (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1);  // 4 phases
+      const double fl = fl_main + 2.0 * ga.M * (double)ga.N * ga.K2;  // executed, incl. the folded K
       // algorithmic (standard) FLOPs: the sub-pixel form stands for nearest-2x + a full 3x3 conv
-      const double algo = ga.mode == GEMM_SUBPIX ? 2.0 * 4.0 * ga.M * (double)ga.N * 9.0 * ga.C : fl;
+      double algo = ga.mode == GEMM_SUBPIX ? 2.0 * 4.0 * ga.M * (double)ga.N * 9.0 * ga.C : fl_main;
+      // folded extra K: a 1x1 shortcut (K2 != N) is real algorithmic work; an identity residual is not
+      if (ga.K2 && ga.K2 != ga.N) algo += 2.0 * ga.M * (double)ga.N * ga.K2;
       char nm[160];
       if (ga.mode == GEMM_PLAIN)
         snprintf(nm, sizeof nm, "%s gemm M%d N%d K%d", what, ga.M, ga.N, ga.K);
@@ -473,28 +476,55 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   int x_site = site++;
   if ((st = conv3(A_, h, w, 64, conv_in, 512, X_, nullptr, x_site, "conv_in")) != LBX_OK) return st;
 
+  // GroupNorm + SiLU of a conv input: fused into the conv's A operand where the kernel supports it
+  // (halo staging, 256-wide N tiles, >= 256 input channels), else a separate apply pass.
+  auto gn_for_conv = [&](int st_site, const NormW& nw, const __half* x, __half* scratch, int C, int H, int W,
+                         int N, GemmArgs* g) -> lbx_status {
+    GemmArgs probe;
+    probe.mode = GEMM_CONV3X3;
+    probe.M = n * H * W; probe.N = N; probe.C = C; probe.W = W;
+    if (gemm_tc_can_fuse_gn(probe)) {
+      LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)H * W * (C / 32), 1e-6f, s),
+                 "gn_finalize", n * C * 8.0);
+      g->A = x;
+      g->gn_ss = ss;
+      return LBX_OK;
+    }
+    g->A = scratch;
+    return gn(st_site, nw, x, scratch, C, H * W, true);
+  };
+
   auto resnet = [&](const ResW& R, int H, int W) -> lbx_status {
     const int hw = H * W;
     lbx_status e;
-    if ((e = gn(x_site, R.n1, X_, A_, R.cin, hw, true)) != LBX_OK) return e;
     const int mid = site++;
-    if ((e = conv3(A_, H, W, R.cin, R.c1, R.cout, Hb, nullptr, mid, "resnet.conv1")) != LBX_OK) return e;
-    if ((e = gn(mid, R.n2, Hb, Hb, R.cout, hw, true)) != LBX_OK) return e;
-    // conv2 + (x or shortcut(x)): the residual is an extra K segment of the same tcgen05 GEMM.
-    // Same width: the output overwrites X in place (each tile reads only its own X rows, via TMA,
-    // before its epilogue writes them).  Cin != Cout: row strides differ, so a tile's output rows
-    // would land on other tiles' unread input rows -- write to A (free after conv1) and swap.
+    {  // conv1(SiLU(GN1(x)))
+      GemmArgs g;
+      g.mode = GEMM_CONV3X3;
+      g.M = n * hw; g.N = R.cout; g.K = 9 * R.cin;
+      g.B_img = n; g.H = H; g.W = W; g.C = R.cin;
+      g.Bw = R.c1.w; g.ldb = 9 * R.cin;
+      g.out = Hb; g.ldo = R.cout; g.bias = R.c1.b;
+      g.gn_stats = site_ptr(mid); g.gn_cpg = R.cout / 32; g.rows_per_img = hw;
+      if ((e = gn_for_conv(x_site, R.n1, X_, A_, R.cin, H, W, R.cout, &g)) != LBX_OK) return e;
+      if ((e = gemm(g, g.gn_ss ? "resnet.conv1+gn" : "resnet.conv1")) != LBX_OK) return e;
+    }
+    // conv2(SiLU(GN2(h))) + (x or shortcut(x)): the residual is an extra K segment of the same
+    // tcgen05 GEMM.  Same width: the output overwrites X in place (each tile reads only its own X
+    // rows, via TMA, before its epilogue writes them).  Cin != Cout: row strides differ, so a tile's
+    // output rows would land on other tiles' unread input rows -- write to A and swap.
     const int out_site = site++;
     {
       GemmArgs g;
       g.mode = GEMM_CONV3X3;
       g.M = n * hw; g.N = R.cout; g.K = 9 * R.cout;
-      g.A = Hb; g.B_img = n; g.H = H; g.W = W; g.C = R.cout;
+      g.B_img = n; g.H = H; g.W = W; g.C = R.cout;
       g.A2 = X_; g.lda2 = R.cin; g.K2 = R.cin;
       g.Bw = R.c2.w; g.ldb = 9 * R.cout + R.cin;
       g.out = R.cin == R.cout ? X_ : A_; g.ldo = R.cout; g.bias = R.c2.b;
       g.gn_stats = site_ptr(out_site); g.gn_cpg = R.cout / 32; g.rows_per_img = hw;
-      if ((e = gemm(g, "resnet.conv2+residual")) != LBX_OK) return e;
+      if ((e = gn_for_conv(mid, R.n2, Hb, Hb, R.cout, H, W, R.cout, &g)) != LBX_OK) return e;
+      if ((e = gemm(g, g.gn_ss ? "resnet.conv2+gn+residual" : "resnet.conv2+residual")) != LBX_OK) return e;
       if (R.cin != R.cout) std::swap(X_, A_);
     }
     x_site = out_site;
@@ -865,6 +895,7 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   g.resid = reinterpret_cast<const __half*>(d->resid); g.ldr = d->ldr;
   g.row_scale = d->row_scale; g.alpha = d->alpha;
   g.gn_stats = d->gn_stats; g.gn_cpg = d->N / 32;
+  g.gn_ss = reinterpret_cast<const float2*>(d->gn_ss);
   g.rows_per_img = (d->mode == 0) ? (d->b > 0 ? d->M / d->b : d->M) : d->h * d->w;
   cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), d->cta_group, d->bn);
   if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,

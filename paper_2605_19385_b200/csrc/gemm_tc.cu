@@ -52,6 +52,7 @@ struct KParams {
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
+  const float2* gn_ss; // fused GroupNorm+SiLU on A (XF kernels): per (image, channel) (scale, shift)
   int k_main;          // K of the main segment (B columns of the extra segment start here)
 };
 
@@ -120,7 +121,15 @@ __device__ __forceinline__ float chunk_group_stats(const uint32_t (&pk)[16], uin
   return x;
 }
 
-template <int BN, int CG>
+// SiLU for the fused A-operand transform: ex2 + rcp on the SFU (fp32-accurate to a few ulp).
+__device__ __forceinline__ float silu_xf(float y) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(y * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return y * r;
+}
+
+template <int BN, int CG, bool XF>
 __global__ void __launch_bounds__(352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const KParams p) {
@@ -135,7 +144,9 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* b_empty = b_full + kMaxStages;
   uint64_t* tfull = b_empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* a_xform = tempty + 2;  // XF: halo transformed (GroupNorm + SiLU applied) and fenced
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_xform + kMaxStages);
+  constexpr int EPI_WARPS = XF ? 4 : 8;  // XF: warps 6..9 transform A instead of draining TMEM
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -156,10 +167,11 @@ __global__ void __launch_bounds__(352, 1)
       ptx::mbar_init(&a_empty[s], 1);
       ptx::mbar_init(&b_full[s], 1);
       ptx::mbar_init(&b_empty[s], 1);
+      ptx::mbar_init(&a_xform[s], 4 * CG);
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 8 * CG);
+      ptx::mbar_init(&tempty[i], EPI_WARPS * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -190,7 +202,9 @@ __global__ void __launch_bounds__(352, 1)
         for (int j = 0; j < n_a; ++j) {
           ptx::mbar_wait(&a_empty[st], ph ^ 1);
           uint8_t* dst = sA + st * p.a_stage_bytes;
-          if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * p.a_tx_bytes);
+          // XF: each CTA's transform warps wait for their own halo, so A lands on the local barrier
+          if (XF) ptx::mbar_arrive_expect_tx(&a_full[st], p.a_tx_bytes);
+          else if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * p.a_tx_bytes);
           int c0 = 0, c1 = 0, c2 = 0, c3 = img;
           if (p.mode == GEMM_PLAIN) {
             c0 = j * 64;
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(352, 1)
             c1 = x0 - 1;
             c2 = p.mode == GEMM_CONV3X3 ? y0 - 1 : y0 + (phs >> 1) - 1;
             for (int sub = 1; sub < p.msub; ++sub) {
-              if constexpr (CG == 1) ptx::tma_load_4d(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
+              if constexpr (CG == 1 || XF) ptx::tma_load_4d(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
               else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
             }
           } else {
@@ -222,7 +236,7 @@ __global__ void __launch_bounds__(352, 1)
             if constexpr (CG == 1) ptx::tma_load_2d(&tmA, &a_full[st], dst, c0, c1);
             else ptx::tma_load_2d_pair(&tmA, &a_full[st], dst, c0, c1);
           } else {
-            if constexpr (CG == 1) ptx::tma_load_4d(&tmA, &a_full[st], dst, c0, c1, c2, c3);
+            if constexpr (CG == 1 || XF) ptx::tma_load_4d(&tmA, &a_full[st], dst, c0, c1, c2, c3);
             else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst, c0, c1, c2, c3);
           }
           if (++st == p.a_stages) { st = 0; ph ^= 1; }
@@ -230,9 +244,10 @@ __global__ void __launch_bounds__(352, 1)
         for (int e = 0; e < p.n_extra; ++e) {  // second operand: plain [M][K2] rows of this tile
           ptx::mbar_wait(&a_empty[st], ph ^ 1);
           uint8_t* dst = sA + st * p.a_stage_bytes;
-          if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * rows_cta * 64 * 2);
+          if (XF) ptx::mbar_arrive_expect_tx(&a_full[st], rows_cta * 64 * 2);
+          else if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * rows_cta * 64 * 2);
           for (int sub = 0; sub < p.msub; ++sub) {
-            if constexpr (CG == 1) ptx::tma_load_2d(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
+            if constexpr (CG == 1 || XF) ptx::tma_load_2d(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
             else ptx::tma_load_2d_pair(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
           }
           if (++st == p.a_stages) { st = 0; ph ^= 1; }
@@ -283,7 +298,8 @@ __global__ void __launch_bounds__(352, 1)
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * (p.msub * BN);
         for (int j = 0; j < n_a; ++j) {
-          ptx::mbar_wait(&a_full[as], aph);
+          if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
+          else ptx::mbar_wait(&a_full[as], aph);
           const uint32_t a_base = ptx::smem_u32(sA + as * p.a_stage_bytes);
           for (int tp = 0; tp < per_a; ++tp) {
             ptx::mbar_wait(&b_full[bs], bph);
@@ -312,7 +328,8 @@ __global__ void __launch_bounds__(352, 1)
           if (++as == p.a_stages) { as = 0; aph ^= 1; }
         }
         for (int e = 0; e < p.n_extra; ++e) {
-          ptx::mbar_wait(&a_full[as], aph);
+          if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
+          else ptx::mbar_wait(&a_full[as], aph);
           ptx::mbar_wait(&b_full[bs], bph);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
@@ -334,13 +351,87 @@ __global__ void __launch_bounds__(352, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (XF && warp >= 6) {
+    // ------------------------------------------------------------ fused GroupNorm + SiLU on A
+    // Warps 6..9 rewrite each landed halo in place: y = SiLU(x * a_c + b_c) (fp32 math, one fp16
+    // rounding) for pixels inside the image; out-of-image rows keep TMA's zero fill (padding comes
+    // after SiLU).  Thread t owns logical 16-byte chunk t & 7 (8 channels) of every 16th row, so its
+    // 8 (a, b) pairs load once per C-block; the physical chunk is (chunk ^ row & 7) (128B swizzle).
+    const int tid = (int)(warp - 6) * 32 + (int)lane;
+    const int cq = tid & 7;
+    const int rows = p.halo_rows * 130;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int t = cluster_id; t < p.tiles; t += nclusters) {
+      int m_tile, n_tile, phs;
+      tile_coords(p, t, m_tile, n_tile, phs);
+      const int rows_cta = 128 * p.msub;
+      const int m0 = m_tile * (rows_cta * CG) + rank * rows_cta;
+      const int hw = p.H * p.W;
+      const int img = m0 / hw;
+      const int rem = m0 - img * hw;
+      const int y0 = rem / p.W, x0 = rem - (rem / p.W) * p.W;
+      for (int j = 0; j < n_a + p.n_extra; ++j) {
+        float ca[8], cb[8];
+        if (j < n_a) {
+          const float4* cp = reinterpret_cast<const float4*>(p.gn_ss + (size_t)img * p.cblocks * 64 + j * 64 + cq * 8);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4 v = __ldg(cp + k);
+            ca[2 * k] = v.x; cb[2 * k] = v.y; ca[2 * k + 1] = v.z; cb[2 * k + 1] = v.w;
+          }
+        }
+        ptx::mbar_wait(&a_full[st], ph);
+        if (j < n_a) {
+          uint8_t* base = sA + st * p.a_stage_bytes;
+          for (int sub = 0; sub < p.msub; ++sub) {
+            uint8_t* hb = base + sub * p.halo_sub_bytes;
+            const int xs = x0 - 1 + sub * 128;
+            int hr = (tid >> 3) / 130, px = (tid >> 3) - hr * 130;
+            // two rows per iteration: 16 independent ex2/rcp chains per thread keep the SFU busy
+            for (int r = tid >> 3; r < rows; r += 32) {
+              int hr2 = hr, px2 = px + 16;
+              if (px2 >= 130) { px2 -= 130; ++hr2; }
+              const int r2 = r + 16;
+              const bool v1 = y0 - 1 + hr >= 0 && y0 - 1 + hr < p.H && xs + px >= 0 && xs + px < p.W;
+              const bool v2 = r2 < rows && y0 - 1 + hr2 >= 0 && y0 - 1 + hr2 < p.H && xs + px2 >= 0 && xs + px2 < p.W;
+              uint4* q1 = reinterpret_cast<uint4*>(hb + r * 128 + ((cq ^ (r & 7)) << 4));
+              uint4* q2 = reinterpret_cast<uint4*>(hb + r2 * 128 + ((cq ^ (r2 & 7)) << 4));
+              const uint4 u1 = v1 ? *q1 : make_uint4(0, 0, 0, 0);
+              const uint4 u2 = v2 ? *q2 : make_uint4(0, 0, 0, 0);
+              uint32_t w[8] = {u1.x, u1.y, u1.z, u1.w, u2.x, u2.y, u2.z, u2.w};
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const int c = k & 3;
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+                const __half2 h = __floats2half2_rn(silu_xf(fmaf(f.x, ca[2 * c], cb[2 * c])),
+                                                    silu_xf(fmaf(f.y, ca[2 * c + 1], cb[2 * c + 1])));
+                w[k] = *reinterpret_cast<const uint32_t*>(&h);
+              }
+              if (v1) *q1 = make_uint4(w[0], w[1], w[2], w[3]);
+              if (v2) *q2 = make_uint4(w[4], w[5], w[6], w[7]);
+              px = px2 + 16;
+              hr = hr2;
+              if (px >= 130) { px -= 130; ++hr; }
+            }
+          }
+          ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) ptx::mbar_arrive(&a_xform[st]);
+          else ptx::mbar_arrive_cluster(&a_xform[st], 0);
+        }
+        if (++st == p.a_stages) { st = 0; ph ^= 1; }
+      }
+    }
   } else {
     // ------------------------------------------------------------ epilogue (warps 2..9)
     // Two warps per TMEM lane quarter; warp half `hsel` takes the even/odd 32-column chunks.
     const uint32_t q = warp & 3;
-    const int hsel = (int)(warp - 2) >> 2;
+    const int hsel = XF ? 0 : (int)(warp - 2) >> 2;
     const int row = q * 32 + lane;
-    constexpr int NCH = BN / 64;  // chunks per warp per tile
+    constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
     // GroupNorm partials: after the per-chunk reduce-scatter each lane owns one (group, sum|sumsq)
     // value per chunk; lanes accumulate those across tiles in fp64 registers and flush with one
     // atomic per owned value only when the (image, n-tile) changes -- not once per tile.
@@ -360,7 +451,7 @@ __global__ void __launch_bounds__(352, 1)
         const int g_in = own - kind * gpc;
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
-          const int c = hsel + 2 * j;
+          const int c = hsel + (EPI_WARPS / 4) * j;
           const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + g_in;
           atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, gacc[j]);
         }
@@ -400,16 +491,17 @@ __global__ void __launch_bounds__(352, 1)
       constexpr int PF = NCH < 2 ? NCH : 2;
       uint4 rr[PF][4];
       const __half* rbase = p.resid ? p.resid + orow * p.ldr + n0 + hsel * 32 : nullptr;
+      constexpr int RSTRIDE = 32 * (EPI_WARPS / 4);  // columns between this warp's chunks
       if (p.resid) {
 #pragma unroll
         for (int j = 0; j < PF; ++j)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) rr[j][i] = __ldg(reinterpret_cast<const uint4*>(rbase + j * 64) + i);
+          for (int i = 0; i < 4; ++i) rr[j][i] = __ldg(reinterpret_cast<const uint4*>(rbase + j * RSTRIDE) + i);
       }
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * (p.msub * BN) + sub * BN;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        const int c = hsel + 2 * j;
+        const int c = hsel + (EPI_WARPS / 4) * j;
         const int n = n0 + c * 32;
         uint32_t r[32];
         ptx::tmem_ld32(t_row + c * 32, r);
@@ -439,7 +531,7 @@ __global__ void __launch_bounds__(352, 1)
           if (j + PF < NCH) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              rr[j % PF][i] = __ldg(reinterpret_cast<const uint4*>(rbase + (j + PF) * 64) + i);
+              rr[j % PF][i] = __ldg(reinterpret_cast<const uint4*>(rbase + (j + PF) * RSTRIDE) + i);
           }
         }
         uint32_t pk[16];
@@ -521,7 +613,7 @@ static bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_
   return r == CUDA_SUCCESS;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
   // ---- operand staging plan
@@ -538,7 +630,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   if (kp.a_stages > kMaxStages) kp.a_stages = kMaxStages;
   if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
   if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
-  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (4 * kMaxStages + 4) * 8 + 16;
+  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16;
   if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
 
   CUtensorMap tmA, tmB;
@@ -569,7 +661,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     cuuint32_t box[2] = {64, (cuuint32_t)Cf::B_ROWS};
     if (!make_map(&tmB, a.Bw, 2, dims, strides, box)) return cudaErrorInvalidValue;
   }
-  auto kern = gemm_tc_kernel<BN, CG>;
+  auto kern = gemm_tc_kernel<BN, CG, XF>;
   const int sms = num_sms();
   int clusters = sms / CG;
   if (clusters > kp.tiles) clusters = kp.tiles;
@@ -590,7 +682,9 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
 
 template <int BN, int CG>
 static bool set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Cfg<BN, CG>::SMEM_MAX) == cudaSuccess &&
+         cudaFuncSetAttribute(gemm_tc_kernel<BN, CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               Cfg<BN, CG>::SMEM_MAX) == cudaSuccess;
 }
 
@@ -607,11 +701,20 @@ bool gemm_tc_prepare() {
 
 static int g_halo_policy = 1;      // 1: use halo staging whenever the geometry allows
 static int g_msub_policy = 1;      // 1: two M sub-tiles per CTA for BN = 128 halo convs
+static int g_fuse_policy = 0;      // fused GroupNorm+SiLU on A: off by default (measured slower)
 static int g_desc_base_mode = 0;   // descriptor base-offset convention for row-shifted A views
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_halo_policy = halo_policy & 1;
-  g_msub_policy = (halo_policy >> 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
+  g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
+  g_fuse_policy = (halo_policy >> 2) & 1;  // bit 2 enables fused GroupNorm on A in the decoder
   g_desc_base_mode = desc_base_mode;
+}
+
+bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
+  // halo staging (128-pixel row segments) and 256-wide N tiles: the four borrowed epilogue warps
+  // have slack there, and the SFU budget of the transform (2 ops / element) fits under the MMAs
+  return g_fuse_policy && g_halo_policy && a.mode == GEMM_CONV3X3 && a.W >= 128 && a.W % 128 == 0 &&
+         a.N % 256 == 0 && a.C >= 256 && a.C % 64 == 0 && a.M % 256 == 0;
 }
 
 cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg, int force_bn) {
@@ -658,10 +761,18 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.m_tiles = a.M / (128 * cg * kp.msub);
   kp.n_tiles = a.N / bn;
   kp.tiles = kp.m_tiles * kp.n_tiles * (a.mode == GEMM_SUBPIX ? 4 : 1);
-  if (bn == 256 && cg == 2) return launch_cfg<256, 2>(a, kp, stream);
-  if (bn == 128 && cg == 2) return launch_cfg<128, 2>(a, kp, stream);
-  if (bn == 256 && cg == 1) return launch_cfg<256, 1>(a, kp, stream);
-  return launch_cfg<128, 1>(a, kp, stream);
+  if (a.gn_ss) {  // fused GroupNorm + SiLU on the A operand: conv3x3 halo staging only
+    if (a.mode != GEMM_CONV3X3 || !kp.halo) return cudaErrorInvalidValue;
+    kp.gn_ss = a.gn_ss;
+    if (bn == 256 && cg == 2) return launch_cfg<256, 2, true>(a, kp, stream);
+    if (bn == 128 && cg == 2) return launch_cfg<128, 2, true>(a, kp, stream);
+    if (bn == 256 && cg == 1) return launch_cfg<256, 1, true>(a, kp, stream);
+    return launch_cfg<128, 1, true>(a, kp, stream);
+  }
+  if (bn == 256 && cg == 2) return launch_cfg<256, 2, false>(a, kp, stream);
+  if (bn == 128 && cg == 2) return launch_cfg<128, 2, false>(a, kp, stream);
+  if (bn == 256 && cg == 1) return launch_cfg<256, 1, false>(a, kp, stream);
+  return launch_cfg<128, 1, false>(a, kp, stream);
 }
 
 }  // namespace lbx

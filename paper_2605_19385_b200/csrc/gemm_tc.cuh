@@ -27,6 +27,9 @@ struct GemmArgs {
   // conv (B = W_sc) into the tensor-core accumulation instead of the epilogue.
   const __half* A2 = nullptr;
   int lda2 = 0, K2 = 0;
+  // optional fused GroupNorm + SiLU on the A operand (conv3x3 halo mode): A' = SiLU(A * a_c + b_c),
+  // (a_c, b_c) = gn_ss[image][channel]; out-of-image padding stays zero (applied after SiLU).
+  const float2* gn_ss = nullptr;
   // B operand: weights [N][K + K2] K-major (conv: K index = (ky*3+kx)*C + ci)
   const __half* Bw = nullptr;
   int ldb = 0;
@@ -45,6 +48,9 @@ struct GemmArgs {
 
 // Launch on `stream`.  Returns cudaSuccess or the launch error.  Chooses tile / CTA-pair config.
 cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg = 0, int force_bn = 0);
+
+// True when a conv3x3 launch of this geometry can fuse GroupNorm + SiLU into its A operand.
+bool gemm_tc_can_fuse_gn(const GemmArgs& a);
 
 // Diagnostics: halo_policy 0 forces per-tap A staging; desc_base_mode selects the UMMA descriptor
 // base-offset convention for row-shifted (non-1024-aligned) halo views.

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--resid", action="store_true")
     ap.add_argument("--fold", action="store_true", help="residual as an extra K segment (identity B)")
     ap.add_argument("--stats", action="store_true")
+    ap.add_argument("--gnfuse", action="store_true", help="fused GroupNorm+SiLU on the A operand")
     ap.add_argument("--cg", type=int, default=0)
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--iters", type=int, default=3)
@@ -59,6 +60,7 @@ def main():
         resid = torch.randn_like(out) if a.resid else None
 
         fold = a.fold and a.op == "conv"
+        gss = (torch.rand(b, c, 2, device=dev) + 0.5) if a.gnfuse else None
         xr = torch.randn_like(out) if fold else None
 
         def run():
@@ -66,7 +68,8 @@ def main():
             lbx.op_gemm(mode, M, n, K, x.data_ptr(), K, w.data_ptr(), K + (n if fold else 0), out.data_ptr(), n,
                         b=b, h=hw, w=hw, c=c, a2=xr.data_ptr() if fold else 0, lda2=n, k2=n if fold else 0,
                         bias=bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
-                        gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn)
+                        gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn,
+                        gn_ss=gss.data_ptr() if gss is not None else 0)
     else:
         gamma = torch.ones(c, device=dev)
         beta = torch.zeros(c, device=dev)

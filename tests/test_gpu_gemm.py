@@ -165,3 +165,34 @@ def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
     o = out.double().reshape(b, h * w, 32, n // 32)
     sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
     torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("b,h,w,c,n,fold", [(2, 16, 128, 256, 256, False), (1, 16, 256, 512, 512, True),
+                                            (2, 8, 256, 256, 256, True)])
+def test_conv3x3_fused_groupnorm_silu(lbx, cg, b, h, w, c, n, fold):
+    """A' = SiLU(A * a[img, c] + b[img, c]) applied to the halo in smem; padding stays zero."""
+    x = _rand(b, h, w, c, seed=41) * 2 + 0.3
+    g = torch.Generator(device="cpu").manual_seed(42)
+    ss = torch.stack([torch.rand(b, c, generator=g) + 0.5, torch.randn(b, c, generator=g) * 0.5], dim=-1).cuda()
+    wt = _rand(n, c, 3, 3, scale=(9 * c) ** -0.5, seed=43)
+    wk = wt.permute(0, 2, 3, 1).reshape(n, 9 * c)
+    xr = _rand(b, h, w, n, seed=44) if fold else None
+    if fold:
+        wk = torch.cat([wk, torch.eye(n, device="cuda").half()], dim=1)
+    wk = wk.contiguous()
+    bias = torch.randn(n, device="cuda")
+    out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
+    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    lbx.op_gemm(1, b * h * w, n, 9 * c, x.data_ptr(), 0, wk.data_ptr(), wk.shape[1], out.data_ptr(), n, b=b, h=h,
+                w=w, c=c, bias=bias.data_ptr(), gn_stats=stats.data_ptr(), cta_group=cg, gn_ss=ss.data_ptr(),
+                a2=xr.data_ptr() if fold else 0, lda2=n if fold else 0, k2=n if fold else 0)
+    torch.cuda.synchronize()
+    act = F.silu(x.float() * ss[:, None, None, :, 0] + ss[:, None, None, :, 1]).half()  # fp16 like the kernel
+    ref = _conv_ref(act, wt, bias)
+    if fold:
+        ref = ref + xr.float()
+    _close(out, ref, rel=3e-3)
+    o = out.double().reshape(b, h * w, 32, n // 32)
+    sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
+    torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
