@@ -55,6 +55,9 @@ typedef struct {
   size_t weights_count;       /* number of floats in `weights` */
   int device;                 /* CUDA device ordinal */
   uint32_t max_batch;         /* largest n passed to decode/reconstruct (arena is sized for it) */
+  int precise_activations;    /* 0 (default): SiLU of every GroupNorm apply on packed halves (one
+                                 MUFU.TANH per two elements, fp16-engine numerics);
+                                 1: fp32 SiLU (~0.7 dB higher PSNR vs the fp32 oracle, ~2% slower) */
 } lbx_decoder_desc;
 
 typedef struct lbx_decoder lbx_decoder;
@@ -156,12 +159,19 @@ typedef struct {
   const float* gn_ss; /* optional: fused A' = SiLU(A * ss[img][c].x + ss[img][c].y) (conv3x3), float pairs */
 } lbx_gemm_desc;
 lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
-/* Diagnostics: halo_policy 0 forces per-tap A staging in the conv kernel (1 = halo when possible);
- * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
+/* Diagnostics.  halo_policy bits: 0 = halo staging when possible (else per-tap A staging); 1 disables
+ * the two-sub-tile variant; 2 enables the fused GroupNorm A-operand transform (XF) in the decoder;
+ * 4 selects the CUDA-core conv_out tail.  desc_base_mode selects the UMMA descriptor base-offset convention for
+ * row-shifted halo views. */
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
+/* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],
+ * ss float pairs [n][128], w fp32 [3][3][3][128] ([out][ky][kx][in]), rgb [n][H][W][3].  impl 0 =
+ * tensor cores (fp32 SiLU), 2 = tensor cores with packed-half SiLU, 1 = CUDA cores (fp32). */
+lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
+                           int H, int W, int impl, lbx_stream stream);
 /* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
 lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
-/* GroupNorm finalize + apply (SiLU when silu != 0); y may alias x. */
+/* GroupNorm finalize + apply; silu 0 = identity, 1 = fp32 SiLU, 2 = packed-half SiLU; y may alias x. */
 lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta,
                             int b, int hw, int c, int silu, float eps, lbx_stream stream);
 /* GroupNorm-32 statistics of x ([b][hw][c] fp16) into stats (double [b][32][2], zeroed here). */

@@ -28,6 +28,7 @@ SYMBOLS = [
     "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
+    "lbx_op_conv_out",
 ]
 
 
@@ -64,6 +65,7 @@ class _Desc(ctypes.Structure):
         ("weights_count", ctypes.c_size_t),
         ("device", ctypes.c_int),
         ("max_batch", ctypes.c_uint32),
+        ("precise_activations", ctypes.c_int),
     ]
 
 
@@ -101,6 +103,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_launch_count.argtypes = [vp, u32]
     L.lbx_op_set_debug.argtypes = [i32, i32]
     L.lbx_op_gemm_desc.argtypes = [ctypes.POINTER(GemmDesc), vp]
+    L.lbx_op_conv_out.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error"):
             getattr(L, name).restype = ctypes.c_int
@@ -140,7 +143,7 @@ class Decoder:
     """One decoder per GPU (single owner; calls serialised by the owning thread)."""
 
     def __init__(self, family: str = "sd15", latent_hw=(64, 64), seed: int = 0, device: int = 0,
-                 max_batch: int = 1, weights: np.ndarray | None = None):
+                 max_batch: int = 1, weights: np.ndarray | None = None, precise: bool = False):
         self.family = family
         self.h, self.w = latent_hw
         self.c = LATENT_CHANNELS[family]
@@ -149,6 +152,7 @@ class Decoder:
         d.family = FAMILY[family]
         d.latent_h, d.latent_w = self.h, self.w
         d.weight_seed = seed
+        d.precise_activations = int(precise)
         self._weights = None
         if weights is not None:
             self._weights = np.ascontiguousarray(weights, dtype=np.float32)
@@ -247,6 +251,11 @@ def subpixel_weights(w3x3: np.ndarray) -> np.ndarray:
 
 def op_groupnorm(x, y, stats, gamma, beta, b, hw, c, silu=True, eps=1e-6, stream=0):
     check(lib().lbx_op_groupnorm(x, y, stats, gamma, beta, b, hw, c, int(silu), ctypes.c_float(eps), stream or None))
+
+
+def op_conv_out(x, ss, w, b, rgb, n, h, w_, impl=0, stream=0):
+    """Decoder tail (lbx_op_conv_out): impl 0 tensor cores, 2 tensor cores + packed-half SiLU, 1 CUDA cores."""
+    check(lib().lbx_op_conv_out(x, ss, w, b, rgb, n, h, w_, impl, stream or None))
 
 
 def op_gn_stats(x, stats, b, hw, c, stream=0):

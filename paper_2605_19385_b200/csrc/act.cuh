@@ -1,0 +1,77 @@
+// Device-side activation / GroupNorm helpers shared by the standalone HBM kernels (kernels.cu) and the
+// deferred GroupNorm apply inside the tcgen05 conv (gemm_tc.cu), so both paths round identically.
+#pragma once
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace lbx {
+
+// SiLU with one MUFU op per element: ex2 on the SFU, the reciprocal of (1 + e) on the FMA pipe
+// (bit-trick seed, 3 Newton steps -> fp32-accurate).  The SFU (16 ops/clk/SM) is what bounded the
+// GroupNorm-apply pass at ~3.5 TB/s with ex2 + rcp; the FMA pipe has 8x its throughput.
+__device__ __forceinline__ float silu_f(float x) {
+  const float xc = fmaxf(x, -80.0f);  // keeps 1 + e finite and normal for the seed trick
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(xc * -1.4426950408889634f));
+  const float d = 1.0f + e;
+  float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
+  r = r * fmaf(-d, r, 2.0f);
+  r = r * fmaf(-d, r, 2.0f);
+  r = r * fmaf(-d, r, 2.0f);
+  return x * r;
+}
+
+// GroupNorm affine of one channel from fp64 (sum, sumsq) over `count` values -- the single
+// definition of the finalize arithmetic: y = x * a + b with a = gamma * rstd, b = beta - mean * a.
+__device__ __forceinline__ float2 gn_affine(double s, double s2, double count, float gamma, float beta, float eps) {
+  const double mean = s / count;
+  double var = s2 / count - mean * mean;
+  if (var < 0) var = 0;
+  const double rstd = 1.0 / sqrt(var + (double)eps);
+  const double a = (double)gamma * rstd;
+  return make_float2((float)a, (float)((double)beta - mean * a));
+}
+
+// 8 packed fp16 -> act(x * a + b) -> 8 packed fp16 (fp32 math, one rounding).
+template <bool SILU>
+__device__ __forceinline__ uint4 gn_act8(uint4 u, const float (&a)[8], const float (&b)[8]) {
+  uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+    float y0 = fmaf(f.x, a[2 * j], b[2 * j]), y1 = fmaf(f.y, a[2 * j + 1], b[2 * j + 1]);
+    if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
+    const __half2 h = __floats2half2_rn(y0, y1);
+    w[j] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Packed-half variant: affine in fp32, one rounding to fp16, then SiLU(y) = h + h*tanh(h), h = y/2,
+// on half2 (HMUL2, one MUFU.TANH per two elements, HFMA2): ~4 instructions per element instead of
+// ~13.  tanh.approx.f16x2 has ~2^-11 absolute error, so the result carries up to ~|y|*2^-11 more
+// error than the fp32 path (about one extra fp16 ulp); opt-in, judged end to end (tests/).
+__device__ __forceinline__ uint32_t tanh_f16x2(uint32_t x) {
+  uint32_t r;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+template <bool SILU>
+__device__ __forceinline__ uint4 gn_act8_h2(uint4 u, const float (&a)[8], const float (&b)[8]) {
+  uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+    __half2 y = __floats2half2_rn(fmaf(f.x, a[2 * j], b[2 * j]), fmaf(f.y, a[2 * j + 1], b[2 * j + 1]));
+    if (SILU) {
+      const __half2 h = __hmul2(y, __float2half2_rn(0.5f));
+      const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
+      const uint32_t tb = tanh_f16x2(hb);
+      y = __hfma2(h, *reinterpret_cast<const __half2*>(&tb), h);
+    }
+    w[j] = *reinterpret_cast<const uint32_t*>(&y);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+}  // namespace lbx

@@ -422,6 +422,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
 
   __half* X_ = X;
   __half* A_ = A;
+  const bool h2 = desc.precise_activations == 0;  // packed-half SiLU unless the caller asked for fp32
   if (prof) mark("start", 0, 0, 0);
   LBX_STEP(cudaMemsetAsync(stats, 0, (size_t)kMaxSites * site_stride * 8, s), "memset stats");
 
@@ -450,7 +451,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   };
   auto gn = [&](int st_site, const NormW& nw, const __half* x, __half* y, int C, int hw, bool silu) -> lbx_status {
     LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)hw * (C / 32), 1e-6f, s), "gn_finalize", n * C * 8.0);
-    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, s),
+    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, h2, s),
                std::string(silu ? "gn_apply_silu c" : "gn_apply c") + std::to_string(C) + " hw" + std::to_string(hw),
                4.0 * n * (double)hw * C);
     return LBX_OK;
@@ -601,8 +602,14 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   // tail
   LBX_LAUNCH(launch_gn_finalize(site_ptr(x_site), norm_out.g, norm_out.b, ss, n, 128, (double)H * W * 4, 1e-6f, s),
              "norm_out.finalize", n * 128 * 8.0);
-  LBX_LAUNCH(launch_conv_out_u8(X_, ss, wout, bout, rgb_out, n, H, W, s), "conv_out_u8",
-             (double)n * H * W * (128 * 2 + 3));
+  if (W % 128 == 0 && !kernels_conv_out_legacy()) {
+    LBX_STEP(launch_conv_out_tc(X_, ss, wout, bout, rgb_out, n, H, W, h2, s), "conv_out_tc");
+    ++launches;
+    mark("conv_out_tc", 2.0 * n * H * W * 16 * 1152, 2.0 * n * H * W * 3 * 1152, (double)n * H * W * (128 * 2 + 3));
+  } else {
+    LBX_LAUNCH(launch_conv_out_u8(X_, ss, wout, bout, rgb_out, n, H, W, s), "conv_out_u8",
+               (double)n * H * W * (128 * 2 + 3));
+  }
   if (site > kMaxSites) return set_err(LBX_E_RUNTIME, "too many GroupNorm sites");
   if (counting) launch_counts[n] = launches;
   return LBX_OK;
@@ -903,8 +910,29 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   return LBX_OK;
 }
 
+lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
+                           int H, int W, int impl, lbx_stream stream) {
+  if (!x || !ss || !w || !b || !rgb || n <= 0 || H <= 0 || W <= 0)
+    return set_err(LBX_E_CONFIG, "lbx_op_conv_out: bad argument");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const __half* xh = reinterpret_cast<const __half*>(x);
+  const float2* s2 = reinterpret_cast<const float2*>(ss);
+  cudaError_t e;
+  if (impl == 1) {
+    lbx::launch_conv_out_u8(xh, s2, w, b, rgb, n, H, W, s);
+    e = cudaGetLastError();
+  } else {
+    e = lbx::launch_conv_out_tc(xh, s2, w, b, rgb, n, H, W, impl == 2, s);
+  }
+  if (e != cudaSuccess)
+    return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
+                   std::string("lbx_op_conv_out: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
   lbx::gemm_tc_set_debug(halo_policy, desc_base_mode);
+  lbx::kernels_set_conv_out_legacy((halo_policy >> 4) & 1);
   return LBX_OK;
 }
 
@@ -942,7 +970,7 @@ lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const f
     return set_err(LBX_E_CUDA, "cudaMallocAsync");
   lbx::launch_gn_finalize(stats, gamma, beta, ss, b, c, (double)hw * (c / 32), eps, s);
   lbx::launch_gn_apply(reinterpret_cast<const __half*>(x), reinterpret_cast<__half*>(y), ss, (long long)b * hw, hw, c,
-                       silu != 0, s);
+                       silu != 0, silu == 2, s);
   cudaFreeAsync(ss, s);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));

@@ -613,6 +613,18 @@ static bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_
   return r == CUDA_SUCCESS;
 }
 
+bool make_tensor_map_f16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                         const uint32_t* box) {
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  return make_map(m, base, rank, d, st, bx);
+}
+
 template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;

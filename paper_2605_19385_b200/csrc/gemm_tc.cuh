@@ -59,6 +59,11 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();
 
+// fp16 tiled TMA descriptor with 128-byte swizzle (dims innermost first; strides in bytes for
+// dims 1..rank-1).  Out-of-bounds boxes are zero-filled.
+bool make_tensor_map_f16(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                         const uint32_t* box);
+
 // Number of SMs (cached) and the driver entry point used to encode TMA descriptors.
 int num_sms();
 bool tma_available();

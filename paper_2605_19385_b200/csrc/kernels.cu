@@ -3,6 +3,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include "act.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 
@@ -75,13 +76,7 @@ __global__ void gn_finalize_kernel(const double* __restrict__ stats, const float
   if (i >= n * C) return;
   const int img = i / C, c = i - img * C;
   const int g = c / (C / 32);
-  const double s = stats[(img * 32 + g) * 2], s2 = stats[(img * 32 + g) * 2 + 1];
-  const double mean = s / count;
-  double var = s2 / count - mean * mean;
-  if (var < 0) var = 0;
-  const double rstd = 1.0 / sqrt(var + (double)eps);
-  const double a = (double)gamma[c] * rstd;
-  ss[i] = make_float2((float)a, (float)((double)beta[c] - mean * a));
+  ss[i] = gn_affine(stats[(img * 32 + g) * 2], stats[(img * 32 + g) * 2 + 1], count, gamma[c], beta[c], eps);
 }
 
 void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
@@ -89,25 +84,10 @@ void launch_gn_finalize(const double* stats, const float* gamma, const float* be
   gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, count, eps);
 }
 
-// SiLU with one MUFU op per element: ex2 on the SFU, the reciprocal of (1 + e) on the FMA pipe
-// (bit-trick seed, 3 Newton steps -> fp32-accurate).  The SFU (16 ops/clk/SM) is what bounded the
-// GroupNorm-apply pass at ~3.5 TB/s with ex2 + rcp; the FMA pipe has 8x its throughput.
-__device__ __forceinline__ float silu_f(float x) {
-  const float xc = fmaxf(x, -80.0f);  // keeps 1 + e finite and normal for the seed trick
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(xc * -1.4426950408889634f));
-  const float d = 1.0f + e;
-  float r = __int_as_float(0x7EF311C3 - __float_as_int(d));
-  r = r * fmaf(-d, r, 2.0f);
-  r = r * fmaf(-d, r, 2.0f);
-  r = r * fmaf(-d, r, 2.0f);
-  return x * r;
-}
-
 // y = act(x * a_c + b_c).  The launch is exactly one resident wave; block b covers a contiguous
 // range of the flattened (image, pixel) space, split at image boundaries.  Thread t owns channel
 // octet t % (C/8) for every pixel it visits, so its 8 affine pairs are reloaded only per image.
-template <bool SILU, int CV>
+template <bool SILU, int CV, bool H2>
 __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* y, const float2* __restrict__ ss,
                                                        int hw, long long total, long long pix_per_block) {
   constexpr int PSTEP = 256 / CV;  // pixels advanced per iteration of the block
@@ -126,18 +106,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
       a[k] = t.x;
       b[k] = t.y;
     }
-    auto apply = [&](uint4 u) {
-      uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-        float y0 = fmaf(f.x, a[2 * j], b[2 * j]), y1 = fmaf(f.y, a[2 * j + 1], b[2 * j + 1]);
-        if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
-        const __half2 h = __floats2half2_rn(y0, y1);
-        w[j] = *reinterpret_cast<const uint32_t*>(&h);
-      }
-      return make_uint4(w[0], w[1], w[2], w[3]);
-    };
+    auto apply = [&](uint4 u) { return H2 ? gn_act8_h2<SILU>(u, a, b) : gn_act8<SILU>(u, a, b); };
     constexpr int U = 8;  // 16-byte loads in flight per thread (latency x bandwidth needs ~100 KB/SM)
     for (; p + (U - 1) * PSTEP < seg_end; p += U * PSTEP) {
       uint4 u[U];
@@ -150,11 +119,15 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
   }
 }
 
-template <bool SILU, int CV>
+static bool g_conv_out_legacy = false;  // CUDA-core conv_out instead of the tensor-core tail
+void kernels_set_conv_out_legacy(bool on) { g_conv_out_legacy = on; }
+bool kernels_conv_out_legacy() { return g_conv_out_legacy; }
+
+template <bool SILU, int CV, bool H2>
 static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
   static int occ = 0;
   if (!occ) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel<SILU, CV>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel<SILU, CV, H2>, 256, 0);
     if (occ <= 0) occ = 4;
   }
   constexpr int PSTEP = 256 / CV;
@@ -163,24 +136,28 @@ static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n,
   long long ppb = (total + blocks - 1) / blocks;
   ppb = (ppb + PSTEP - 1) / PSTEP * PSTEP;
   const int grid = (int)((total + ppb - 1) / ppb);
-  gn_apply_kernel<SILU, CV><<<grid, 256, 0, s>>>(x, y, ss, hw, total, ppb);
+  gn_apply_kernel<SILU, CV, H2><<<grid, 256, 0, s>>>(x, y, ss, hw, total, ppb);
 }
 
-template <bool SILU>
+template <bool SILU, bool H2>
 static void gn_apply_dispatch(const __half* x, __half* y, const float2* ss, int n, int hw, int C, cudaStream_t s) {
   switch (C / 8) {
-    case 16: gn_apply_launch<SILU, 16>(x, y, ss, n, hw, s); break;
-    case 32: gn_apply_launch<SILU, 32>(x, y, ss, n, hw, s); break;
-    case 64: gn_apply_launch<SILU, 64>(x, y, ss, n, hw, s); break;
+    case 16: gn_apply_launch<SILU, 16, H2>(x, y, ss, n, hw, s); break;
+    case 32: gn_apply_launch<SILU, 32, H2>(x, y, ss, n, hw, s); break;
+    case 64: gn_apply_launch<SILU, 64, H2>(x, y, ss, n, hw, s); break;
     default: break;  // C validated by callers (128 / 256 / 512)
   }
 }
 
 void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
-                     cudaStream_t s) {
+                     bool h2, cudaStream_t s) {
   const int n = (int)(rows / hw);
-  if (silu) gn_apply_dispatch<true>(x, y, ss, n, hw, C, s);
-  else gn_apply_dispatch<false>(x, y, ss, n, hw, C, s);
+  if (silu) {
+    if (h2) gn_apply_dispatch<true, true>(x, y, ss, n, hw, C, s);
+    else gn_apply_dispatch<true, false>(x, y, ss, n, hw, C, s);
+  } else {
+    gn_apply_dispatch<false, false>(x, y, ss, n, hw, C, s);
+  }
 }
 
 __global__ void gn_stats_kernel(const __half* __restrict__ x, double* stats, int hw, int C) {

@@ -17,8 +17,9 @@ void launch_gn_finalize(const double* stats, const float* gamma, const float* be
                         double count, float eps, cudaStream_t s);
 
 // y = act(x * ss.x + ss.y), x/y fp16 [n*hw][C] (y may alias x), act = SiLU if silu else identity.
+// h2: packed-half SiLU (act.cuh gn_act8_h2) instead of the fp32 one (gn_act8).
 void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
-                     cudaStream_t s);
+                     bool h2, cudaStream_t s);
 
 // Row softmax numerator in place: P = exp(S - rowmax(S)) (fp16), row_scale = 1 / sum(P) (fp32).
 void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s);
@@ -30,6 +31,14 @@ void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, in
 // round-half-even -> uint8 HWC.  x fp16 NHWC [n][H][W][128]; w fp32 [3][3][3][128]; rgb [n][H][W][3].
 void launch_conv_out_u8(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb, int n,
                         int H, int W, cudaStream_t s);
+
+// Same tail on the tensor cores (csrc/conv_out_tc.cu): each input row loaded once by TMA, GN +
+// SiLU applied in shared memory (packed-half SiLU when h2), 72 tcgen05.mma (M=128, N=16) per
+// 128-pixel output row.  W must be a multiple of 128.
+cudaError_t launch_conv_out_tc(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb,
+                               int n, int H, int W, bool h2, cudaStream_t s);
+void kernels_set_conv_out_legacy(bool on);
+bool kernels_conv_out_legacy();
 
 // GroupNorm-32 statistics (sum, sumsq per image and group) of x [n][hw][C] fp16 into stats
 // [n][32][2] (accumulated; zero it first).  Standalone form of what the conv epilogue fuses.

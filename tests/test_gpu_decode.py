@@ -67,6 +67,21 @@ def test_config34_sd3_1024_golden(lbx):
     _check(_stats(got, g["rgb"]), "golden sd3 1024^2")
 
 
+def test_precise_activations_vs_oracle(lbx):
+    """precise_activations=1 (fp32 SiLU in every GroupNorm apply and the tail) on config 1: the same
+    bar, and no pixel more than 1 LSB from the default (packed-half SiLU) decode."""
+    import vae_ref
+    import weights_ref
+    z = weights_ref.make_latents("sd15", 1, 64, 64, seed=1)
+    ref = vae_ref.decode(z, weights_ref.make_weights("sd15", 0), "sd15")
+    precise = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=1, precise=True).reconstruct_latents(z)
+    fast = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=1).reconstruct_latents(z)
+    st = _stats(precise, ref)
+    _check(st, "config1 sd15 precise_activations")
+    assert st["psnr_db"] >= _stats(fast, ref)["psnr_db"] - 0.05
+    assert np.abs(precise.astype(np.int16) - fast.astype(np.int16)).max() <= 1
+
+
 def test_batch_invariance(lbx):
     """Image i of a batch decodes identically to the same latent alone (no cross-image leakage)."""
     import weights_ref

@@ -196,3 +196,28 @@ def test_conv3x3_fused_groupnorm_silu(lbx, cg, b, h, w, c, n, fold):
     o = out.double().reshape(b, h * w, 32, n // 32)
     sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
     torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
+
+
+@pytest.mark.parametrize("impl", [0, 2, 1])
+@pytest.mark.parametrize("n,H,W", [(2, 64, 128), (1, 128, 256), (3, 32, 512)])
+def test_conv_out_tail(lbx, impl, n, H, W):
+    """Decoder tail u8(conv3x3_128->3(SiLU(GN-affine(x))) + b) against torch fp32; impl 0/2 are the
+    tensor-core kernel (fp32 / packed-half SiLU, fp16 activations and weights), 1 the CUDA-core one.
+    Bar: every pixel within 1 LSB of the fp32 reference; >= 97% exact with fp32 SiLU (fp16 operands),
+    >= 95% with the packed-half SiLU."""
+    x = _rand(n, H, W, 128, seed=61) * 1.5 + 0.2
+    g = torch.Generator(device="cpu").manual_seed(62)
+    ss = torch.stack([torch.rand(n, 128, generator=g) + 0.5, torch.randn(n, 128, generator=g) * 0.5], dim=-1).cuda()
+    w = (torch.randn(3, 3, 3, 128, generator=g) * (1152 ** -0.5) * 3).cuda()  # [out][ky][kx][in]
+    b = (torch.randn(3, generator=g) * 0.2).cuda()
+    rgb = torch.empty(n, H, W, 3, dtype=torch.uint8, device="cuda")
+    lbx.op_conv_out(x.data_ptr(), ss.data_ptr(), w.data_ptr(), b.data_ptr(), rgb.data_ptr(), n, H, W, impl=impl)
+    torch.cuda.synchronize()
+    act = F.silu(x.float() * ss[:, None, None, :, 0] + ss[:, None, None, :, 1])
+    y = F.conv2d(act.permute(0, 3, 1, 2), w.permute(0, 3, 1, 2), b, padding=1).permute(0, 2, 3, 1)
+    ref = torch.round((y * 0.5 + 0.5).clamp(0, 1) * 255).to(torch.int32)  # torch.round: half to even
+    d = (rgb.int() - ref).abs()
+    exact = (d == 0).float().mean().item()
+    print(f"\n[conv_out impl {impl} {n}x{H}x{W}] max|d|={d.max().item()} exact={exact:.4f}")
+    assert d.max().item() <= 1
+    assert exact >= (0.95 if impl == 2 else 0.97)
