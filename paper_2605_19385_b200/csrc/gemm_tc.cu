@@ -49,6 +49,7 @@ struct KParams {
   int a_stages, b_stages;
   int desc_base_mode;  // descriptor base-offset convention for row-shifted views (0 or 1)
   int msub;            // 128-row M sub-tiles per CTA sharing every B tile (1 or 2)
+  int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -79,6 +80,21 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile
     phase = 0;
     m_tile = r;
   }
+}
+
+// First A row of sub-tile `sub` of this CTA's tile.  Horizontal sub-tiles (vsub = 0): the CTA's
+// rows are contiguous, m0 + 128 sub.  Vertical sub-tiles (vsub = 1, conv halo mode): the CTA owns
+// 128 pixels x msub image rows and the CTA pair covers 128 CG consecutive pixels of those rows,
+// so both sub-tiles' taps read one (halo_rows + 1)-row halo box.
+__device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank, int CG, int sub) {
+  if (!p.vsub) return m_tile * (128 * p.msub * CG) + rank * (128 * p.msub) + sub * 128;
+  const int segs = p.W / (128 * CG);
+  const int per_img = (p.H / p.msub) * segs;
+  const int img = m_tile / per_img;
+  const int r = m_tile - img * per_img;
+  const int yp = r / segs;
+  const int x0 = (r - yp * segs) * 128 * CG + rank * 128;
+  return (img * p.H + yp * p.msub + sub) * p.W + x0;
 }
 
 // Per-chunk GroupNorm partials.  pk holds this lane's 32 stored fp16 values (one pixel, 32
@@ -190,7 +206,7 @@ __global__ void __launch_bounds__(352, 1)
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int rows_cta = 128 * p.msub;
-        const int m0 = m_tile * (rows_cta * CG) + rank * rows_cta;  // this CTA's first A row
+        const int m0 = tile_row0(p, m_tile, rank, CG, 0);  // this CTA's first A row
         int img = 0, y0 = 0, x0 = 0;
         if (p.mode != GEMM_PLAIN) {
           const int hw = p.H * p.W;
@@ -213,7 +229,7 @@ __global__ void __launch_bounds__(352, 1)
             c0 = j * 64;
             c1 = x0 - 1;
             c2 = p.mode == GEMM_CONV3X3 ? y0 - 1 : y0 + (phs >> 1) - 1;
-            for (int sub = 1; sub < p.msub; ++sub) {
+            for (int sub = 1; sub < (p.vsub ? 1 : p.msub); ++sub) {
               if constexpr (CG == 1 || XF) ptx::tma_load_4d(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
               else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst + sub * p.halo_sub_bytes, c0, c1 + sub * 128, c2, c3);
             }
@@ -247,8 +263,9 @@ __global__ void __launch_bounds__(352, 1)
           if (XF) ptx::mbar_arrive_expect_tx(&a_full[st], rows_cta * 64 * 2);
           else if (leader) ptx::mbar_arrive_expect_tx(&a_full[st], CG * rows_cta * 64 * 2);
           for (int sub = 0; sub < p.msub; ++sub) {
-            if constexpr (CG == 1 || XF) ptx::tma_load_2d(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
-            else ptx::tma_load_2d_pair(&tmA2, &a_full[st], dst + sub * 16384, e * 64, m0 + sub * 128);
+            const int ms = p.vsub ? tile_row0(p, m_tile, rank, CG, sub) : m0 + sub * 128;
+            if constexpr (CG == 1 || XF) ptx::tma_load_2d(&tmA2, &a_full[st], dst + sub * 16384, e * 64, ms);
+            else ptx::tma_load_2d_pair(&tmA2, &a_full[st], dst + sub * 16384, e * 64, ms);
           }
           if (++st == p.a_stages) { st = 0; ph ^= 1; }
         }
@@ -286,45 +303,53 @@ __global__ void __launch_bounds__(352, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
-    if (leader) {
+    // One thread runs the whole issue loop (no per-tap elect / reconvergence).  Descriptors are
+    // built once and advanced by adding (byte offset >> 4) to the address field: every smem
+    // address is < 256 KB, so the 14-bit field never carries.
+    if (leader && ptx::elect_one()) {
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const uint64_t a_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
+      const uint64_t b_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+      const uint32_t a_stage16 = (uint32_t)p.a_stage_bytes >> 4, sub16 = (uint32_t)p.halo_sub_bytes >> 4;
+      const int msub = p.msub;
+      const bool conv = p.mode == GEMM_CONV3X3, halo = p.halo != 0, dbm = p.desc_base_mode != 0;
       for (int t = cluster_id; t < p.tiles; t += nclusters) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * (p.msub * BN);
+        const uint32_t d_tmem = tmem_base + acc * (msub * BN);
         for (int j = 0; j < n_a; ++j) {
           if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
           else ptx::mbar_wait(&a_full[as], aph);
-          const uint32_t a_base = ptx::smem_u32(sA + as * p.a_stage_bytes);
+          const uint64_t a_stage = a_desc0 + (uint64_t)(as * a_stage16);
+          int r0 = halo && !conv ? (phs & 1) : 0;  // the tap's 128 A rows start r0 rows into the halo
           for (int tp = 0; tp < per_a; ++tp) {
             ptx::mbar_wait(&b_full[bs], bph);
             ptx::tc_fence_after();
-            if (ptx::elect_one()) {
-              // halo: the tap's 128 A rows start `r0` rows into the halo box
-              int r0 = 0;
-              if (p.halo) r0 = p.mode == GEMM_CONV3X3 ? (tp / 3) * 130 + tp % 3 : (tp >> 1) * 130 + (tp & 1) + (phs & 1);
-              const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + bs * C::B_BYTES));
-              for (int sub = 0; sub < p.msub; ++sub) {  // sub-tiles share this B tile
-                uint64_t a_desc = ptx::sdesc_k_sw128(a_base + sub * p.halo_sub_bytes + r0 * 128);
-                if (p.desc_base_mode) a_desc |= (uint64_t)(r0 & 7) << 49;
+            const uint64_t b_desc = b_desc0 + (uint64_t)(bs * (C::B_BYTES >> 4));
+#pragma unroll
+            for (int sub = 0; sub < 2; ++sub) {  // sub-tiles share this B tile
+              if (sub < msub) {
+                uint64_t a_desc = a_stage + (uint64_t)(sub * sub16 + r0 * 8);
+                if (dbm) a_desc |= (uint64_t)(r0 & 7) << 49;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide k-block; +32 B per step inside the swizzle atom
                   ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, (j | tp | k) != 0);
               }
-              ptx::mma_commit<CG>(&b_empty[bs]);
-              if (tp == per_a - 1) {
-                ptx::mma_commit<CG>(&a_empty[as]);
-                if (j == n_a - 1 && p.n_extra == 0) ptx::mma_commit<CG>(&tfull[acc]);
-              }
             }
-            __syncwarp();
+            ptx::mma_commit<CG>(&b_empty[bs]);
             if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
+            if (halo) {  // conv3x3: r0 = ky*130 + kx; sub-pixel: (tap >> 1)*130 + (tap & 1) + (phase & 1)
+              if (conv) r0 += (tp % 3 == 2) ? 128 : 1;
+              else r0 += (tp & 1) ? 129 : 1;
+            }
           }
+          ptx::mma_commit<CG>(&a_empty[as]);
+          if (j == n_a - 1 && p.n_extra == 0) ptx::mma_commit<CG>(&tfull[acc]);
           if (++as == p.a_stages) { as = 0; aph ^= 1; }
         }
         for (int e = 0; e < p.n_extra; ++e) {
@@ -332,19 +357,20 @@ __global__ void __launch_bounds__(352, 1)
           else ptx::mbar_wait(&a_full[as], aph);
           ptx::mbar_wait(&b_full[bs], bph);
           ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + bs * C::B_BYTES));
-            for (int sub = 0; sub < p.msub; ++sub) {
-              const uint64_t a_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sA + as * p.a_stage_bytes + sub * 16384));
+          const uint64_t b_desc = b_desc0 + (uint64_t)(bs * (C::B_BYTES >> 4));
+          const uint64_t a_stage = a_desc0 + (uint64_t)(as * a_stage16);
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            if (sub < msub) {
+              const uint64_t a_desc = a_stage + (uint64_t)(sub * (16384 >> 4));
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, 1u);
             }
-            ptx::mma_commit<CG>(&b_empty[bs]);
-            ptx::mma_commit<CG>(&a_empty[as]);
-            if (e == p.n_extra - 1) ptx::mma_commit<CG>(&tfull[acc]);
           }
-          __syncwarp();
+          ptx::mma_commit<CG>(&b_empty[bs]);
+          ptx::mma_commit<CG>(&a_empty[as]);
+          if (e == p.n_extra - 1) ptx::mma_commit<CG>(&tfull[acc]);
           if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
           if (++as == p.a_stages) { as = 0; aph ^= 1; }
         }
@@ -468,7 +494,7 @@ __global__ void __launch_bounds__(352, 1)
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       for (int sub = 0; sub < p.msub; ++sub) {
-      const int m = m_tile * (128 * p.msub * CG) + rank * (128 * p.msub) + sub * 128 + row;
+      const int m = tile_row0(p, m_tile, (int)rank, CG, sub) + row;
       long long orow = m;
       if (p.mode == GEMM_SUBPIX) {
         const int hw = p.H * p.W;
@@ -625,15 +651,40 @@ bool make_tensor_map_f16(CUtensorMap* m, const void* base, int rank, const uint6
   return make_map(m, base, rank, d, st, bx);
 }
 
+static int g_halo_policy = 1;      // 1: use halo staging whenever the geometry allows
+static int g_msub_policy = 1;      // 1: two M sub-tiles per CTA for BN = 128 halo convs
+static int g_fuse_policy = 0;      // fused GroupNorm+SiLU on A: off by default (measured slower, DESIGN.md 8)
+static int g_desc_base_mode = 0;   // descriptor base-offset convention for row-shifted A views
+static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to B (bit 5 sets; measured
+                                   // equal for c128, ~3% slower for the 256-wide c512 / sub-pixel tiles)
+static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
+void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
+  g_halo_policy = halo_policy & 1;
+  g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
+  g_fuse_policy = (halo_policy >> 2) & 1;  // bit 2 enables fused GroupNorm on A in the decoder
+  g_desc_base_mode = desc_base_mode;
+  g_stage_policy = (halo_policy >> 5) & 1;
+  g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
+}
+
 template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
   // ---- operand staging plan
   if (kp.halo) {
-    kp.halo_sub_bytes = (64 * 130 * kp.halo_rows * 2 + 1023) & ~1023;
-    kp.a_tx_bytes = kp.msub * 64 * 130 * kp.halo_rows * 2;
-    kp.a_stage_bytes = kp.msub * kp.halo_sub_bytes;
-    kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
+    if (kp.vsub) {  // one box of halo_rows + msub - 1 rows; sub-tile s starts 130 s rows in
+      kp.halo_sub_bytes = 130 * 128;
+      kp.a_tx_bytes = 64 * 130 * (kp.halo_rows + kp.msub - 1) * 2;
+      kp.a_stage_bytes = (kp.a_tx_bytes + 1023) & ~1023;
+    } else {
+      kp.halo_sub_bytes = (64 * 130 * kp.halo_rows * 2 + 1023) & ~1023;
+      kp.a_tx_bytes = kp.msub * 64 * 130 * kp.halo_rows * 2;
+      kp.a_stage_bytes = kp.msub * kp.halo_sub_bytes;
+    }
+    // policy 1: a halo stage feeds >= 36 MMAs, so two are enough and the rest of the budget goes to
+    // B; policy 0 (default): three A stages when the B tile is small and there is one sub-tile
+    if (g_stage_policy) kp.a_stages = 2;
+    else kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
     kp.b_stages = (kSmemBudget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
   } else {
     kp.a_tx_bytes = kp.a_stage_bytes = 128 * 64 * 2;
@@ -654,7 +705,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   } else {
     cuuint64_t dims[4] = {(cuuint64_t)a.C, (cuuint64_t)a.W, (cuuint64_t)a.H, (cuuint64_t)a.B_img};
     cuuint64_t strides[3] = {(cuuint64_t)a.C * 2, (cuuint64_t)a.W * a.C * 2, (cuuint64_t)a.H * a.W * a.C * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)(kp.halo ? 130 : kp.Wt), (cuuint32_t)(kp.halo ? kp.halo_rows : kp.Ht), 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)(kp.halo ? 130 : kp.Wt),
+                         (cuuint32_t)(kp.halo ? kp.halo_rows + (kp.vsub ? kp.msub - 1 : 0) : kp.Ht), 1};
     if (!make_map(&tmA, a.A, 4, dims, strides, box)) return cudaErrorInvalidValue;
   }
   CUtensorMap tmA2;
@@ -711,17 +763,6 @@ bool gemm_tc_prepare() {
   return ok == 1;
 }
 
-static int g_halo_policy = 1;      // 1: use halo staging whenever the geometry allows
-static int g_msub_policy = 1;      // 1: two M sub-tiles per CTA for BN = 128 halo convs
-static int g_fuse_policy = 0;      // fused GroupNorm+SiLU on A: off by default (measured slower, DESIGN.md 8)
-static int g_desc_base_mode = 0;   // descriptor base-offset convention for row-shifted A views
-void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
-  g_halo_policy = halo_policy & 1;
-  g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
-  g_fuse_policy = (halo_policy >> 2) & 1;  // bit 2 enables fused GroupNorm on A in the decoder
-  g_desc_base_mode = desc_base_mode;
-}
-
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments) and 256-wide N tiles: the four borrowed epilogue warps
   // have slack there, and the SFU budget of the transform (2 ops / element) fits under the MMAs
@@ -769,6 +810,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   if (a.M % (128 * cg)) return cudaErrorInvalidValue;
   kp.msub = (kp.halo && g_msub_policy && bn == 128 && cg == 2 && a.mode == GEMM_CONV3X3 && a.W % 256 == 0 &&
              a.M % (512 * cg) == 0) ? 2 : 1;
+  kp.vsub = (kp.msub == 2 && g_vsub_policy && !a.gn_ss && a.H % 2 == 0 && a.W % (128 * cg) == 0) ? 1 : 0;
   kp.tmem_cols = 2 * bn * kp.msub;
   kp.m_tiles = a.M / (128 * cg * kp.msub);
   kp.n_tiles = a.N / bn;

@@ -31,7 +31,9 @@ def main():
     ap.add_argument("--cg", type=int, default=0)
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--bits", type=int, default=1, help="lbx_op_set_debug halo_policy bits")
     a = ap.parse_args()
+    lbx.check(lbx.lib().lbx_op_set_debug(a.bits, 0))
     dev = torch.device("cuda")
     b, hw, c = a.b, a.hw, a.c
     n = a.n or c

@@ -141,7 +141,8 @@ def test_gn_stats_and_apply(lbx):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("b,h,w,c,cin", [(2, 16, 256, 128, 128), (1, 16, 256, 128, 256), (1, 64, 64, 256, 512)])
+@pytest.mark.parametrize("b,h,w,c,cin", [(2, 16, 256, 128, 128), (1, 16, 256, 128, 256), (1, 64, 64, 256, 512),
+                                         (3, 8, 512, 128, 128)])
 def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
     """conv3x3(H) + X.W2^T as an extra K segment (identity -> residual, W_sc -> 1x1 shortcut)."""
     n = c
