@@ -520,7 +520,16 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       g.mode = GEMM_CONV3X3;
       g.M = n * hw; g.N = R.cout; g.K = 9 * R.cout;
       g.B_img = n; g.H = H; g.W = W; g.C = R.cout;
-      g.A2 = X_; g.lda2 = R.cin; g.K2 = R.cin;
+      // identity residual at >= 256 channels: added in the epilogue (in place: each thread reads its
+      // residual chunk before writing it).  Folding it as 4-8 short extra k-blocks starves the MMA
+      // (each lasts 4 MMAs against a full TMA round trip) -- measured 5-10% slower there, while at
+      // 128 channels (2 extra k-blocks) the fold wins.  A 1x1 shortcut is always folded.
+      const bool epi_resid = R.cin == R.cout && R.cout >= 256 && !resid_fold_always();
+      if (epi_resid) {
+        g.resid = X_; g.ldr = R.cout;
+      } else {
+        g.A2 = X_; g.lda2 = R.cin; g.K2 = R.cin;
+      }
       g.Bw = R.c2.w; g.ldb = 9 * R.cout + R.cin;
       g.out = R.cin == R.cout ? X_ : A_; g.ldo = R.cout; g.bias = R.c2.b;
       g.gn_stats = site_ptr(out_site); g.gn_cpg = R.cout / 32; g.rows_per_img = hw;

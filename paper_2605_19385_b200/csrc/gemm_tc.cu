@@ -102,8 +102,13 @@ __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank,
 // then group sums of squares) are reduce-scattered across the warp with NV + log2(32/NV)
 // shuffles (instead of 5 * NV for a butterfly per value): lane L ends up owning the warp total
 // of value index (L >> (5 - log2 NV)) & (NV - 1).
+__device__ __forceinline__ uint32_t word_of(const uint4 (&q)[4], int i) {
+  const uint4 v = q[i >> 2];
+  return (i & 3) == 0 ? v.x : (i & 3) == 1 ? v.y : (i & 3) == 2 ? v.z : v.w;
+}
+
 template <int NV>
-__device__ __forceinline__ float chunk_group_stats(const uint32_t (&pk)[16], uint32_t lane) {
+__device__ __forceinline__ float chunk_group_stats(const uint4 (&pk)[4], uint32_t lane) {
   constexpr int G = NV / 2, H2 = 16 / G;  // half2 words per group
   constexpr int LG = NV == 16 ? 4 : (NV == 8 ? 3 : 2);
   float v[NV];
@@ -112,7 +117,8 @@ __device__ __forceinline__ float chunk_group_stats(const uint32_t (&pk)[16], uin
     float s = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < H2; ++i) {
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&pk[g * H2 + i]));
+      const uint32_t w = word_of(pk, g * H2 + i);
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
       s += f.x + f.y;
       s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
     }
@@ -162,6 +168,8 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* a_xform = tempty + 2;  // XF: halo transformed (GroupNorm + SiLU applied) and fenced
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_xform + kMaxStages);
+  // 8 epilogue warps x (BN / 2) floats, 16-byte aligned for LDS.128
+  float* sBias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
   constexpr int EPI_WARPS = XF ? 4 : 8;  // XF: warps 6..9 transform A instead of draining TMEM
 
   const uint32_t warp = ptx::warp_id();
@@ -459,11 +467,18 @@ __global__ void __launch_bounds__(352, 1)
     const int row = q * 32 + lane;
     constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
     // GroupNorm partials: after the per-chunk reduce-scatter each lane owns one (group, sum|sumsq)
-    // value per chunk; lanes accumulate those across tiles in fp64 registers and flush with one
-    // atomic per owned value only when the (image, n-tile) changes -- not once per tile.
-    double gacc[NCH];
+    // value per chunk; lanes accumulate those across tiles as unevaluated fp32 pairs (TwoSum: hi +
+    // lo carries the rounding error exactly, ~fp64 accuracy without the FP64 pipe, which stalled
+    // the epilogue) and flush with one fp64 atomic per owned value only when the (image, n-tile)
+    // changes -- not once per tile.
+    float ghi[NCH], glo[NCH];
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) gacc[j] = 0.0;
+    for (int j = 0; j < NCH; ++j) ghi[j] = glo[j] = 0.f;
+    // bias of this warp's chunks, staged once per n-tile in the warp's own smem slice and read back
+    // as broadcast LDS.128 (an LDG per chunk put the L1 latency on the epilogue's critical path)
+    float* wbias = sBias + (warp - 2) * (NCH * 32);
+    int bias_ntile = -1;
+    const bool scaled = p.row_scale != nullptr || p.alpha != 1.f;
     int g_img = -1, g_ntile = -1;
     const int nv = p.gn_stats ? 64 / p.gn_cpg : 0;  // values per chunk: 2 * groups-per-chunk
     const int lg = nv == 16 ? 4 : (nv == 8 ? 3 : 2);
@@ -479,11 +494,11 @@ __global__ void __launch_bounds__(352, 1)
         for (int j = 0; j < NCH; ++j) {
           const int c = hsel + (EPI_WARPS / 4) * j;
           const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + g_in;
-          atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, gacc[j]);
+          atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, (double)ghi[j] + (double)glo[j]);
         }
       }
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) gacc[j] = 0.0;
+      for (int j = 0; j < NCH; ++j) ghi[j] = glo[j] = 0.f;
     };
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -491,6 +506,13 @@ __global__ void __launch_bounds__(352, 1)
       int m_tile, n_tile, ph;
       tile_coords(p, t, m_tile, n_tile, ph);
       const int n0 = n_tile * BN;
+      if (p.bias && n_tile != bias_ntile) {
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) wbias[j * 32 + lane] = p.bias[n0 + (hsel + (EPI_WARPS / 4) * j) * 32 + lane];
+        __syncwarp();
+        bias_ntile = n_tile;
+      }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       for (int sub = 0; sub < p.msub; ++sub) {
@@ -503,7 +525,7 @@ __global__ void __launch_bounds__(352, 1)
         const int i = rem / p.W, j = rem - (rem / p.W) * p.W;
         orow = ((long long)img * (2 * p.H) + (2 * i + (ph >> 1))) * (2 * p.W) + (2 * j + (ph & 1));
       }
-      const float rs = p.alpha * (p.row_scale ? p.row_scale[m] : 1.f);
+      const float rs = scaled ? p.alpha * (p.row_scale ? p.row_scale[m] : 1.f) : 1.f;
       if (p.gn_stats) {
         const int img = m / p.rows_per_img;  // warp-uniform: 32-row slices never straddle images
         if (img != g_img || n_tile != g_ntile) {
@@ -534,12 +556,17 @@ __global__ void __launch_bounds__(352, 1)
         ptx::tmem_ld_wait();
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * rs;
-        if (p.bias) {
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (scaled) {
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(p.bias + n + i));
-            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+          for (int i = 0; i < 32; ++i) v[i] *= rs;
+        }
+        if (p.bias) {
+          const float4* bv = reinterpret_cast<const float4*>(wbias + j * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 b = bv[i];
+            v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
           }
         }
         if (p.resid) {
@@ -560,21 +587,29 @@ __global__ void __launch_bounds__(352, 1)
               rr[j % PF][i] = __ldg(reinterpret_cast<const uint4*>(rbase + (j + PF) * RSTRIDE) + i);
           }
         }
-        uint32_t pk[16];
+        // pack straight into four aligned register quads (no MOVs into a shared staging quad,
+        // whose reuse serialised each STG.128 behind the previous one's operand read)
+        uint4 pk[4];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-          pk[i] = *reinterpret_cast<const uint32_t*>(&h);
+        for (int i = 0; i < 4; ++i) {
+          __half2 h0 = __floats2half2_rn(v[8 * i], v[8 * i + 1]), h1 = __floats2half2_rn(v[8 * i + 2], v[8 * i + 3]);
+          __half2 h2 = __floats2half2_rn(v[8 * i + 4], v[8 * i + 5]), h3 = __floats2half2_rn(v[8 * i + 6], v[8 * i + 7]);
+          pk[i] = make_uint4(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1),
+                             *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
         }
         uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) op[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < 4; ++i) op[i] = pk[i];
         if (p.gn_stats) {
           float val;
           if (nv == 16) val = chunk_group_stats<16>(pk, lane);
           else if (nv == 8) val = chunk_group_stats<8>(pk, lane);
           else val = chunk_group_stats<4>(pk, lane);
-          gacc[j] += (double)val;
+          // TwoSum(ghi, val): exact error term accumulated in glo
+          const float sum = ghi[j] + val;
+          const float bb = sum - ghi[j];
+          glo[j] += (ghi[j] - (sum - bb)) + (val - bb);
+          ghi[j] = sum;
         }
       }
       }  // sub-tiles
@@ -658,6 +693,7 @@ static int g_desc_base_mode = 0;   // descriptor base-offset convention for row-
 static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to B (bit 5 sets; measured
                                    // equal for c128, ~3% slower for the 256-wide c512 / sub-pixel tiles)
 static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
+static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_halo_policy = halo_policy & 1;
   g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
@@ -665,6 +701,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_desc_base_mode = desc_base_mode;
   g_stage_policy = (halo_policy >> 5) & 1;
   g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
+  g_fold_always = (halo_policy >> 7) & 1;
 }
 
 template <int BN, int CG, bool XF>
@@ -693,7 +730,8 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   if (kp.a_stages > kMaxStages) kp.a_stages = kMaxStages;
   if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
   if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
-  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16;
+  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16 +
+                   16 + 8 * (BN / 2) * 4;
   if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
 
   CUtensorMap tmA, tmB;
@@ -762,6 +800,8 @@ bool gemm_tc_prepare() {
   }
   return ok == 1;
 }
+
+bool resid_fold_always() { return g_fold_always != 0; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments) and 256-wide N tiles: the four borrowed epilogue warps

@@ -55,6 +55,8 @@ bool gemm_tc_can_fuse_gn(const GemmArgs& a);
 // Diagnostics: halo_policy 0 forces per-tap A staging; desc_base_mode selects the UMMA descriptor
 // base-offset convention for row-shifted (non-1024-aligned) halo views.
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
+// Debug bit 7: fold identity residuals into the K loop at every width (default: only at 128 channels).
+bool resid_fold_always();
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();
