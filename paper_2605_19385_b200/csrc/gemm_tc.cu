@@ -97,30 +97,25 @@ __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank,
   return (img * p.H + yp * p.msub + sub) * p.W + x0;
 }
 
-// Per-chunk GroupNorm partials.  pk holds this lane's 32 stored fp16 values (one pixel, 32
-// consecutive channels) as half2 pairs.  NV = 2 * groups-per-chunk values per lane (group sums,
+// Per-chunk GroupNorm partials.  xs holds this lane's 32 output values (one pixel, 32 consecutive
+// channels).  NV = 2 * groups-per-chunk values per lane (group sums,
 // then group sums of squares) are reduce-scattered across the warp with NV + log2(32/NV)
 // shuffles (instead of 5 * NV for a butterfly per value): lane L ends up owning the warp total
 // of value index (L >> (5 - log2 NV)) & (NV - 1).
-__device__ __forceinline__ uint32_t word_of(const uint4 (&q)[4], int i) {
-  const uint4 v = q[i >> 2];
-  return (i & 3) == 0 ? v.x : (i & 3) == 1 ? v.y : (i & 3) == 2 ? v.z : v.w;
-}
-
+// The partials are of the fp32 values just before the fp16 rounding of the store (the rounding
+// is < 2^-12 relative and unbiased; summing the fp32 values skips one HADD2.F32 per element).
 template <int NV>
-__device__ __forceinline__ float chunk_group_stats(const uint4 (&pk)[4], uint32_t lane) {
-  constexpr int G = NV / 2, H2 = 16 / G;  // half2 words per group
+__device__ __forceinline__ float chunk_group_stats(const float (&xs)[32], uint32_t lane) {
+  constexpr int G = NV / 2, E = 32 / G;  // elements per group
   constexpr int LG = NV == 16 ? 4 : (NV == 8 ? 3 : 2);
   float v[NV];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     float s = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < H2; ++i) {
-      const uint32_t w = word_of(pk, g * H2 + i);
-      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
-      s += f.x + f.y;
-      s2 = fmaf(f.x, f.x, fmaf(f.y, f.y, s2));
+    for (int i = 0; i < E; ++i) {
+      s += xs[g * E + i];
+      s2 = fmaf(xs[g * E + i], xs[g * E + i], s2);
     }
     v[g] = s;
     v[G + g] = s2;
@@ -602,9 +597,9 @@ __global__ void __launch_bounds__(352, 1)
         for (int i = 0; i < 4; ++i) op[i] = pk[i];
         if (p.gn_stats) {
           float val;
-          if (nv == 16) val = chunk_group_stats<16>(pk, lane);
-          else if (nv == 8) val = chunk_group_stats<8>(pk, lane);
-          else val = chunk_group_stats<4>(pk, lane);
+          if (nv == 16) val = chunk_group_stats<16>(v, lane);
+          else if (nv == 8) val = chunk_group_stats<8>(v, lane);
+          else val = chunk_group_stats<4>(v, lane);
           // TwoSum(ghi, val): exact error term accumulated in glo
           const float sum = ghi[j] + val;
           const float bb = sum - ghi[j];

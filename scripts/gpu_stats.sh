@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+timeout -s KILL 600 python -m pytest tests/test_gpu_gemm.py tests/test_gpu_decode.py -q -x -p no:cacheprovider --timeout=120 2>&1 | tail -2
+timeout -s KILL 120 python scripts/op_bench.py conv --b 16 --hw 1024 --c 128 --n 128 --stats --iters 4
+timeout -s KILL 120 python scripts/op_bench.py conv --b 16 --hw 1024 --c 128 --n 128 --iters 4
+timeout -s KILL 120 python scripts/op_bench.py conv --b 16 --hw 1024 --c 128 --fold --stats --iters 4
+timeout -s KILL 120 python scripts/op_bench.py conv --b 16 --hw 1024 --c 128 --resid --stats --iters 4
+timeout -s KILL 600 python scripts/ab_decode.py --bits 1 --batch 32 --rounds 4 --steps 2 --profile

@@ -68,6 +68,21 @@ def test_gemm_strided_views(lbx):
     _close(S, (q.float() @ k.float().t()) * 512 ** -0.5)
 
 
+def _check_gn_stats(stats, out, b, hw, n):
+    """GN partials are sums of the fp32 epilogue values just before their fp16 rounding; check the
+    per-(image, group) mean and variance they imply against a float64 reduction of the stored fp16
+    output: |d mean| <= 2e-4 * rms and |d var| <= 1e-3 * var (the rounding is < 2^-12 relative)."""
+    o = out.double().reshape(b, hw, 32, n // 32)
+    cnt = hw * (n // 32)
+    mean_r = o.sum(dim=(1, 3)) / cnt
+    var_r = (o * o).sum(dim=(1, 3)) / cnt - mean_r ** 2
+    mean = stats[..., 0] / cnt
+    var = stats[..., 1] / cnt - mean ** 2
+    rms = (var_r + mean_r ** 2).sqrt()
+    assert ((mean - mean_r).abs() <= 2e-4 * rms + 1e-6).all(), (mean - mean_r).abs().max()
+    assert ((var - var_r).abs() <= 1e-3 * var_r + 1e-6).all(), ((var - var_r).abs() / var_r).max()
+
+
 def _conv_ref(x_nhwc, w_oihw, bias):
     x = x_nhwc.permute(0, 3, 1, 2).float()
     y = F.conv2d(x, w_oihw.float(), bias, padding=1)
@@ -102,10 +117,7 @@ def test_conv3x3_resid_gnstats(lbx, cg):
                 c=c, resid=resid.data_ptr(), ldr=n, gn_stats=stats.data_ptr(), cta_group=cg)
     torch.cuda.synchronize()
     _close(out, _conv_ref(x, wt, None) + resid.float())
-    # GN partial sums are of the stored fp16 values: compare with a float64 reduction of `out`
-    o = out.double().reshape(b, h * w, 32, n // 32)
-    ref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
-    torch.testing.assert_close(stats, ref, rtol=1e-5, atol=1e-3)
+    _check_gn_stats(stats, out, b, h * w, n)
 
 
 @pytest.mark.parametrize("cg", [1, 2])
@@ -163,9 +175,7 @@ def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
     torch.cuda.synchronize()
     ref = _conv_ref(hin, wt, bias) + (x.float().reshape(-1, cin) @ wsc.float().t()).reshape(b, h, w, n)
     _close(out, ref)
-    o = out.double().reshape(b, h * w, 32, n // 32)
-    sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
-    torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
+    _check_gn_stats(stats, out, b, h * w, n)
 
 
 @pytest.mark.parametrize("cg", [1, 2])
@@ -194,9 +204,7 @@ def test_conv3x3_fused_groupnorm_silu(lbx, cg, b, h, w, c, n, fold):
     if fold:
         ref = ref + xr.float()
     _close(out, ref, rel=3e-3)
-    o = out.double().reshape(b, h * w, 32, n // 32)
-    sref = torch.stack([o.sum(dim=(1, 3)), (o * o).sum(dim=(1, 3))], dim=-1)
-    torch.testing.assert_close(stats, sref, rtol=1e-5, atol=1e-3)
+    _check_gn_stats(stats, out, b, h * w, n)
 
 
 @pytest.mark.parametrize("impl", [0, 2, 1])
