@@ -163,7 +163,8 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * the two-sub-tile variant; 2 enables the fused GroupNorm A-operand transform (XF) in the decoder;
  * 4 selects the CUDA-core conv_out tail; 5 gives halo convs two A stages and the rest of smem to B;
  * 6 uses horizontally (instead of vertically) adjacent sub-tiles for the two-sub-tile variant; 7 folds
- * identity residuals into the K loop at every width (default: epilogue add at >= 256 channels).
+ * identity residuals into the K loop at every width (default: epilogue add at >= 256 channels); 8
+ * selects the register-staged GroupNorm apply instead of the bulk-copy (1-D TMA) one.
  * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
 /* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],

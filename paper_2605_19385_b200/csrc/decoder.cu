@@ -942,6 +942,7 @@ lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
   lbx::gemm_tc_set_debug(halo_policy, desc_base_mode);
   lbx::kernels_set_conv_out_legacy((halo_policy >> 4) & 1);
+  lbx::kernels_set_apply_bulk(!((halo_policy >> 8) & 1));
   return LBX_OK;
 }
 

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <mutex>
 
+#include "act.cuh"
 #include "gemm_tc.cuh"
 #include "ptx.cuh"
 
@@ -66,7 +67,9 @@ struct Cfg {
   static constexpr int B_ROWS = BN / CG;             // B rows staged per CTA
   static constexpr int B_BYTES = B_ROWS * 64 * 2;    // one 64-wide k-block
   static constexpr int SMEM_MAX = 227 * 1024;
-  static constexpr int THREADS = 352;  // warp 0 A-producer, 1 MMA, 2..9 epilogue, 10 B-producer
+  // warp 0 A-producer, 1 MMA, 2..9 epilogue, 10 B-producer (+ 11..14 A transform in XF kernels)
+  static constexpr int THREADS = 352;
+  static constexpr int THREADS_XF = 480;
   static constexpr uint32_t IDESC = ptx::idesc_f16(128 * CG, BN);
 };
 
@@ -138,16 +141,9 @@ __device__ __forceinline__ float chunk_group_stats(const float (&xs)[32], uint32
   return x;
 }
 
-// SiLU for the fused A-operand transform: ex2 + rcp on the SFU (fp32-accurate to a few ulp).
-__device__ __forceinline__ float silu_xf(float y) {
-  float e, r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(y * -1.4426950408889634f));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
-  return y * r;
-}
 
 template <int BN, int CG, bool XF>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(XF ? 480 : 352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const KParams p) {
   using C = Cfg<BN, CG>;
@@ -165,7 +161,7 @@ __global__ void __launch_bounds__(352, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_xform + kMaxStages);
   // 8 epilogue warps x (BN / 2) floats, 16-byte aligned for LDS.128
   float* sBias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
-  constexpr int EPI_WARPS = XF ? 4 : 8;  // XF: warps 6..9 transform A instead of draining TMEM
+  constexpr int EPI_WARPS = 8;
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -380,22 +376,24 @@ __global__ void __launch_bounds__(352, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (XF && warp >= 6) {
+  } else if (XF && warp >= 11) {
     // ------------------------------------------------------------ fused GroupNorm + SiLU on A
-    // Warps 6..9 rewrite each landed halo in place: y = SiLU(x * a_c + b_c) (fp32 math, one fp16
-    // rounding) for pixels inside the image; out-of-image rows keep TMA's zero fill (padding comes
-    // after SiLU).  Thread t owns logical 16-byte chunk t & 7 (8 channels) of every 16th row, so its
-    // 8 (a, b) pairs load once per C-block; the physical chunk is (chunk ^ row & 7) (128B swizzle).
-    const int tid = (int)(warp - 6) * 32 + (int)lane;
+    // Warps 11..14 rewrite each landed halo in place: y = SiLU(x * a_c + b_c) (fp32 affine, SiLU
+    // on packed halves as in act.cuh gn_act8_h2, one fp16 rounding) for pixels inside the image;
+    // out-of-image positions keep TMA's zero fill (the conv pads after the activation).  Thread t
+    // owns logical 16-byte chunk t & 7 (8 channels) of every 16th halo row, so its 8 (a, b) pairs
+    // load once per C-block; the physical chunk is (chunk ^ row & 7) (128B swizzle).
+    const int tid = (int)(warp - 11) * 32 + (int)lane;
     const int cq = tid & 7;
-    const int rows = p.halo_rows * 130;
+    const int nbox = p.vsub ? 1 : p.msub;
+    const int box_rows = p.vsub ? p.halo_rows + p.msub - 1 : p.halo_rows;
+    const int rows = box_rows * 130;
     int st = 0;
     uint32_t ph = 0;
     for (int t = cluster_id; t < p.tiles; t += nclusters) {
       int m_tile, n_tile, phs;
       tile_coords(p, t, m_tile, n_tile, phs);
-      const int rows_cta = 128 * p.msub;
-      const int m0 = m_tile * (rows_cta * CG) + rank * rows_cta;
+      const int m0 = tile_row0(p, m_tile, (int)rank, CG, 0);
       const int hw = p.H * p.W;
       const int img = m0 / hw;
       const int rem = m0 - img * hw;
@@ -413,11 +411,11 @@ __global__ void __launch_bounds__(352, 1)
         ptx::mbar_wait(&a_full[st], ph);
         if (j < n_a) {
           uint8_t* base = sA + st * p.a_stage_bytes;
-          for (int sub = 0; sub < p.msub; ++sub) {
-            uint8_t* hb = base + sub * p.halo_sub_bytes;
-            const int xs = x0 - 1 + sub * 128;
+          for (int bx = 0; bx < nbox; ++bx) {
+            uint8_t* hb = base + bx * p.halo_sub_bytes;
+            const int xs = x0 - 1 + bx * 128;
             int hr = (tid >> 3) / 130, px = (tid >> 3) - hr * 130;
-            // two rows per iteration: 16 independent ex2/rcp chains per thread keep the SFU busy
+            // two rows per iteration: independent MUFU chains per thread
             for (int r = tid >> 3; r < rows; r += 32) {
               int hr2 = hr, px2 = px + 16;
               if (px2 >= 130) { px2 -= 130; ++hr2; }
@@ -428,17 +426,10 @@ __global__ void __launch_bounds__(352, 1)
               uint4* q2 = reinterpret_cast<uint4*>(hb + r2 * 128 + ((cq ^ (r2 & 7)) << 4));
               const uint4 u1 = v1 ? *q1 : make_uint4(0, 0, 0, 0);
               const uint4 u2 = v2 ? *q2 : make_uint4(0, 0, 0, 0);
-              uint32_t w[8] = {u1.x, u1.y, u1.z, u1.w, u2.x, u2.y, u2.z, u2.w};
-#pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const int c = k & 3;
-                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-                const __half2 h = __floats2half2_rn(silu_xf(fmaf(f.x, ca[2 * c], cb[2 * c])),
-                                                    silu_xf(fmaf(f.y, ca[2 * c + 1], cb[2 * c + 1])));
-                w[k] = *reinterpret_cast<const uint32_t*>(&h);
-              }
-              if (v1) *q1 = make_uint4(w[0], w[1], w[2], w[3]);
-              if (v2) *q2 = make_uint4(w[4], w[5], w[6], w[7]);
+              const uint4 w1 = gn_act8_h2<true>(u1, ca, cb);
+              const uint4 w2 = gn_act8_h2<true>(u2, ca, cb);
+              if (v1) *q1 = w1;
+              if (v2) *q2 = w2;
               px = px2 + 16;
               hr = hr2;
               if (px >= 130) { px -= 130; ++hr; }
@@ -458,7 +449,7 @@ __global__ void __launch_bounds__(352, 1)
     // ------------------------------------------------------------ epilogue (warps 2..9)
     // Two warps per TMEM lane quarter; warp half `hsel` takes the even/odd 32-column chunks.
     const uint32_t q = warp & 3;
-    const int hsel = XF ? 0 : (int)(warp - 2) >> 2;
+    const int hsel = (int)(warp - 2) >> 2;
     const int row = q * 32 + lane;
     constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
     // GroupNorm partials: after the per-chunk reduce-scatter each lane owns one (group, sum|sumsq)
@@ -764,7 +755,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   if (clusters > kp.tiles) clusters = kp.tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG);
-  cfg.blockDim = dim3(Cf::THREADS);
+  cfg.blockDim = dim3(XF ? Cf::THREADS_XF : Cf::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -799,10 +790,9 @@ bool gemm_tc_prepare() {
 bool resid_fold_always() { return g_fold_always != 0; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
-  // halo staging (128-pixel row segments) and 256-wide N tiles: the four borrowed epilogue warps
-  // have slack there, and the SFU budget of the transform (2 ops / element) fits under the MMAs
+  // halo staging (128-pixel row segments); four extra warps transform each landed halo
   return g_fuse_policy && g_halo_policy && a.mode == GEMM_CONV3X3 && a.W >= 128 && a.W % 128 == 0 &&
-         a.N % 256 == 0 && a.C >= 256 && a.C % 64 == 0 && a.M % 256 == 0;
+         a.N % 128 == 0 && a.C % 64 == 0 && a.M % 256 == 0;
 }
 
 cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg, int force_bn) {
@@ -845,7 +835,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   if (a.M % (128 * cg)) return cudaErrorInvalidValue;
   kp.msub = (kp.halo && g_msub_policy && bn == 128 && cg == 2 && a.mode == GEMM_CONV3X3 && a.W % 256 == 0 &&
              a.M % (512 * cg) == 0) ? 2 : 1;
-  kp.vsub = (kp.msub == 2 && g_vsub_policy && !a.gn_ss && a.H % 2 == 0 && a.W % (128 * cg) == 0) ? 1 : 0;
+  kp.vsub = (kp.msub == 2 && g_vsub_policy && a.H % 2 == 0 && a.W % (128 * cg) == 0) ? 1 : 0;
   kp.tmem_cols = 2 * bn * kp.msub;
   kp.m_tiles = a.M / (128 * cg * kp.msub);
   kp.n_tiles = a.N / bn;

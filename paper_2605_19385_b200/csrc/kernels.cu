@@ -6,6 +6,7 @@
 #include "act.cuh"
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace lbx {
 
@@ -119,12 +120,125 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
   }
 }
 
+// Bulk-copy form of the same apply (default): one persistent CTA per SM streams 32 KB chunks
+// through a 4-stage smem ring with 1-D TMA (cp.async.bulk global -> smem, mbarrier completion),
+// all 256 threads rewrite the chunk in smem, and one thread writes it back with a bulk store
+// (cp.async.bulk smem -> global, bulk_group).  Three loads stay in flight per SM without holding
+// registers, so the stream runs closer to copy bandwidth than the register-staged kernel above.
+// A chunk never straddles an image (every image is a multiple of 32 KB), and thread t always
+// owns channel octet t mod CV (256 is a multiple of CV), so its 8 affine pairs change only with
+// the image.
+constexpr int kApChunk = 32768, kApStages = 4;
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(ptx::smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+template <bool SILU, int CV, bool H2>
+__global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, __half* y, const float2* __restrict__ ss,
+                                                              long long img_bytes, long long chunks) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kApStages * kApChunk);
+  const int tid = threadIdx.x;
+  const int cvec = tid % CV;
+  if (tid == 0) {
+    for (int i = 0; i < kApStages; ++i) ptx::mbar_init(&full[i], 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(x);
+  uint8_t* dst = reinterpret_cast<uint8_t*>(y);
+  const long long first = blockIdx.x, step = gridDim.x;
+  const long long mine = first < chunks ? (chunks - first + step - 1) / step : 0;
+  constexpr int P = kApStages - 1;  // loads in flight
+  if (tid == 0) {
+    for (long long k = 0; k < P && k < mine; ++k) {
+      ptx::mbar_arrive_expect_tx(&full[k], kApChunk);
+      bulk_load(ring + k * kApChunk, src + (first + k * step) * kApChunk, kApChunk, &full[k]);
+    }
+  }
+  int cur_img = -1;
+  float a[8], b[8];
+  for (long long k = 0; k < mine; ++k) {
+    const int st = (int)(k % kApStages);
+    const long long c = first + k * step;
+    const int img = (int)(c * kApChunk / img_bytes);
+    if (img != cur_img) {
+      cur_img = img;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 t = ss[(size_t)img * CV * 8 + cvec * 8 + j];
+        a[j] = t.x;
+        b[j] = t.y;
+      }
+    }
+    ptx::mbar_wait(&full[st], (uint32_t)((k / kApStages) & 1));
+    uint4* q = reinterpret_cast<uint4*>(ring + st * kApChunk);
+#pragma unroll
+    for (int i = 0; i < kApChunk / 16 / 256; ++i) {
+      const uint4 u = q[tid + 256 * i];
+      q[tid + 256 * i] = H2 ? gn_act8_h2<SILU>(u, a, b) : gn_act8<SILU>(u, a, b);
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
+    __syncthreads();
+    if (tid == 0) {
+      bulk_store(dst + c * kApChunk, ring + st * kApChunk, kApChunk);
+      if (k + P < mine) {
+        // the refill targets the stage of chunk k-1: its store must have finished reading smem
+        bulk_wait_read<1>();
+        const int ns = (int)((k + P) % kApStages);
+        ptx::mbar_arrive_expect_tx(&full[ns], kApChunk);
+        bulk_load(ring + ns * kApChunk, src + (first + (k + P) * step) * kApChunk, kApChunk, &full[ns]);
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static bool g_apply_bulk = true;  // bulk-copy apply (debug bit 8 selects the register-staged one)
+void kernels_set_apply_bulk(bool on) { g_apply_bulk = on; }
+
+template <bool SILU, int CV, bool H2>
+static bool gn_apply_bulk_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
+  const long long img_bytes = (long long)hw * CV * 16;
+  // measured per site in the decoder: faster at 128 and 512 channels (5.8 / 6.6 TB/s vs 5.2 / 5.5),
+  // slower at 256 (4.0-5.0 vs 5.2-5.3 TB/s), where the register-staged kernel stays
+  if (!g_apply_bulk || CV == 32 || img_bytes % kApChunk) return false;
+  constexpr int smem = kApStages * kApChunk + kApStages * 8;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gn_apply_bulk_kernel<SILU, CV, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess)
+      return false;
+    attr = true;
+  }
+  const long long chunks = (long long)n * img_bytes / kApChunk;
+  const int grid = (int)(chunks < num_sms() ? chunks : num_sms());
+  gn_apply_bulk_kernel<SILU, CV, H2><<<grid, 256, smem, s>>>(x, y, ss, img_bytes, chunks);
+  return true;
+}
+
 static bool g_conv_out_legacy = false;  // CUDA-core conv_out instead of the tensor-core tail
 void kernels_set_conv_out_legacy(bool on) { g_conv_out_legacy = on; }
 bool kernels_conv_out_legacy() { return g_conv_out_legacy; }
 
 template <bool SILU, int CV, bool H2>
 static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
+  if (gn_apply_bulk_launch<SILU, CV, H2>(x, y, ss, n, hw, s)) return;
   static int occ = 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel<SILU, CV, H2>, 256, 0);

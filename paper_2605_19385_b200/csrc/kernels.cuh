@@ -38,6 +38,7 @@ void launch_conv_out_u8(const __half* x, const float2* ss, const float* w, const
 cudaError_t launch_conv_out_tc(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb,
                                int n, int H, int W, bool h2, cudaStream_t s);
 void kernels_set_conv_out_legacy(bool on);
+void kernels_set_apply_bulk(bool on);
 bool kernels_conv_out_legacy();
 
 // GroupNorm-32 statistics (sum, sumsq per image and group) of x [n][hw][C] fp16 into stats

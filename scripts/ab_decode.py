@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--grep", default="", help="with --profile: print per-kernel rows whose name contains this")
     a = ap.parse_args()
     c = 4 if a.fam == "sd15" else 16
     dev = torch.device("cuda")
@@ -43,6 +44,14 @@ def main():
             prof = d.profile(a.batch)
             tot = sum(p["ms"] for p in prof)
             print(f"bits {b}: eager profile total {tot:.2f} ms")
+            if a.grep:
+                agg = {}
+                for p in prof:
+                    if a.grep in p["name"]:
+                        g = agg.setdefault(p["name"], [0.0, 0, 0.0])
+                        g[0] += p["ms"]; g[1] += 1; g[2] += p["bytes"]
+                for k, (ms, cnt, by) in sorted(agg.items()):
+                    print(f"    {ms:8.2f} ms {cnt:3d}x {by / ms / 1e6:7.0f} GB/s  {k}")
     ref = None
     for b, d in decs.items():
         d.decode_ptr(lat.data_ptr(), a.batch, rgb.data_ptr(), stream.cuda_stream)

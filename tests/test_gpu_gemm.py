@@ -180,9 +180,11 @@ def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("b,h,w,c,n,fold", [(2, 16, 128, 256, 256, False), (1, 16, 256, 512, 512, True),
-                                            (2, 8, 256, 256, 256, True)])
+                                            (2, 8, 256, 256, 256, True), (2, 16, 256, 128, 128, True),
+                                            (1, 8, 512, 256, 128, False)])
 def test_conv3x3_fused_groupnorm_silu(lbx, cg, b, h, w, c, n, fold):
-    """A' = SiLU(A * a[img, c] + b[img, c]) applied to the halo in smem; padding stays zero."""
+    """A' = SiLU(A * a[img, c] + b[img, c]) applied to the halo in smem (packed-half SiLU, as the
+    decoder's GroupNorm applies); padding stays zero.  128-wide N exercises the vertical sub-tiles."""
     x = _rand(b, h, w, c, seed=41) * 2 + 0.3
     g = torch.Generator(device="cpu").manual_seed(42)
     ss = torch.stack([torch.rand(b, c, generator=g) + 0.5, torch.randn(b, c, generator=g) * 0.5], dim=-1).cuda()
