@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--bits", type=int, default=1, help="lbx_op_set_debug halo_policy bits")
+    ap.add_argument("--sustain", type=float, default=0.0,
+                    help="run back to back for this many seconds under nvidia-smi sampling (power-capped rate, J/unit)")
     a = ap.parse_args()
     lbx.check(lbx.lib().lbx_op_set_debug(a.bits, 0))
     dev = torch.device("cuda")
@@ -85,6 +87,34 @@ def main():
 
     run()
     torch.cuda.synchronize()
+    if a.sustain > 0:
+        import subprocess
+        import time
+        unit_scale = 1e9 if a.op == "gn" else 1e12
+        smi = subprocess.Popen(["nvidia-smi", "--query-gpu=power.draw,clocks.sm", "--format=csv,noheader,nounits",
+                                "-lms", "100"], stdout=subprocess.PIPE, text=True)
+        t0 = time.time()
+        reps = 0
+        ev0.record()
+        while time.time() - t0 < a.sustain:
+            for _ in range(4):
+                run()
+            reps += 4
+            torch.cuda.synchronize()
+        ev1.record()
+        torch.cuda.synchronize()
+        smi.terminate()
+        out = smi.communicate()[0].strip().splitlines()
+        samples = [tuple(float(v) for v in l.split(",")) for l in out if l.strip()]
+        half = samples[len(samples) // 3:]  # skip the ramp
+        pw = sum(x[0] for x in half) / max(1, len(half))
+        clk = sorted(x[1] for x in half)[len(half) // 2] if half else 0
+        ms = ev0.elapsed_time(ev1) / reps
+        rate = flops / (ms / 1e3) / unit_scale
+        unit = "GB/s" if a.op == "gn" else "TFLOP/s(algo)"
+        print(f"SUSTAINED {a.op} b{b} hw{hw} c{c} n{n}: {ms:.3f} ms  {rate:.1f} {unit}  power {pw:.0f} W  sm {clk:.0f} MHz  "
+              f"{pw / rate:.3f} W per {unit}")
+        return
     ev0.record()
     for _ in range(a.iters):
         run()

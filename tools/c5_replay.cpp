@@ -33,6 +33,7 @@ struct Opts {
   int n_devices = 1;
   std::string service;         // "ms1,ms2,ms4,ms8,ms16,ms32" (sim mode); empty = defaults
   std::string json;
+  std::string dump;            // live: per-job "submit_ms start_ms end_ms batch" lines (diagnostics)
 };
 
 // Batch service curve measured on one B200 for 16x128x128 -> 1024^2 (lbx_reconstruct, host blobs,
@@ -76,6 +77,7 @@ bool parse(int argc, char** argv, Opts& o) {
     else if (k == "--window-start") o.window_start = std::stod(v);
     else if (k == "--service") o.service = v;
     else if (k == "--json") o.json = v;
+    else if (k == "--dump") o.dump = v;
     else {
       std::fprintf(stderr, "unknown option %s\n", k.c_str());
       return false;
@@ -227,6 +229,7 @@ int main(int argc, char** argv) {
     for (int i = nbuf - 1; i >= 0; --i) free_bufs.push_back(i);
     std::vector<int> buf_of(jobs.size(), -1);
     std::vector<double> live_dec, sim_dec;
+    std::vector<lbx_completion> all_comp;
     std::vector<lbx_completion> comp(512);
     uint64_t backpressure = 0;
     auto drain = [&](uint32_t wait_us) {
@@ -234,6 +237,7 @@ int main(int argc, char** argv) {
       for (int i = 0; i < k; ++i) {
         const size_t q = comp[i].request_id;
         live_dec.push_back((comp[i].t_end_us - comp[i].t_submit_us) / 1000.0);
+        if (!o.dump.empty()) all_comp.push_back(comp[i]);
         free_bufs.push_back(buf_of[q]);
       }
       return k;
@@ -257,6 +261,14 @@ int main(int argc, char** argv) {
     while (lbx_batcher_pending(b)) drain(10000);
     const double wall = (now_ms() - wall0) / 1000.0;
     lbx_batcher_destroy(b);
+    if (!o.dump.empty() && !all_comp.empty()) {
+      FILE* f = std::fopen(o.dump.c_str(), "w");
+      const uint64_t base = all_comp.front().t_submit_us;
+      for (const auto& c : all_comp)
+        if (f) std::fprintf(f, "%.3f %.3f %.3f %u\n", (c.t_submit_us - base) / 1e3, (c.t_start_us - base) / 1e3,
+                            (c.t_end_us - base) / 1e3, c.batch_size);
+      if (f) std::fclose(f);
+    }
     std::sort(live_dec.begin(), live_dec.end());
     std::sort(sim_dec.begin(), sim_dec.end());
     len = std::snprintf(buf, sizeof buf,
