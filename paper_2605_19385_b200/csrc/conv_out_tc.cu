@@ -7,12 +7,16 @@
 // 1-pixel halo x 128 channels) is loaded once by TMA, normalised + activated in place by eight
 // transform warps (GroupNorm affine in fp32, SiLU, one fp16 rounding; out-of-image pixels keep
 // TMA's zero fill because the conv pads *after* the activation), and then feeds the three output
-// rows that need it.  Output row y = sum over (ky, kx, 64-channel block, K16) of
-//   A = rows of input row y+ky-1 shifted by kx pixels (a row-shifted UMMA descriptor into the
-//       same 128B-swizzled buffer, as in gemm_tc.cu's halo staging)
-//   B = conv_out weights, [16 (3 real + 13 zero) x 1152] fp16, resident in smem
-// i.e. 72 tcgen05.mma (M = 128 pixels, N = 16, K = 16) into a double-buffered 16-column TMEM
-// accumulator; four epilogue warps read it back (one pixel per thread) and write the uint8 RGB.
+// rows that need it.  The three kernel rows are folded into N: per INPUT row y',
+//   E_y'[px, 4 ky + c] = sum over (kx, 64-channel block, K16) of A_y'[px + kx] . W[ky][kx][c]
+// with A = rows of input row y' shifted by kx pixels (a row-shifted UMMA descriptor into the same
+// 128B-swizzled buffer, as in gemm_tc.cu's halo staging) and B = [16 x 384] fp16 weights resident
+// in smem (rows 4 ky + c, c < 3; the rest zero): 24 tcgen05.mma (M = 128 pixels, N = 16, K = 16)
+// into a 4-deep ring of 16-column TMEM accumulators.  Output row y = E_{y-1}[., 0..2] +
+// E_y[., 4..6] + E_{y+1}[., 8..10] is summed by four epilogue warps (one pixel per thread), which
+// write the uint8 RGB.  An input row's smem slot is released right after its own 24 MMAs, so the
+// whole ring prefetches (the first version kept three rows resident for 72 MMAs per output row
+// and ran latency-bound at ~2.5 TB/s).
 //
 // Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 epilogue, 6..13 transform.
 #include <cuda.h>
@@ -29,11 +33,12 @@ namespace lbx {
 namespace {
 
 constexpr int kCoThreads = 448;
-constexpr int kCoSlots = 5;                       // input-row ring depth (3 in use + 2 in flight)
+constexpr int kCoSlots = 6;                       // input-row ring depth
 constexpr int kCoBoxBytes = 64 * 130 * 2;         // one TMA box: 64 channels x 130 pixels
 constexpr int kCoCbPitch = 17408;                 // 1024-aligned pitch of one 64-channel block
 constexpr int kCoSlotBytes = 2 * kCoCbPitch;      // one input row, 128 channels
-constexpr int kCoBBytes = 18 * 2048;              // 18 k-blocks x (16 rows x 128 B)
+constexpr int kCoBBytes = 6 * 2048;               // 6 k-blocks (kx, channel block) x (16 rows x 128 B)
+constexpr int kCoE = 4;                           // TMEM ring of per-input-row partial sums
 constexpr int kCoSmem = 1024 + kCoSlots * kCoSlotBytes + kCoBBytes + 256;
 constexpr uint32_t kCoIdesc = ptx::idesc_f16(128, 16);
 
@@ -50,6 +55,15 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr));
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
 __device__ __forceinline__ void item_coords(const CoParams& p, int it, int& img, int& x0, int& y0) {
@@ -72,17 +86,20 @@ __global__ void __launch_bounds__(kCoThreads, 1)
   uint64_t* slot_xf = slot_full + kCoSlots;
   uint64_t* slot_empty = slot_xf + kCoSlots;
   uint64_t* acc_full = slot_empty + kCoSlots;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_empty = acc_full + kCoE;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + kCoE);
 
   const uint32_t warp = ptx::warp_id(), lane = ptx::lane_id();
 
-  // weights -> smem once: fp32 [3][1152] -> fp16 K-major SW128, rows 3..15 zero
-  for (int q = threadIdx.x; q < 18 * 16 * 8; q += blockDim.x) {
+  // weights -> smem once: fp32 [c][ky][kx][ci] -> fp16 B[n = 4 ky + c][k = kx * 128 + ci], K-major
+  // SW128 in 6 k-blocks of 64; rows with c = 3 or ky = 3 are zero
+  for (int q = threadIdx.x; q < 6 * 16 * 8; q += blockDim.x) {
     const int kb = q / 128, rem = q - kb * 128, row = rem >> 3, ch = rem & 7;
+    const int ky = row >> 2, c = row & 3;
     uint32_t wd[4] = {0, 0, 0, 0};
-    if (row < 3) {
-      const float* src = p.w + row * 1152 + kb * 64 + ch * 8;
+    if (ky < 3 && c < 3) {
+      const int kx = kb >> 1, cb = kb & 1;
+      const float* src = p.w + ((c * 3 + ky) * 3 + kx) * 128 + cb * 64 + ch * 8;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const __half2 h = __floats2half2_rn(src[2 * j], src[2 * j + 1]);
@@ -99,13 +116,13 @@ __global__ void __launch_bounds__(kCoThreads, 1)
       ptx::mbar_init(&slot_xf[s], 8);
       ptx::mbar_init(&slot_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kCoE; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
       ptx::mbar_init(&acc_empty[i], 4);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc<1>(tmem_slot, 32);
+  if (warp == 1) ptx::tmem_alloc<1>(tmem_slot, 16 * kCoE);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -130,66 +147,72 @@ __global__ void __launch_bounds__(kCoThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    uint32_t gi = 0, ai = 0;
-    for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-      const uint32_t base = gi;
-      for (uint32_t r = 0; r < 2; ++r) ptx::mbar_wait(&slot_xf[(base + r) % kCoSlots], ((base + r) / kCoSlots) & 1);
-      for (int j = 0; j < p.R; ++j, ++ai) {
-        const uint32_t nr = base + j + 2;
-        ptx::mbar_wait(&slot_xf[nr % kCoSlots], (nr / kCoSlots) & 1);
-        const uint32_t buf = ai & 1;
-        ptx::mbar_wait(&acc_empty[buf], ((ai >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint32_t d_tmem = tmem_base + buf * 16;
-#pragma unroll 1
-          for (int ky = 0; ky < 3; ++ky) {
-            const uint32_t a_row = ptx::smem_u32(sRow + ((base + j + ky) % kCoSlots) * kCoSlotBytes);
+    // ------------------------------------------------------------------ MMA issuer (one thread)
+    // input row i of the CTA's global sequence -> E slot i % kCoE; it waits for the slot's previous
+    // occupant E_{i-4}, whose last reader is the epilogue of output row i - 4 of the same band (or
+    // the band's end)
+    if (ptx::elect_one()) {
+      uint32_t gi = 0;
+      const uint64_t b_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+      for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+        for (int r = 0; r < rows_in; ++r, ++gi) {
+          const uint32_t s_row = gi % kCoSlots, e = gi % kCoE;
+          ptx::mbar_wait(&slot_xf[s_row], (gi / kCoSlots) & 1);
+          ptx::mbar_wait(&acc_empty[e], ((gi / kCoE) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint64_t a_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sRow + s_row * kCoSlotBytes));
+          const uint32_t d_tmem = tmem_base + e * 16;
 #pragma unroll
-            for (int kx = 0; kx < 3; ++kx) {
+          for (int kx = 0; kx < 3; ++kx) {
 #pragma unroll
-              for (int cb = 0; cb < 2; ++cb) {
-                const uint64_t a_desc = ptx::sdesc_k_sw128(a_row + cb * kCoCbPitch + kx * 128);
-                const uint64_t b_desc = ptx::sdesc_k_sw128(ptx::smem_u32(sB + ((ky * 3 + kx) * 2 + cb) * 2048));
+            for (int cb = 0; cb < 2; ++cb) {
+              const uint64_t a_desc = a_desc0 + (uint64_t)((cb * kCoCbPitch + kx * 128) >> 4);
+              const uint64_t b_desc = b_desc0 + (uint64_t)(((kx * 2 + cb) * 2048) >> 4);
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  ptx::mma_f16_ss<1>(d_tmem, a_desc + 2 * k, b_desc + 2 * k, kCoIdesc, (ky | kx | cb | k) != 0);
-              }
+              for (int k = 0; k < 4; ++k)
+                ptx::mma_f16_ss<1>(d_tmem, a_desc + 2 * k, b_desc + 2 * k, kCoIdesc, (kx | cb | k) != 0);
             }
           }
-          ptx::mma_commit<1>(&acc_full[buf]);
-          ptx::mma_commit<1>(&slot_empty[(base + j) % kCoSlots]);  // input row j is done
+          ptx::mma_commit<1>(&acc_full[e]);
+          ptx::mma_commit<1>(&slot_empty[s_row]);  // the input row is consumed
         }
-        __syncwarp();
       }
-      if (ptx::elect_one()) {  // the band's last two input rows
-        ptx::mma_commit<1>(&slot_empty[(base + p.R) % kCoSlots]);
-        ptx::mma_commit<1>(&slot_empty[(base + p.R + 1) % kCoSlots]);
-      }
-      __syncwarp();
-      gi = base + rows_in;
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------------ epilogue (one pixel per thread)
+    // output row j of a band whose first input row has global index base: E_{base+j} (ky = 0),
+    // E_{base+j+1} (ky = 1), E_{base+j+2} (ky = 2); afterwards E_{base+j} has no later reader
     const uint32_t q = warp & 3;
     const float b0 = p.bias[0], b1 = p.bias[1], b2 = p.bias[2];
-    uint32_t ai = 0;
+    uint32_t gi = 0;
     for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
       int img, x0, y0;
       item_coords(p, it, img, x0, y0);
       const int x = x0 + (int)(q * 32 + lane);
-      for (int j = 0; j < p.R; ++j, ++ai) {
-        const uint32_t buf = ai & 1;
-        ptx::mbar_wait(&acc_full[buf], (ai >> 1) & 1);
-        ptx::tc_fence_after();
-        uint32_t r[4];
-        tmem_ld4(tmem_base + ((q * 32u) << 16) + buf * 16, r);
-        ptx::tmem_ld_wait();
+      const uint32_t base = gi;
+      for (int j = 0; j < p.R; ++j) {
+        float acc[3] = {b0, b1, b2};
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+          const uint32_t i = base + j + ky, e = i % kCoE;
+          ptx::mbar_wait(&acc_full[e], (i / kCoE) & 1);
+          ptx::tc_fence_after();
+          uint32_t r[4];
+          tmem_ld4(tmem_base + ((q * 32u) << 16) + e * 16 + ky * 4, r);
+          ptx::tmem_ld_wait();
+          acc[0] += __uint_as_float(r[0]);
+          acc[1] += __uint_as_float(r[1]);
+          acc[2] += __uint_as_float(r[2]);
+        }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_relaxed(&acc_empty[buf]);
-        const float acc[3] = {__uint_as_float(r[0]) + b0, __uint_as_float(r[1]) + b1, __uint_as_float(r[2]) + b2};
+        if (lane == 0) {
+          ptx::mbar_arrive_relaxed(&acc_empty[(base + j) % kCoE]);
+          if (j == p.R - 1) {  // the band's last two input rows have no later reader either
+            ptx::mbar_arrive_relaxed(&acc_empty[(base + j + 1) % kCoE]);
+            ptx::mbar_arrive_relaxed(&acc_empty[(base + j + 2) % kCoE]);
+          }
+        }
         uint8_t* o = p.rgb + (((size_t)img * p.H + (y0 + j)) * p.W + x) * 3;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -198,6 +221,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
           o[k] = (uint8_t)__float2int_rn(__fmul_rn(t, 255.f));  // round-half-even
         }
       }
+      gi = base + rows_in;
     }
   } else {
     // ------------------------------------------------------------------ transform (warps 6..13)
@@ -226,13 +250,25 @@ __global__ void __launch_bounds__(kCoThreads, 1)
         ptx::mbar_wait(&slot_full[s], (gi / kCoSlots) & 1);
         const int y = y0 - 1 + r;
         if (y >= 0 && y < p.H) {
-          uint8_t* blk = sRow + s * kCoSlotBytes + cb * kCoCbPitch;
-#pragma unroll 3
-          for (int px = p0; px < 130; px += 16) {
+          const uint32_t blk = ptx::smem_u32(sRow + s * kCoSlotBytes + cb * kCoCbPitch);  // shared-space
+                                                                                       // address: LDS/STS, not generic LD/ST
+          // all of this thread's chunks of the row (pixels p0 + 16k, k < 9) are loaded before any
+          // is transformed: nine independent LDS -> math -> STS chains instead of one at a time
+          constexpr int NK = 9;
+          uint4 v[NK];
+          bool ok[NK];
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            const int px = p0 + 16 * k;
             const int gx = x0 - 1 + px;
-            if (gx < 0 || gx >= p.W) continue;  // padding stays zero
-            uint4* q4 = reinterpret_cast<uint4*>(blk + px * 128 + ((lc ^ (px & 7)) << 4));
-            *q4 = H2 ? gn_act8_h2<true>(*q4, a, b) : gn_act8<true>(*q4, a, b);
+            ok[k] = px < 130 && gx >= 0 && gx < p.W;  // padding stays zero
+            if (ok[k]) v[k] = lds128(blk + px * 128 + ((lc ^ (px & 7)) << 4));
+          }
+#pragma unroll
+          for (int k = 0; k < NK; ++k) {
+            const int px = p0 + 16 * k;
+            if (ok[k])
+              sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_act8_h2<true>(v[k], a, b) : gn_act8<true>(v[k], a, b));
           }
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         }
@@ -246,7 +282,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<1>(tmem_base, 32);
+    ptx::tmem_dealloc<1>(tmem_base, 16 * kCoE);
   }
 }
 
