@@ -57,15 +57,6 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
                : "r"(taddr));
 }
 
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-
 __device__ __forceinline__ void item_coords(const CoParams& p, int it, int& img, int& x0, int& y0) {
   const int per_img = p.strips * p.bands;
   img = it / per_img;
@@ -262,13 +253,13 @@ __global__ void __launch_bounds__(kCoThreads, 1)
             const int px = p0 + 16 * k;
             const int gx = x0 - 1 + px;
             ok[k] = px < 130 && gx >= 0 && gx < p.W;  // padding stays zero
-            if (ok[k]) v[k] = lds128(blk + px * 128 + ((lc ^ (px & 7)) << 4));
+            if (ok[k]) v[k] = ptx::lds128(blk + px * 128 + ((lc ^ (px & 7)) << 4));
           }
 #pragma unroll
           for (int k = 0; k < NK; ++k) {
             const int px = p0 + 16 * k;
             if (ok[k])
-              sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_act8_h2<true>(v[k], a, b) : gn_act8<true>(v[k], a, b));
+              ptx::sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_act8_h2<true>(v[k], a, b) : gn_act8<true>(v[k], a, b));
           }
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         }

@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         if (j < n_a) {
           uint8_t* base = sA + st * p.a_stage_bytes;
           for (int bx = 0; bx < nbox; ++bx) {
-            uint8_t* hb = base + bx * p.halo_sub_bytes;
+            const uint32_t hb = ptx::smem_u32(base + bx * p.halo_sub_bytes);
             const int xs = x0 - 1 + bx * 128;
             int hr = (tid >> 3) / 130, px = (tid >> 3) - hr * 130;
             // two rows per iteration: independent MUFU chains per thread
@@ -422,14 +422,14 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
               const int r2 = r + 16;
               const bool v1 = y0 - 1 + hr >= 0 && y0 - 1 + hr < p.H && xs + px >= 0 && xs + px < p.W;
               const bool v2 = r2 < rows && y0 - 1 + hr2 >= 0 && y0 - 1 + hr2 < p.H && xs + px2 >= 0 && xs + px2 < p.W;
-              uint4* q1 = reinterpret_cast<uint4*>(hb + r * 128 + ((cq ^ (r & 7)) << 4));
-              uint4* q2 = reinterpret_cast<uint4*>(hb + r2 * 128 + ((cq ^ (r2 & 7)) << 4));
-              const uint4 u1 = v1 ? *q1 : make_uint4(0, 0, 0, 0);
-              const uint4 u2 = v2 ? *q2 : make_uint4(0, 0, 0, 0);
+              const uint32_t q1 = hb + r * 128 + ((cq ^ (r & 7)) << 4);
+              const uint32_t q2 = hb + r2 * 128 + ((cq ^ (r2 & 7)) << 4);
+              const uint4 u1 = v1 ? ptx::lds128(q1) : make_uint4(0, 0, 0, 0);
+              const uint4 u2 = v2 ? ptx::lds128(q2) : make_uint4(0, 0, 0, 0);
               const uint4 w1 = gn_act8_h2<true>(u1, ca, cb);
               const uint4 w2 = gn_act8_h2<true>(u2, ca, cb);
-              if (v1) *q1 = w1;
-              if (v2) *q2 = w2;
+              if (v1) ptx::sts128(q1, w1);
+              if (v2) ptx::sts128(q2, w2);
               px = px2 + 16;
               hr = hr2;
               if (px >= 130) { px -= 130; ++hr; }
@@ -462,7 +462,9 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     for (int j = 0; j < NCH; ++j) ghi[j] = glo[j] = 0.f;
     // bias of this warp's chunks, staged once per n-tile in the warp's own smem slice and read back
     // as broadcast LDS.128 (an LDG per chunk put the L1 latency on the epilogue's critical path)
-    float* wbias = sBias + (warp - 2) * (NCH * 32);
+    // shared-space address: the pointer arithmetic on the dynamic smem base makes the compiler emit
+    // generic LD.E/ST.E for plain dereferences (long-scoreboard stalls in ncu), so use LDS/STS
+    const uint32_t wbias = ptx::smem_u32(sBias) + (warp - 2) * (NCH * 32) * 4;
     int bias_ntile = -1;
     const bool scaled = p.row_scale != nullptr || p.alpha != 1.f;
     int g_img = -1, g_ntile = -1;
@@ -495,7 +497,10 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       if (p.bias && n_tile != bias_ntile) {
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < NCH; ++j) wbias[j * 32 + lane] = p.bias[n0 + (hsel + (EPI_WARPS / 4) * j) * 32 + lane];
+        for (int j = 0; j < NCH; ++j)
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(wbias + (j * 32 + lane) * 4),
+                       "f"(p.bias[n0 + (hsel + (EPI_WARPS / 4) * j) * 32 + lane])
+                       : "memory");
         __syncwarp();
         bias_ntile = n_tile;
       }
@@ -548,10 +553,12 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
           for (int i = 0; i < 32; ++i) v[i] *= rs;
         }
         if (p.bias) {
-          const float4* bv = reinterpret_cast<const float4*>(wbias + j * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 b = bv[i];
+            float4 b;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                         : "r"(wbias + (j * 32 + 4 * i) * 4));
             v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
           }
         }
