@@ -157,6 +157,7 @@ typedef struct {
   double* gn_stats;
   int cta_group, bn;
   const float* gn_ss; /* optional: fused A' = SiLU(A * ss[img][c].x + ss[img][c].y) (conv3x3), float pairs */
+  int b_mn_major;     /* plain GEMM: B is [K][N] with N contiguous (row stride ldb) instead of [N][K] */
 } lbx_gemm_desc;
 lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
 /* Diagnostics.  halo_policy bits: 0 = halo staging when possible (else per-tap A staging); 1 disables
@@ -164,7 +165,8 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * 4 selects the CUDA-core conv_out tail; 5 gives halo convs two A stages and the rest of smem to B;
  * 6 uses horizontally (instead of vertically) adjacent sub-tiles for the two-sub-tile variant; 7 folds
  * identity residuals into the K loop at every width (default: epilogue add at >= 256 channels); 8
- * selects the register-staged GroupNorm apply instead of the bulk-copy (1-D TMA) one.
+ * selects the register-staged GroupNorm apply instead of the bulk-copy (1-D TMA) one; 9 transposes the
+ * attention's V with a kernel instead of reading it in place as an MN-major B operand.
  * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
 /* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],

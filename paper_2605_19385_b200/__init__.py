@@ -52,7 +52,8 @@ class GemmDesc(ctypes.Structure):
                 ("K2", ctypes.c_int), ("B", ctypes.c_void_p), ("ldb", ctypes.c_int), ("out", ctypes.c_void_p),
                 ("ldo", ctypes.c_int), ("bias", ctypes.c_void_p), ("resid", ctypes.c_void_p), ("ldr", ctypes.c_int),
                 ("row_scale", ctypes.c_void_p), ("alpha", ctypes.c_float), ("gn_stats", ctypes.c_void_p),
-                ("cta_group", ctypes.c_int), ("bn", ctypes.c_int), ("gn_ss", ctypes.c_void_p)]
+                ("cta_group", ctypes.c_int), ("bn", ctypes.c_int), ("gn_ss", ctypes.c_void_p),
+                ("b_mn_major", ctypes.c_int)]
 
 
 class _Desc(ctypes.Structure):
@@ -227,12 +228,13 @@ def _blob_arrays(blobs):
 
 
 def op_gemm(mode, M, N, K, A, lda, B, ldb, out, ldo, *, b=0, h=0, w=0, c=0, bias=0, resid=0, ldr=0, row_scale=0,
-            alpha=1.0, gn_stats=0, cta_group=0, bn=0, stream=0, a2=0, lda2=0, k2=0, gn_ss=0):
+            alpha=1.0, gn_stats=0, cta_group=0, bn=0, stream=0, a2=0, lda2=0, k2=0, gn_ss=0, b_mn_major=False):
     """Diagnostic entry to the tcgen05 GEMM/conv kernel (device pointers as ints).  a2/lda2/k2 add
     the extra K segment (lbx_op_gemm_desc)."""
-    if k2 or gn_ss:
+    if k2 or gn_ss or b_mn_major:
         d = GemmDesc(mode, M, N, K, A, lda, b, h, w, c, a2 or None, lda2, k2, B, ldb, out, ldo, bias or None,
-                     resid or None, ldr, row_scale or None, alpha, gn_stats or None, cta_group, bn, gn_ss or None)
+                     resid or None, ldr, row_scale or None, alpha, gn_stats or None, cta_group, bn, gn_ss or None,
+                     int(b_mn_major))
         check(lib().lbx_op_gemm_desc(ctypes.byref(d), stream or None))
         return
     check(lib().lbx_op_gemm(mode, M, N, K, A, lda, b, h, w, c, B, ldb, out, ldo, bias or None, resid or None, ldr,

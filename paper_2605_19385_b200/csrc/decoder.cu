@@ -563,12 +563,16 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       sq.alpha = 1.0f / std::sqrt(512.0f);
       if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
       LBX_LAUNCH(launch_softmax_rows(S, rowscale, L, L, s), "attn.softmax", 4.0 * L * (double)L);
-      LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose", 4.0 * L * 512.0);
       GemmArgs pv;
       pv.mode = GEMM_PLAIN;
       pv.M = L; pv.N = 512; pv.K = L;
       pv.A = S; pv.lda = L;
-      pv.Bw = Vt; pv.ldb = L;
+      if (v_transpose_legacy()) {
+        LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose", 4.0 * L * 512.0);
+        pv.Bw = Vt; pv.ldb = L;
+      } else {  // V read in place from the QKV buffer as an MN-major B operand (no transpose)
+        pv.Bw = base + 1024; pv.ldb = 1536; pv.b_mn_major = 1;
+      }
       pv.out = A_ + (size_t)i * L * 512; pv.ldo = 512;
       pv.row_scale = rowscale;
       if ((st = gemm(pv, "attn.pv")) != LBX_OK) return st;
@@ -912,6 +916,7 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   g.row_scale = d->row_scale; g.alpha = d->alpha;
   g.gn_stats = d->gn_stats; g.gn_cpg = d->N / 32;
   g.gn_ss = reinterpret_cast<const float2*>(d->gn_ss);
+  g.b_mn_major = d->b_mn_major;
   g.rows_per_img = (d->mode == 0) ? (d->b > 0 ? d->M / d->b : d->M) : d->h * d->w;
   cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), d->cta_group, d->bn);
   if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,

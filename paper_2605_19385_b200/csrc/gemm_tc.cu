@@ -51,6 +51,7 @@ struct KParams {
   int desc_base_mode;  // descriptor base-offset convention for row-shifted views (0 or 1)
   int msub;            // 128-row M sub-tiles per CTA sharing every B tile (1 or 2)
   int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
+  int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -285,8 +286,16 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
             if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
             const int k0 = p.halo ? tp * (p.cblocks * 64) + j * 64 : j * 64;  // K = (tap, channel)
             uint8_t* dst = sB + st * C::B_BYTES;
-            if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst, k0, b_row);
-            else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst, k0, b_row);
+            if (p.b_mn) {  // B_ROWS / 64 boxes of (64 N) x (64 K), one per 64-wide N atom
+              for (int na = 0; na < C::B_ROWS / 64; ++na) {
+                if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0);
+                else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0);
+              }
+            } else if constexpr (CG == 1) {
+              ptx::tma_load_2d(&tmB, &b_full[st], dst, k0, b_row);
+            } else {
+              ptx::tma_load_2d_pair(&tmB, &b_full[st], dst, k0, b_row);
+            }
             if (++st == p.b_stages) { st = 0; ph ^= 1; }
           }
         }
@@ -311,7 +320,12 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint64_t a_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
-      const uint64_t b_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+      // MN-major B (SW128 canonical ((8,n),(8,k)) in 16-byte units): LBO = 8 KB between 64-wide N
+      // atoms, SBO = 1 KB between 8-row K groups; a K16 step is two K groups (+2 KB)
+      const uint64_t b_desc0 = p.b_mn ? ptx::sdesc_mn_sw128(ptx::smem_u32(sB), 8192, 1024)
+                                      : ptx::sdesc_k_sw128(ptx::smem_u32(sB));
+      const uint32_t b_k16 = p.b_mn ? (2048 >> 4) : 2;
+      const uint32_t idesc = C::IDESC | (p.b_mn ? (1u << 16) : 0u);
       const uint32_t a_stage16 = (uint32_t)p.a_stage_bytes >> 4, sub16 = (uint32_t)p.halo_sub_bytes >> 4;
       const int msub = p.msub;
       const bool conv = p.mode == GEMM_CONV3X3, halo = p.halo != 0, dbm = p.desc_base_mode != 0;
@@ -337,7 +351,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
                 if (dbm) a_desc |= (uint64_t)(r0 & 7) << 49;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide k-block; +32 B per step inside the swizzle atom
-                  ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, (j | tp | k) != 0);
+                  ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + b_k16 * k, idesc, (j | tp | k) != 0);
               }
             }
             ptx::mma_commit<CG>(&b_empty[bs]);
@@ -364,7 +378,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
               const uint64_t a_desc = a_stage + (uint64_t)(sub * (16384 >> 4));
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + 2 * k, C::IDESC, 1u);
+                ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + b_k16 * k, idesc, 1u);
             }
           }
           ptx::mma_commit<CG>(&b_empty[bs]);
@@ -687,6 +701,7 @@ static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to 
                                    // equal for c128, ~3% slower for the 256-wide c512 / sub-pixel tiles)
 static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
+static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_halo_policy = halo_policy & 1;
   g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
@@ -695,6 +710,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_stage_policy = (halo_policy >> 5) & 1;
   g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
   g_fold_always = (halo_policy >> 7) & 1;
+  g_vt_legacy = (halo_policy >> 9) & 1;
 }
 
 template <int BN, int CG, bool XF>
@@ -749,7 +765,12 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   } else {
     tmA2 = tmA;
   }
-  {
+  if (kp.b_mn) {  // B stored [K][N] (row stride ldb): boxes of 64 N x 64 K
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.K};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ldb * 2};
+    cuuint32_t box[2] = {64, 64};
+    if (!make_map(&tmB, a.Bw, 2, dims, strides, box)) return cudaErrorInvalidValue;
+  } else {
     const int brows = a.mode == GEMM_SUBPIX ? 4 * a.N : a.N;
     cuuint64_t dims[2] = {(cuuint64_t)(a.K + a.K2), (cuuint64_t)brows};
     cuuint64_t strides[1] = {(cuuint64_t)a.ldb * 2};
@@ -795,6 +816,7 @@ bool gemm_tc_prepare() {
 }
 
 bool resid_fold_always() { return g_fold_always != 0; }
+bool v_transpose_legacy() { return g_vt_legacy != 0; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments); four extra warps transform each landed halo
@@ -827,6 +849,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
     kp.halo_rows = a.mode == GEMM_CONV3X3 ? 3 : 2;
     kp.halo = (g_halo_policy && kp.Ht == 1) ? 1 : 0;  // a tap's 128 rows must be contiguous in the halo
     kp.desc_base_mode = g_desc_base_mode;
+  }
+  if (a.b_mn_major) {  // plain GEMM only, no extra K segment
+    if (a.mode != GEMM_PLAIN || a.K2 || a.N % 64) return cudaErrorInvalidValue;
+    kp.b_mn = 1;
   }
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;

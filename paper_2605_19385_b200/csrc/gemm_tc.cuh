@@ -30,9 +30,11 @@ struct GemmArgs {
   // optional fused GroupNorm + SiLU on the A operand (conv3x3 halo mode): A' = SiLU(A * a_c + b_c),
   // (a_c, b_c) = gn_ss[image][channel]; out-of-image padding stays zero (applied after SiLU).
   const float2* gn_ss = nullptr;
-  // B operand: weights [N][K + K2] K-major (conv: K index = (ky*3+kx)*C + ci)
+  // B operand: weights [N][K + K2] K-major (conv: K index = (ky*3+kx)*C + ci); with b_mn_major
+  // (plain GEMM) B is [K][N] with N contiguous (row stride ldb), e.g. V of the attention for P.V
   const __half* Bw = nullptr;
   int ldb = 0;
+  int b_mn_major = 0;
   // epilogue
   __half* out = nullptr;
   int ldo = 0;
@@ -57,6 +59,8 @@ bool gemm_tc_can_fuse_gn(const GemmArgs& a);
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
 // Debug bit 7: fold identity residuals into the K loop at every width (default: only at 128 channels).
 bool resid_fold_always();
+// Debug bit 9: transpose V with a kernel for P.V (default: V read in place as an MN-major B).
+bool v_transpose_legacy();
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();

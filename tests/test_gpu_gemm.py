@@ -57,6 +57,24 @@ def test_gemm_epilogue(lbx, cg):
     _close(out, ref)
 
 
+@pytest.mark.parametrize("cg,bn", [(1, 128), (1, 256), (2, 128), (2, 256)])
+@pytest.mark.parametrize("M,N,K,ldb", [(512, 512, 512, 512), (1024, 256, 1024, 1536), (256, 512, 2048, 1536)])
+def test_gemm_mn_major_b(lbx, cg, bn, M, N, K, ldb):
+    """B given as [K][N] (N contiguous, row stride ldb) -- the attention's V inside the QKV buffer
+    for P.V, no transpose kernel -- staged as 64-wide MN atoms with an MN-major UMMA descriptor."""
+    if N % bn:
+        pytest.skip("N not a multiple of the tile")
+    A = _rand(M, K, seed=31)
+    Bfull = _rand(K, ldb, scale=K ** -0.5, seed=32)
+    B = Bfull[:, ldb - N:] if ldb > N else Bfull  # a column window, like V at columns 1024..1535
+    rs = torch.rand(M, device="cuda") + 0.5
+    out = torch.empty(M, N, dtype=torch.half, device="cuda")
+    lbx.op_gemm(0, M, N, K, A.data_ptr(), K, B.data_ptr(), ldb, out.data_ptr(), N, row_scale=rs.data_ptr(),
+                cta_group=cg, bn=bn, b_mn_major=True)
+    torch.cuda.synchronize()
+    _close(out, rs[:, None] * (A.float() @ B.float()))
+
+
 def test_gemm_strided_views(lbx):
     """Q K^T on column views of a [L, 1536] QKV buffer (row stride 1536), as the attention uses."""
     L = 512
