@@ -21,15 +21,20 @@ __device__ __forceinline__ float silu_f(float x) {
   return x * r;
 }
 
-// GroupNorm affine of one channel from fp64 (sum, sumsq) over `count` values -- the single
+// GroupNorm affine of one channel from fp64 (sum, sumsq) over 1/inv_count values -- the single
 // definition of the finalize arithmetic: y = x * a + b with a = gamma * rstd, b = beta - mean * a.
-__device__ __forceinline__ float2 gn_affine(double s, double s2, double count, float gamma, float beta, float eps) {
-  const double mean = s / count;
-  double var = s2 / count - mean * mean;
+// Mean and variance stay fp64 (the E[x^2] - mean^2 cancellation), but only multiplies: the fp64
+// divide / sqrt sequences cost too much when every apply thread finalizes its own channels;
+// rstd is an IEEE fp32 sqrt + divide of the fp32-rounded variance.
+__device__ __forceinline__ float2 gn_affine(double s, double s2, double inv_count, float gamma, float beta,
+                                            float eps) {
+  const double inv = inv_count;  // 1 / values per group, computed once on the host
+  const double mean = s * inv;
+  double var = fma(s2, inv, -mean * mean);
   if (var < 0) var = 0;
-  const double rstd = 1.0 / sqrt(var + (double)eps);
-  const double a = (double)gamma * rstd;
-  return make_float2((float)a, (float)((double)beta - mean * a));
+  const float rstd = 1.0f / sqrtf((float)var + eps);
+  const float a = gamma * rstd;
+  return make_float2(a, (float)fma(-mean, (double)a, (double)beta));
 }
 
 // 8 packed fp16 -> act(x * a + b) -> 8 packed fp16 (fp32 math, one rounding).

@@ -450,8 +450,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     return e;
   };
   auto gn = [&](int st_site, const NormW& nw, const __half* x, __half* y, int C, int hw, bool silu) -> lbx_status {
-    LBX_LAUNCH(launch_gn_finalize(site_ptr(st_site), nw.g, nw.b, ss, n, C, (double)hw * (C / 32), 1e-6f, s), "gn_finalize", n * C * 8.0);
-    LBX_LAUNCH(launch_gn_apply(x, y, ss, (long long)n * hw, hw, C, silu, h2, s),
+    const GnSrc gs{site_ptr(st_site), nw.g, nw.b, 1.0 / ((double)hw * (C / 32)), 1e-6f};
+    LBX_LAUNCH(launch_gn_apply(x, y, gs, (long long)n * hw, hw, C, silu, h2, s),
                std::string(silu ? "gn_apply_silu c" : "gn_apply c") + std::to_string(C) + " hw" + std::to_string(hw),
                4.0 * n * (double)hw * C);
     return LBX_OK;
@@ -980,13 +980,9 @@ lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const f
   if (!x || !y || !stats || !gamma || !beta || !(c == 128 || c == 256 || c == 512))
     return set_err(LBX_E_CONFIG, "lbx_op_groupnorm: bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  float2* ss = nullptr;
-  if (cudaMallocAsync(&ss, (size_t)b * c * sizeof(float2), s) != cudaSuccess)
-    return set_err(LBX_E_CUDA, "cudaMallocAsync");
-  lbx::launch_gn_finalize(stats, gamma, beta, ss, b, c, (double)hw * (c / 32), eps, s);
-  lbx::launch_gn_apply(reinterpret_cast<const __half*>(x), reinterpret_cast<__half*>(y), ss, (long long)b * hw, hw, c,
+  const lbx::GnSrc gs{stats, gamma, beta, 1.0 / ((double)hw * (c / 32)), eps};
+  lbx::launch_gn_apply(reinterpret_cast<const __half*>(x), reinterpret_cast<__half*>(y), gs, (long long)b * hw, hw, c,
                        silu != 0, silu == 2, s);
-  cudaFreeAsync(ss, s);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));
   return LBX_OK;

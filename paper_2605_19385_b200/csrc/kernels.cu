@@ -72,25 +72,32 @@ void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, in
 // ----------------------------------------------------------------------------- GroupNorm
 __global__ void gn_finalize_kernel(const double* __restrict__ stats, const float* __restrict__ gamma,
                                    const float* __restrict__ beta, float2* __restrict__ ss, int n, int C,
-                                   double count, float eps) {
+                                   double inv_count, float eps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * C) return;
   const int img = i / C, c = i - img * C;
   const int g = c / (C / 32);
-  ss[i] = gn_affine(stats[(img * 32 + g) * 2], stats[(img * 32 + g) * 2 + 1], count, gamma[c], beta[c], eps);
+  ss[i] = gn_affine(stats[(img * 32 + g) * 2], stats[(img * 32 + g) * 2 + 1], inv_count, gamma[c], beta[c], eps);
 }
 
 void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
                         double count, float eps, cudaStream_t s) {
-  gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, count, eps);
+  gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, 1.0 / count, eps);
+}
+
+// The apply kernels finalize the statistics themselves (the same gn_affine arithmetic as
+// gn_finalize_kernel, so results are bit-identical): one launch per GroupNorm site instead of two.
+__device__ __forceinline__ float2 site_affine(const GnSrc& g, int img, int c, int cpg) {
+  const double* st = g.stats + ((size_t)img * 32 + c / cpg) * 2;
+  return gn_affine(__ldg(st), __ldg(st + 1), g.inv_count, __ldg(g.gamma + c), __ldg(g.beta + c), g.eps);
 }
 
 // y = act(x * a_c + b_c).  The launch is exactly one resident wave; block b covers a contiguous
 // range of the flattened (image, pixel) space, split at image boundaries.  Thread t owns channel
 // octet t % (C/8) for every pixel it visits, so its 8 affine pairs are reloaded only per image.
 template <bool SILU, int CV, bool H2>
-__global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* y, const float2* __restrict__ ss,
-                                                       int hw, long long total, long long pix_per_block) {
+__global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* y, const GnSrc g, int hw,
+                                                       long long total, long long pix_per_block) {
   constexpr int PSTEP = 256 / CV;  // pixels advanced per iteration of the block
   const int cvec = threadIdx.x % CV;
   const long long end = min(total, (blockIdx.x + 1) * pix_per_block);
@@ -103,7 +110,7 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
     float a[8], b[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const float2 t = ss[(size_t)img * CV * 8 + cvec * 8 + k];
+      const float2 t = site_affine(g, img, cvec * 8 + k, CV / 4);
       a[k] = t.x;
       b[k] = t.y;
     }
@@ -148,7 +155,7 @@ __device__ __forceinline__ void bulk_wait_read() {
 }
 
 template <bool SILU, int CV, bool H2>
-__global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, __half* y, const float2* __restrict__ ss,
+__global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, __half* y, const GnSrc g,
                                                               long long img_bytes, long long chunks) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = smem_raw;
@@ -177,11 +184,11 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
     const int st = (int)(k % kApStages);
     const long long c = first + k * step;
     const int img = (int)(c * kApChunk / img_bytes);
-    if (img != cur_img) {
+    if (img != cur_img) {  // finalize this thread's 8 channels of the new image
       cur_img = img;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float2 t = ss[(size_t)img * CV * 8 + cvec * 8 + j];
+        const float2 t = site_affine(g, img, cvec * 8 + j, CV / 4);
         a[j] = t.x;
         b[j] = t.y;
       }
@@ -213,7 +220,7 @@ static bool g_apply_bulk = true;  // bulk-copy apply (debug bit 8 selects the re
 void kernels_set_apply_bulk(bool on) { g_apply_bulk = on; }
 
 template <bool SILU, int CV, bool H2>
-static bool gn_apply_bulk_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
+static bool gn_apply_bulk_launch(const __half* x, __half* y, const GnSrc& g, int n, int hw, cudaStream_t s) {
   const long long img_bytes = (long long)hw * CV * 16;
   // measured per site in the decoder: faster at 128 and 512 channels (5.8 / 6.6 TB/s vs 5.2 / 5.5),
   // slower at 256 (4.0-5.0 vs 5.2-5.3 TB/s), where the register-staged kernel stays
@@ -228,7 +235,7 @@ static bool gn_apply_bulk_launch(const __half* x, __half* y, const float2* ss, i
   }
   const long long chunks = (long long)n * img_bytes / kApChunk;
   const int grid = (int)(chunks < num_sms() ? chunks : num_sms());
-  gn_apply_bulk_kernel<SILU, CV, H2><<<grid, 256, smem, s>>>(x, y, ss, img_bytes, chunks);
+  gn_apply_bulk_kernel<SILU, CV, H2><<<grid, 256, smem, s>>>(x, y, g, img_bytes, chunks);
   return true;
 }
 
@@ -237,8 +244,8 @@ void kernels_set_conv_out_legacy(bool on) { g_conv_out_legacy = on; }
 bool kernels_conv_out_legacy() { return g_conv_out_legacy; }
 
 template <bool SILU, int CV, bool H2>
-static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n, int hw, cudaStream_t s) {
-  if (gn_apply_bulk_launch<SILU, CV, H2>(x, y, ss, n, hw, s)) return;
+static void gn_apply_launch(const __half* x, __half* y, const GnSrc& g, int n, int hw, cudaStream_t s) {
+  if (gn_apply_bulk_launch<SILU, CV, H2>(x, y, g, n, hw, s)) return;
   static int occ = 0;
   if (!occ) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gn_apply_kernel<SILU, CV, H2>, 256, 0);
@@ -250,27 +257,27 @@ static void gn_apply_launch(const __half* x, __half* y, const float2* ss, int n,
   long long ppb = (total + blocks - 1) / blocks;
   ppb = (ppb + PSTEP - 1) / PSTEP * PSTEP;
   const int grid = (int)((total + ppb - 1) / ppb);
-  gn_apply_kernel<SILU, CV, H2><<<grid, 256, 0, s>>>(x, y, ss, hw, total, ppb);
+  gn_apply_kernel<SILU, CV, H2><<<grid, 256, 0, s>>>(x, y, g, hw, total, ppb);
 }
 
 template <bool SILU, bool H2>
-static void gn_apply_dispatch(const __half* x, __half* y, const float2* ss, int n, int hw, int C, cudaStream_t s) {
+static void gn_apply_dispatch(const __half* x, __half* y, const GnSrc& g, int n, int hw, int C, cudaStream_t s) {
   switch (C / 8) {
-    case 16: gn_apply_launch<SILU, 16, H2>(x, y, ss, n, hw, s); break;
-    case 32: gn_apply_launch<SILU, 32, H2>(x, y, ss, n, hw, s); break;
-    case 64: gn_apply_launch<SILU, 64, H2>(x, y, ss, n, hw, s); break;
+    case 16: gn_apply_launch<SILU, 16, H2>(x, y, g, n, hw, s); break;
+    case 32: gn_apply_launch<SILU, 32, H2>(x, y, g, n, hw, s); break;
+    case 64: gn_apply_launch<SILU, 64, H2>(x, y, g, n, hw, s); break;
     default: break;  // C validated by callers (128 / 256 / 512)
   }
 }
 
-void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
-                     bool h2, cudaStream_t s) {
+void launch_gn_apply(const __half* x, __half* y, const GnSrc& g, long long rows, int hw, int C, bool silu, bool h2,
+                     cudaStream_t s) {
   const int n = (int)(rows / hw);
   if (silu) {
-    if (h2) gn_apply_dispatch<true, true>(x, y, ss, n, hw, C, s);
-    else gn_apply_dispatch<true, false>(x, y, ss, n, hw, C, s);
+    if (h2) gn_apply_dispatch<true, true>(x, y, g, n, hw, C, s);
+    else gn_apply_dispatch<true, false>(x, y, g, n, hw, C, s);
   } else {
-    gn_apply_dispatch<false, false>(x, y, ss, n, hw, C, s);
+    gn_apply_dispatch<false, false>(x, y, g, n, hw, C, s);
   }
 }
 

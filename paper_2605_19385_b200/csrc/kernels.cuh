@@ -16,10 +16,20 @@ void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, in
 void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
                         double count, float eps, cudaStream_t s);
 
-// y = act(x * ss.x + ss.y), x/y fp16 [n*hw][C] (y may alias x), act = SiLU if silu else identity.
-// h2: packed-half SiLU (act.cuh gn_act8_h2) instead of the fp32 one (gn_act8).
-void launch_gn_apply(const __half* x, __half* y, const float2* ss, long long rows, int hw, int C, bool silu,
-                     bool h2, cudaStream_t s);
+// One GroupNorm site: fp64 statistics [n][32][2] over 1/inv_count values per group, affine, eps.
+struct GnSrc {
+  const double* stats;
+  const float* gamma;
+  const float* beta;
+  double inv_count;
+  float eps;
+};
+
+// y = act(GN(x)), x/y fp16 [n*hw][C] (y may alias x), act = SiLU if silu else identity; the kernel
+// finalizes the statistics itself (same arithmetic as launch_gn_finalize).  h2: packed-half SiLU
+// (act.cuh gn_act8_h2) instead of the fp32 one (gn_act8).
+void launch_gn_apply(const __half* x, __half* y, const GnSrc& g, long long rows, int hw, int C, bool silu, bool h2,
+                     cudaStream_t s);
 
 // Row softmax numerator in place: P = exp(S - rowmax(S)) (fp16), row_scale = 1 / sum(P) (fp32).
 void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s);
