@@ -101,18 +101,13 @@ __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank,
   return (img * p.H + yp * p.msub + sub) * p.W + x0;
 }
 
-// Per-chunk GroupNorm partials.  xs holds this lane's 32 output values (one pixel, 32 consecutive
-// channels).  NV = 2 * groups-per-chunk values per lane (group sums,
-// then group sums of squares) are reduce-scattered across the warp with NV + log2(32/NV)
-// shuffles (instead of 5 * NV for a butterfly per value): lane L ends up owning the warp total
-// of value index (L >> (5 - log2 NV)) & (NV - 1).
-// The partials are of the fp32 values just before the fp16 rounding of the store (the rounding
-// is < 2^-12 relative and unbiased; summing the fp32 values skips one HADD2.F32 per element).
+// Per-lane GroupNorm partials of one chunk: NV = 2 * (groups per chunk) values -- the group sums,
+// then the group sums of squares of this lane's 32 fp32 outputs -- added to the lane's running
+// accumulators a[0..NV).  The cross-lane reduction happens once per flush (warp_flush_stats), not per
+// chunk: it was two thirds of the epilogue's instructions.
 template <int NV>
-__device__ __forceinline__ float chunk_group_stats(const float (&xs)[32], uint32_t lane) {
-  constexpr int G = NV / 2, E = 32 / G;  // elements per group
-  constexpr int LG = NV == 16 ? 4 : (NV == 8 ? 3 : 2);
-  float v[NV];
+__device__ __forceinline__ void lane_group_stats(const float (&xs)[32], float* a) {
+  constexpr int G = NV / 2, E = 32 / G;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     float s = 0.f, s2 = 0.f;
@@ -121,27 +116,27 @@ __device__ __forceinline__ float chunk_group_stats(const float (&xs)[32], uint32
       s += xs[g * E + i];
       s2 = fmaf(xs[g * E + i], xs[g * E + i], s2);
     }
-    v[g] = s;
-    v[G + g] = s2;
+    a[g] += s;
+    a[G + g] += s2;
   }
+}
+
+// Reduce-scatter 32 per-lane values across the warp (31 shuffles): lane L returns the warp total of
+// value index L.
+__device__ __forceinline__ float warp_reduce_scatter32(float (&x)[32], uint32_t lane) {
 #pragma unroll
-  for (int lvl = 0; lvl < LG; ++lvl) {
-    const int cnt = NV >> lvl;
-    const int o = 16 >> lvl;
+  for (int lvl = 0; lvl < 5; ++lvl) {
+    const int cnt = 32 >> lvl, o = 16 >> lvl;
     const bool upper = (lane & o) != 0;
 #pragma unroll
     for (int i = 0; i < cnt / 2; ++i) {
-      const float send = upper ? v[i] : v[i + cnt / 2];
-      const float keep = upper ? v[i + cnt / 2] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      const float send = upper ? x[i] : x[i + cnt / 2];
+      const float keep = upper ? x[i + cnt / 2] : x[i];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
     }
   }
-  float x = v[0];
-#pragma unroll
-  for (int o = 16 >> LG; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-  return x;
+  return x[0];
 }
-
 
 template <int BN, int CG, bool XF>
 __global__ void __launch_bounds__(XF ? 480 : 352, 1)
@@ -466,14 +461,13 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     const int hsel = (int)(warp - 2) >> 2;
     const int row = q * 32 + lane;
     constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
-    // GroupNorm partials: after the per-chunk reduce-scatter each lane owns one (group, sum|sumsq)
-    // value per chunk; lanes accumulate those across tiles as unevaluated fp32 pairs (TwoSum: hi +
-    // lo carries the rounding error exactly, ~fp64 accuracy without the FP64 pipe, which stalled
-    // the epilogue) and flush with one fp64 atomic per owned value only when the (image, n-tile)
-    // changes -- not once per tile.
-    float ghi[NCH], glo[NCH];
+    // GroupNorm partials: each lane accumulates its own per-chunk (group sum, group sumsq) values in
+    // fp32 registers across tiles (NCH x NV <= 32 of them); at a flush -- when the (image, n-tile)
+    // changes -- the warp reduce-scatters them (lane L owns value L) and adds them with one fp64
+    // atomic per value.
+    float sacc[32];
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) ghi[j] = glo[j] = 0.f;
+    for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
     // bias of this warp's chunks, staged once per n-tile in the warp's own smem slice and read back
     // as broadcast LDS.128 (an LDG per chunk put the L1 latency on the epilogue's critical path)
     // shared-space address: the pointer arithmetic on the dynamic smem base makes the compiler emit
@@ -483,24 +477,19 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     const bool scaled = p.row_scale != nullptr || p.alpha != 1.f;
     int g_img = -1, g_ntile = -1;
     const int nv = p.gn_stats ? 64 / p.gn_cpg : 0;  // values per chunk: 2 * groups-per-chunk
-    const int lg = nv == 16 ? 4 : (nv == 8 ? 3 : 2);
-    const int own = nv ? (int)(lane >> (5 - lg)) & (nv - 1) : 0;
-    const bool rep = nv ? (lane & ((1u << (5 - lg)) - 1u)) == 0 : false;
     auto flush = [&]() {
       if (g_img < 0) return;
-      if (rep) {
+      const float tot = warp_reduce_scatter32(sacc, lane);
+      if ((int)lane < nv * NCH) {
+        const int j = (int)lane / nv, i = (int)lane - j * nv;
         const int gpc = nv >> 1;  // groups per chunk
-        const int kind = own >= gpc;
-        const int g_in = own - kind * gpc;
-#pragma unroll
-        for (int j = 0; j < NCH; ++j) {
-          const int c = hsel + (EPI_WARPS / 4) * j;
-          const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + g_in;
-          atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, (double)ghi[j] + (double)glo[j]);
-        }
+        const int kind = i >= gpc;
+        const int c = hsel + (EPI_WARPS / 4) * j;
+        const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + (i - kind * gpc);
+        atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, (double)tot);
       }
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) ghi[j] = glo[j] = 0.f;
+      for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
     };
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -607,16 +596,14 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
 #pragma unroll
         for (int i = 0; i < 4; ++i) op[i] = pk[i];
-        if (p.gn_stats) {
-          float val;
-          if (nv == 16) val = chunk_group_stats<16>(v, lane);
-          else if (nv == 8) val = chunk_group_stats<8>(v, lane);
-          else val = chunk_group_stats<4>(v, lane);
-          // TwoSum(ghi, val): exact error term accumulated in glo
-          const float sum = ghi[j] + val;
-          const float bb = sum - ghi[j];
-          glo[j] += (ghi[j] - (sum - bb)) + (val - bb);
-          ghi[j] = sum;
+        if (p.gn_stats) {  // NCH * nv <= 32 always (nv = 16 only with 128-wide tiles, NCH = 2)
+          if (nv == 16) {
+            if constexpr (NCH <= 2) lane_group_stats<16>(v, sacc + j * 16);
+          } else if (nv == 8) {
+            if constexpr (NCH <= 4) lane_group_stats<8>(v, sacc + j * 8);
+          } else {
+            lane_group_stats<4>(v, sacc + j * 4);
+          }
         }
       }
       }  // sub-tiles
