@@ -520,11 +520,12 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       g.mode = GEMM_CONV3X3;
       g.M = n * hw; g.N = R.cout; g.K = 9 * R.cout;
       g.B_img = n; g.H = H; g.W = W; g.C = R.cout;
-      // identity residual at >= 256 channels: added in the epilogue (in place: each thread reads its
-      // residual chunk before writing it).  Folding it as 4-8 short extra k-blocks starves the MMA
-      // (each lasts 4 MMAs against a full TMA round trip) -- measured 5-10% slower there, while at
-      // 128 channels (2 extra k-blocks) the fold wins.  A 1x1 shortcut is always folded.
-      const bool epi_resid = R.cin == R.cout && R.cout >= 256 && !resid_fold_always();
+      // identity residual: preloaded into the TMEM accumulator by the epilogue warps before the
+      // tile's MMAs (gemm_tc rpf; in place: a tile's residual rows are read before its outputs are
+      // written).  Without the preload (debug bit 10) it is added in the epilogue at >= 256
+      // channels and folded as extra K at 128.  A 1x1 shortcut is always folded.
+      const bool epi_resid =
+          R.cin == R.cout && !resid_fold_always() && (resid_preload() || R.cout >= 256);
       if (epi_resid) {
         g.resid = X_; g.ldr = R.cout;
       } else {

@@ -52,6 +52,7 @@ struct KParams {
   int msub;            // 128-row M sub-tiles per CTA sharing every B tile (1 or 2)
   int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
   int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
+  int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -327,9 +328,11 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       for (int t = cluster_id; t < p.tiles; t += nclusters) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
-        ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        // rpf: every use of a buffer (the first included) waits for the epilogue's residual preload
+        ptx::mbar_wait_cluster(&tempty[acc], p.rpf ? acc_phase : acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * (msub * BN);
+        const uint32_t acc0 = p.rpf ? 1u : 0u;  // accumulate onto the preloaded residual
         for (int j = 0; j < n_a; ++j) {
           if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
           else ptx::mbar_wait(&a_full[as], aph);
@@ -346,7 +349,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
                 if (dbm) a_desc |= (uint64_t)(r0 & 7) << 49;
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // 4 x K16 per 64-wide k-block; +32 B per step inside the swizzle atom
-                  ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + b_k16 * k, idesc, (j | tp | k) != 0);
+                  ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + b_k16 * k, idesc, (acc0 | j | tp | k) != 0);
               }
             }
             ptx::mma_commit<CG>(&b_empty[bs]);
@@ -491,6 +494,50 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
 #pragma unroll
       for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
     };
+    // Residual preload (rpf): the residual of tile tn goes into accumulator buffer `buf` (fp16 ->
+    // fp32, tcgen05.st) before its MMAs start, which then accumulate onto it; the release of the
+    // buffer to the MMA issuer is the arrival after the preload.  It replaces the folded extra K
+    // (4-8 short k-blocks of MMAs) and the epilogue's late residual reads.
+    auto prefill = [&](int tn, int buf) {
+      if (tn < p.tiles) {
+        int mt, nt, phn;
+        tile_coords(p, tn, mt, nt, phn);
+        for (int sub = 0; sub < p.msub; ++sub) {
+          const long long mrow = tile_row0(p, mt, (int)rank, CG, sub) + row;
+          const __half* rb = p.resid + mrow * p.ldr + nt * BN + hsel * 32;
+          const uint32_t tb = tmem_base + ((q * 32u) << 16) + buf * (p.msub * BN) + sub * BN;
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            uint4 u[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(rb + j * 32 * (EPI_WARPS / 4)) + i);
+            uint32_t r[32];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint32_t w4[4] = {u[i].x, u[i].y, u[i].z, u[i].w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
+                r[i * 8 + 2 * k] = __float_as_uint(f.x);
+                r[i * 8 + 2 * k + 1] = __float_as_uint(f.y);
+              }
+            }
+            ptx::tmem_st32(tb + (hsel + (EPI_WARPS / 4) * j) * 32, r);
+          }
+        }
+        ptx::tmem_st_wait();
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty[buf]);
+        else ptx::mbar_arrive_cluster_relaxed(&tempty[buf], 0);
+      }
+    };
+    if (p.rpf) {
+      prefill(cluster_id, 0);
+      prefill(cluster_id + nclusters, 1);
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster_id; t < p.tiles; t += nclusters) {
@@ -532,9 +579,10 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       // residual prefetch ring, two chunks deep, issued before waiting for the accumulator
       constexpr int PF = NCH < 2 ? NCH : 2;
       uint4 rr[PF][4];
-      const __half* rbase = p.resid ? p.resid + orow * p.ldr + n0 + hsel * 32 : nullptr;
+      const bool eresid = p.resid && !p.rpf;  // residual added here (not preloaded into TMEM)
+      const __half* rbase = eresid ? p.resid + orow * p.ldr + n0 + hsel * 32 : nullptr;
       constexpr int RSTRIDE = 32 * (EPI_WARPS / 4);  // columns between this warp's chunks
-      if (p.resid) {
+      if (eresid) {
 #pragma unroll
         for (int j = 0; j < PF; ++j)
 #pragma unroll
@@ -565,7 +613,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
             v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
           }
         }
-        if (p.resid) {
+        if (eresid) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const uint4 q4 = rr[j % PF][i];
@@ -607,11 +655,15 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         }
       }
       }  // sub-tiles
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty[acc]);
-        else ptx::mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+      if (p.rpf) {
+        prefill(t + 2 * nclusters, acc);  // this buffer's next tile: preload, then release
+      } else {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) ptx::mbar_arrive_relaxed(&tempty[acc]);
+          else ptx::mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+        }
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -689,6 +741,7 @@ static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to 
 static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
+static int g_rpf_policy = 1;       // 1: preload conv residuals into the TMEM accumulator (bit 10 clears)
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_halo_policy = halo_policy & 1;
   g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
@@ -698,6 +751,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
+  g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : 1;
 }
 
 template <int BN, int CG, bool XF>
@@ -804,6 +858,7 @@ bool gemm_tc_prepare() {
 
 bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
+bool resid_preload() { return g_rpf_policy != 0; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments); four extra warps transform each landed halo
@@ -842,6 +897,8 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
     kp.b_mn = 1;
   }
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
+  // residual preload into TMEM: conv mode, unscaled outputs (the preload would be scaled too)
+  kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||

@@ -61,6 +61,8 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
 bool resid_fold_always();
 // Debug bit 9: transpose V with a kernel for P.V (default: V read in place as an MN-major B).
 bool v_transpose_legacy();
+// Debug bit 10 clears: conv residuals preloaded into the TMEM accumulator (default on).
+bool resid_preload();
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();
