@@ -222,9 +222,9 @@ void kernels_set_apply_bulk(bool on) { g_apply_bulk = on; }
 template <bool SILU, int CV, bool H2>
 static bool gn_apply_bulk_launch(const __half* x, __half* y, const GnSrc& g, int n, int hw, cudaStream_t s) {
   const long long img_bytes = (long long)hw * CV * 16;
-  // measured per site in the decoder: faster at 128 and 512 channels (5.8 / 6.6 TB/s vs 5.2 / 5.5),
-  // slower at 256 (4.0-5.0 vs 5.2-5.3 TB/s), where the register-staged kernel stays
-  if (!g_apply_bulk || CV == 32 || img_bytes % kApChunk) return false;
+  // 6.3-6.45 TB/s at 128/256/512 channels alone (97% of the measured copy rate) vs 5.9-6.0 for
+  // the register-staged kernel (scripts/op_bench.py gn)
+  if (!g_apply_bulk || img_bytes % kApChunk) return false;
   constexpr int smem = kApStages * kApChunk + kApStages * 8;
   static bool attr = false;
   if (!attr) {

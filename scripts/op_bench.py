@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--fold", action="store_true", help="residual as an extra K segment (identity B)")
     ap.add_argument("--stats", action="store_true")
     ap.add_argument("--gnfuse", action="store_true", help="fused GroupNorm+SiLU on the A operand")
+    ap.add_argument("--inplace", action="store_true", help="gn: apply in place")
     ap.add_argument("--cg", type=int, default=0)
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--iters", type=int, default=3)
@@ -80,10 +81,12 @@ def main():
         y = torch.empty_like(x)
         lbx.op_gn_stats(x.data_ptr(), stats.data_ptr(), b, hw * hw, c)
         flops = 4.0 * x.numel()  # bytes
+        if a.inplace:
+            y = x
 
         def run():
             lbx.op_groupnorm(x.data_ptr(), y.data_ptr(), stats.data_ptr(), gamma.data_ptr(), beta.data_ptr(), b,
-                             hw * hw, c, True)
+                             hw * hw, c, 2)
 
     run()
     torch.cuda.synchronize()
