@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--stats", action="store_true")
     ap.add_argument("--gnfuse", action="store_true", help="fused GroupNorm+SiLU on the A operand")
     ap.add_argument("--inplace", action="store_true", help="gn: apply in place")
+    ap.add_argument("--nobias", action="store_true")
     ap.add_argument("--cg", type=int, default=0)
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--iters", type=int, default=3)
@@ -72,7 +73,7 @@ def main():
             stats.zero_()
             lbx.op_gemm(mode, M, n, K, x.data_ptr(), K, w.data_ptr(), K + (n if fold else 0), out.data_ptr(), n,
                         b=b, h=hw, w=hw, c=c, a2=xr.data_ptr() if fold else 0, lda2=n, k2=n if fold else 0,
-                        bias=bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
+                        bias=0 if a.nobias else bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
                         gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn,
                         gn_ss=gss.data_ptr() if gss is not None else 0)
     else:
