@@ -72,8 +72,8 @@ def ncu_dom(tag):
             "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
             "smsp__issue_active.avg.pct_of_peak_sustained_active"]
     vals = {}
-    out = [f"# ncu --set full --clock-control none of the dominant kernel (conv3x3 c128->128 + folded residual + GN "
-           f"statistics, batch 32 at 1024^2): scripts/op_bench.py conv --b 32 --hw 1024 --c 128 --fold --stats"]
+    out = [f"# ncu --set full --clock-control none of the dominant kernel (conv3x3 c128->128 + residual + GN "
+           f"statistics, batch 32 at 1024^2): scripts/op_bench.py conv --b 32 --hw 1024 --c 128 --resid --stats (residual preloaded into TMEM, as in the decoder)"]
     for i, name in enumerate(h):
         if name in want:
             vals[name] = (v[i], u[i])
@@ -91,7 +91,7 @@ def ncu_dom(tag):
     traffic = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
     tj = {"resnet.conv2+residual conv3x3 c128->128 @1024x1024": traffic,
           "_source": f"profiles/{tag}_ncu_dominant.txt: ncu --set full of scripts/op_bench.py conv --b 32 --hw 1024 "
-                     "--c 128 --fold --stats (the bench's dominant launch config); dram__bytes_read.sum + "
+                     "--c 128 --resid --stats (the bench's dominant launch config); dram__bytes_read.sum + "
                      "dram__bytes_write.sum per launch; algorithmic = 3 x 8.59 GB (input, residual, output)"}
     json.dump(tj, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
