@@ -53,6 +53,8 @@ struct KParams {
   int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
   int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
+  int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
+  int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -74,6 +76,8 @@ struct Cfg {
   static constexpr int THREADS_XF = 480;
   static constexpr uint32_t IDESC = ptx::idesc_f16(128 * CG, BN);
 };
+
+__device__ __forceinline__ int g_store_mode_dev(const KParams& p) { return p.store_mode; }
 
 __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile, int& n_tile, int& phase) {
   n_tile = t % p.n_tiles;
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       }
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
-      for (int sub = 0; sub < p.msub; ++sub) {
+      for (int sub = 0; sub < (p.epi_skip == 1 ? 0 : p.msub); ++sub) {
       const int m = tile_row0(p, m_tile, (int)rank, CG, sub) + row;
       long long orow = m;
       if (p.mode == GEMM_SUBPIX) {
@@ -596,6 +600,10 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         uint32_t r[32];
         ptx::tmem_ld32(t_row + c * 32, r);
         ptx::tmem_ld_wait();
+        if (p.epi_skip == 2) {  // diagnostics: TMEM reads only
+          if (r[0] == 0x7fc00001u && r[31] == 0x7fc00001u) p.out[0] = __float2half(0.f);  // keep the load
+          continue;
+        }
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -642,9 +650,23 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
                              *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
         }
         uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
+        if (p.epi_skip == 3) {  // diagnostics: no stores
+          if (pk[0].x == 0x7fc07fc1u && pk[3].w == 0x7fc07fc1u) op[0] = pk[0];
+        } else if (g_store_mode_dev(p) == 1) {  // two 256-bit stores (STG.256)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) op[i] = pk[i];
-        if (p.gn_stats) {  // NCH * nv <= 32 always (nv = 16 only with 128-wide tiles, NCH = 2)
+          for (int i = 0; i < 2; ++i)
+            asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(op + 2 * i), "r"(pk[2 * i].x),
+                         "r"(pk[2 * i].y), "r"(pk[2 * i].z), "r"(pk[2 * i].w), "r"(pk[2 * i + 1].x),
+                         "r"(pk[2 * i + 1].y), "r"(pk[2 * i + 1].z), "r"(pk[2 * i + 1].w)
+                         : "memory");
+        } else if (g_store_mode_dev(p) == 2) {  // streaming stores
+#pragma unroll
+          for (int i = 0; i < 4; ++i) __stcs(op + i, pk[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) op[i] = pk[i];
+        }
+        if (p.gn_stats && p.epi_skip != 4) {  // NCH * nv <= 32 always (nv = 16 only with 128-wide tiles, NCH = 2)
           if (nv == 16) {
             if constexpr (NCH <= 2) lane_group_stats<16>(v, sacc + j * 16);
           } else if (nv == 8) {
@@ -742,6 +764,10 @@ static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
 static int g_rpf_policy = 1;       // 1: preload conv residuals into the TMEM accumulator (bit 10 clears)
+static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
+static int g_store_mode = 1;       // epilogue stores (bits 16-17 = mode + 1 override): 0 STG.128,
+                                   // 1 STG.256 (default: full 32-byte sectors per lane; 3% on c128
+                                   // convs, 17% on the score GEMM), 2 streaming STG.128
 void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_halo_policy = halo_policy & 1;
   g_msub_policy = ((halo_policy >> 1) & 1) ? 0 : 1;  // bit 1 disables the two-sub-tile variant
@@ -752,6 +778,9 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : 1;
+  g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
+  g_epi_skip = ((halo_policy >> 12) & 1) ? 1 : ((halo_policy >> 13) & 1) ? 2 : ((halo_policy >> 14) & 1) ? 3
+                                                                     : ((halo_policy >> 15) & 1) ? 4 : 0;
 }
 
 template <int BN, int CG, bool XF>
@@ -898,6 +927,9 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   }
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
   // residual preload into TMEM: conv mode, unscaled outputs (the preload would be scaled too)
+  kp.epi_skip = g_epi_skip;
+  kp.store_mode = g_store_mode;
+  if (kp.store_mode == 1 && ((reinterpret_cast<uintptr_t>(a.out) & 31) || (a.ldo % 16))) kp.store_mode = 0;
   kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
