@@ -55,6 +55,7 @@ struct KParams {
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
+  int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -146,7 +147,8 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&x)[32], uint32_t 
 template <int BN, int CG, bool XF>
 __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmA2, const KParams p) {
+                   const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmO,
+                   const KParams p) {
   using C = Cfg<BN, CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -162,6 +164,8 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_xform + kMaxStages);
   // 8 epilogue warps x (BN / 2) floats, 16-byte aligned for LDS.128
   float* sBias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
+  // tstore: per epilogue warp, two 2 KB staging tiles (32 rows x 64 B, SWIZZLE_64B), 1 KB aligned
+  uint8_t* sOut = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sBias + 8 * (BN / 2)) + 1023) & ~uintptr_t(1023));
   constexpr int EPI_WARPS = 8;
 
   const uint32_t warp = ptx::warp_id();
@@ -544,6 +548,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     }
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t ochunk = 0;  // tstore: staged chunks so far (selects the staging buffer)
     for (int t = cluster_id; t < p.tiles; t += nclusters) {
       int m_tile, n_tile, ph;
       tile_coords(p, t, m_tile, n_tile, ph);
@@ -650,7 +655,20 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
                              *reinterpret_cast<uint32_t*>(&h2), *reinterpret_cast<uint32_t*>(&h3));
         }
         uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
-        if (p.epi_skip == 3) {  // diagnostics: no stores
+        if (p.tstore) {
+          // stage the warp's 32 x 32 chunk (conflict-free under the 64B swizzle) and TMA-store it:
+          // 16 smem wavefronts instead of 64 L1 wavefronts for two STG.256 with 32 distinct rows
+          uint8_t* buf = sOut + ((warp - 2) * 2 + (ochunk & 1)) * 2048;
+          if (lane == 0) ptx::bulk_wait_read<1>();  // the store that used this buffer has read it
+          __syncwarp();
+          const uint32_t base = ptx::smem_u32(buf) + lane * 64;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ptx::sts128(base + ((i ^ ((lane >> 1) & 3)) << 4), pk[i]);
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) ptx::tma_store_2d(&tmO, buf, n, (int)(orow - lane));
+          ++ochunk;
+        } else if (p.epi_skip == 3) {  // diagnostics: no stores
           if (pk[0].x == 0x7fc07fc1u && pk[3].w == 0x7fc07fc1u) op[0] = pk[0];
         } else if (g_store_mode_dev(p) == 1) {  // two 256-bit stores (STG.256)
 #pragma unroll
@@ -690,6 +708,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (p.gn_stats) flush();
+    if (p.tstore && lane == 0) ptx::bulk_wait_all();
   }
 
   ptx::tc_fence_before();
@@ -732,12 +751,12 @@ int num_sms() {
 }
 
 static bool make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-                     const cuuint32_t* box) {
+                     const cuuint32_t* box, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, rank, const_cast<void*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -765,6 +784,8 @@ static int g_fold_always = 0;      // 1: fold identity residuals into K at every
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
 static int g_rpf_policy = 1;       // 1: preload conv residuals into the TMEM accumulator (bit 10 clears)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
+static int g_tstore_policy = 0;    // TMA-store epilogue where it applies (bit 18 sets; measured equal
+                                   // to STG.256, so off: it costs 33 KB of operand stages)
 static int g_store_mode = 1;       // epilogue stores (bits 16-17 = mode + 1 override): 0 STG.128,
                                    // 1 STG.256 (default: full 32-byte sectors per lane; 3% on c128
                                    // convs, 17% on the score GEMM), 2 streaming STG.128
@@ -778,6 +799,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : 1;
+  g_tstore_policy = (halo_policy >> 18) & 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
   g_epi_skip = ((halo_policy >> 12) & 1) ? 1 : ((halo_policy >> 13) & 1) ? 2 : ((halo_policy >> 14) & 1) ? 3
                                                                      : ((halo_policy >> 15) & 1) ? 4 : 0;
@@ -786,7 +808,8 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
 template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
-  // ---- operand staging plan
+  // ---- operand staging plan (tstore: 32 KB of the budget go to the output staging tiles)
+  const int budget = kSmemBudget - (kp.tstore ? 33 * 1024 : 0);
   if (kp.halo) {
     if (kp.vsub) {  // one box of halo_rows + msub - 1 rows; sub-tile s starts 130 s rows in
       kp.halo_sub_bytes = 130 * 128;
@@ -799,18 +822,18 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     }
     // policy 1: a halo stage feeds >= 36 MMAs, so two are enough and the rest of the budget goes to
     // B; policy 0 (default): three A stages when the B tile is small and there is one sub-tile
-    if (g_stage_policy) kp.a_stages = 2;
+    if (g_stage_policy || (kp.tstore && Cf::B_BYTES >= 16384)) kp.a_stages = 2;
     else kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
-    kp.b_stages = (kSmemBudget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
+    kp.b_stages = (budget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
   } else {
     kp.a_tx_bytes = kp.a_stage_bytes = 128 * 64 * 2;
-    kp.a_stages = kp.b_stages = kSmemBudget / (kp.a_stage_bytes + Cf::B_BYTES);
+    kp.a_stages = kp.b_stages = budget / (kp.a_stage_bytes + Cf::B_BYTES);
   }
   if (kp.a_stages > kMaxStages) kp.a_stages = kMaxStages;
   if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
   if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
   const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16 +
-                   16 + 8 * (BN / 2) * 4;
+                   16 + 8 * (BN / 2) * 4 + (kp.tstore ? 1024 + 8 * 2 * 2048 : 0);
   if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
 
   CUtensorMap tmA, tmB;
@@ -834,6 +857,13 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     if (!make_map(&tmA2, a.A2, 2, dims, strides, box)) return cudaErrorInvalidValue;
   } else {
     tmA2 = tmA;
+  }
+  CUtensorMap tmO = tmA;
+  if (kp.tstore) {  // output [M][N] (row stride ldo): boxes of 32 columns x 32 rows, 64B swizzle
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.M};
+    cuuint64_t strides[1] = {(cuuint64_t)a.ldo * 2};
+    cuuint32_t box[2] = {32, 32};
+    if (!make_map(&tmO, a.out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
   }
   if (kp.b_mn) {  // B stored [K][N] (row stride ldb): boxes of 64 N x 64 K
     cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.K};
@@ -863,7 +893,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA2, kp);
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA2, tmO, kp);
 }
 
 template <int BN, int CG>
@@ -930,6 +960,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.epi_skip = g_epi_skip;
   kp.store_mode = g_store_mode;
   if (kp.store_mode == 1 && ((reinterpret_cast<uintptr_t>(a.out) & 31) || (a.ldo % 16))) kp.store_mode = 0;
+  // TMA-store epilogue: rows of a warp's chunk are contiguous output rows (not the sub-pixel
+  // phases), 16-byte aligned rows, no XF transform warps
+  kp.tstore = (g_tstore_policy && a.mode != GEMM_SUBPIX && !a.gn_ss && !(reinterpret_cast<uintptr_t>(a.out) & 15) &&
+               a.ldo % 8 == 0) ? 1 : 0;
   kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;

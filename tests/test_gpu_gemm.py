@@ -75,6 +75,37 @@ def test_gemm_mn_major_b(lbx, cg, bn, M, N, K, ldb):
     _close(out, rs[:, None] * (A.float() @ B.float()))
 
 
+@pytest.mark.parametrize("bits", [1 | (1 << 18), 1 | (1 << 16), 1 | (3 << 16)])
+def test_epilogue_store_variants(lbx, bits):
+    """The TMA-store epilogue (bit 18) and the STG.128 / streaming store modes give the same
+    results as the default (STG.256): conv with residual + statistics and a plain GEMM."""
+    b, h, w, c = 2, 16, 256, 128
+    x = _rand(b, h, w, c, seed=71)
+    wt = _rand(c, c, 3, 3, scale=(9 * c) ** -0.5, seed=72)
+    wk = wt.permute(0, 2, 3, 1).contiguous()
+    resid = _rand(b, h, w, c, seed=73)
+    bias = torch.randn(c, device="cuda")
+    outs = []
+    try:
+        for bb in (1, bits):
+            lbx.check(lbx.lib().lbx_op_set_debug(bb, 0))
+            out = torch.empty(b, h, w, c, dtype=torch.half, device="cuda")
+            stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+            lbx.op_gemm(1, b * h * w, c, 9 * c, x.data_ptr(), 0, wk.data_ptr(), 9 * c, out.data_ptr(), c, b=b, h=h,
+                        w=w, c=c, bias=bias.data_ptr(), resid=resid.data_ptr(), ldr=c, gn_stats=stats.data_ptr())
+            A = _rand(512, 512, seed=74)
+            B = _rand(1024, 512, scale=512 ** -0.5, seed=75)
+            g = torch.empty(512, 1024, dtype=torch.half, device="cuda")
+            lbx.op_gemm(0, 512, 1024, 512, A.data_ptr(), 512, B.data_ptr(), 512, g.data_ptr(), 1024, alpha=0.5)
+            torch.cuda.synchronize()
+            outs.append((out.clone(), g.clone(), stats.clone()))
+    finally:
+        lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    _close(outs[1][0], _conv_ref(x, wt, bias) + resid.float())
+    _check_gn_stats(outs[1][2], outs[1][0], b, h * w, c)
+
+
 def test_gemm_strided_views(lbx):
     """Q K^T on column views of a [L, 1536] QKV buffer (row stride 1536), as the attention uses."""
     L = 512
