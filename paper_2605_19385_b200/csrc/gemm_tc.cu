@@ -56,6 +56,7 @@ struct KParams {
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
+  int cmap;            // epilogue column chunks per warp: 1 contiguous (hsel*NCH + j), 0 interleaved
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -472,6 +473,9 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     const int hsel = (int)(warp - 2) >> 2;
     const int row = q * 32 + lane;
     constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
+    // 32-column chunk j of this warp: contiguous (the warp owns whole 128-byte row segments, so a
+    // lane's consecutive stores complete a cache line) or interleaved with the other column half
+    const int cbase = p.cmap ? hsel * NCH : hsel, cstep = p.cmap ? 1 : (EPI_WARPS / 4);
     // GroupNorm partials: each lane accumulates its own per-chunk (group sum, group sumsq) values in
     // fp32 registers across tiles (NCH x NV <= 32 of them); at a flush -- when the (image, n-tile)
     // changes -- the warp reduce-scatters them (lane L owns value L) and adds them with one fp64
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         const int j = (int)lane / nv, i = (int)lane - j * nv;
         const int gpc = nv >> 1;  // groups per chunk
         const int kind = i >= gpc;
-        const int c = hsel + (EPI_WARPS / 4) * j;
+        const int c = cbase + cstep * j;
         const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + (i - kind * gpc);
         atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, (double)tot);
       }
@@ -512,13 +516,13 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         tile_coords(p, tn, mt, nt, phn);
         for (int sub = 0; sub < p.msub; ++sub) {
           const long long mrow = tile_row0(p, mt, (int)rank, CG, sub) + row;
-          const __half* rb = p.resid + mrow * p.ldr + nt * BN + hsel * 32;
+          const __half* rb = p.resid + mrow * p.ldr + nt * BN + cbase * 32;
           const uint32_t tb = tmem_base + ((q * 32u) << 16) + buf * (p.msub * BN) + sub * BN;
 #pragma unroll
           for (int j = 0; j < NCH; ++j) {
             uint4 u[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(rb + j * 32 * (EPI_WARPS / 4)) + i);
+            for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(rb + j * 32 * cstep) + i);
             uint32_t r[32];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
                 r[i * 8 + 2 * k + 1] = __float_as_uint(f.y);
               }
             }
-            ptx::tmem_st32(tb + (hsel + (EPI_WARPS / 4) * j) * 32, r);
+            ptx::tmem_st32(tb + (cbase + cstep * j) * 32, r);
           }
         }
         ptx::tmem_st_wait();
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
 #pragma unroll
         for (int j = 0; j < NCH; ++j)
           asm volatile("st.shared.f32 [%0], %1;" ::"r"(wbias + (j * 32 + lane) * 4),
-                       "f"(p.bias[n0 + (hsel + (EPI_WARPS / 4) * j) * 32 + lane])
+                       "f"(p.bias[n0 + (cbase + cstep * j) * 32 + lane])
                        : "memory");
         __syncwarp();
         bias_ntile = n_tile;
@@ -589,8 +593,8 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       constexpr int PF = NCH < 2 ? NCH : 2;
       uint4 rr[PF][4];
       const bool eresid = p.resid && !p.rpf;  // residual added here (not preloaded into TMEM)
-      const __half* rbase = eresid ? p.resid + orow * p.ldr + n0 + hsel * 32 : nullptr;
-      constexpr int RSTRIDE = 32 * (EPI_WARPS / 4);  // columns between this warp's chunks
+      const __half* rbase = eresid ? p.resid + orow * p.ldr + n0 + cbase * 32 : nullptr;
+      const int RSTRIDE = 32 * cstep;  // columns between this warp's chunks
       if (eresid) {
 #pragma unroll
         for (int j = 0; j < PF; ++j)
@@ -600,7 +604,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * (p.msub * BN) + sub * BN;
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        const int c = hsel + (EPI_WARPS / 4) * j;
+        const int c = cbase + cstep * j;
         const int n = n0 + c * 32;
         uint32_t r[32];
         ptx::tmem_ld32(t_row + c * 32, r);
@@ -784,6 +788,7 @@ static int g_fold_always = 0;      // 1: fold identity residuals into K at every
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
 static int g_rpf_policy = 1;       // 1: preload conv residuals into the TMEM accumulator (bit 10 clears)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
+static int g_cmap_policy = 1;      // 1: contiguous epilogue column chunks per warp (bit 19 clears)
 static int g_tstore_policy = 0;    // TMA-store epilogue where it applies (bit 18 sets; measured equal
                                    // to STG.256, so off: it costs 33 KB of operand stages)
 static int g_store_mode = 1;       // epilogue stores (bits 16-17 = mode + 1 override): 0 STG.128,
@@ -800,6 +805,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
+  g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
   g_epi_skip = ((halo_policy >> 12) & 1) ? 1 : ((halo_policy >> 13) & 1) ? 2 : ((halo_policy >> 14) & 1) ? 3
                                                                      : ((halo_policy >> 15) & 1) ? 4 : 0;
@@ -959,6 +965,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   // residual preload into TMEM: conv mode, unscaled outputs (the preload would be scaled too)
   kp.epi_skip = g_epi_skip;
   kp.store_mode = g_store_mode;
+  kp.cmap = g_cmap_policy;
   if (kp.store_mode == 1 && ((reinterpret_cast<uintptr_t>(a.out) & 31) || (a.ldo % 16))) kp.store_mode = 0;
   // TMA-store epilogue: rows of a warp's chunk are contiguous output rows (not the sub-pixel
   // phases), 16-byte aligned rows, no XF transform warps
