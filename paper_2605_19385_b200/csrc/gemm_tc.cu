@@ -1,16 +1,22 @@
 // tcgen05 implicit-GEMM for the VAE decoder's dense contractions:
-//   conv3x3 (pad 1, NHWC), conv1x1 / linear (plain GEMM), and nearest-2x upsample fused with the
-//   following conv3x3 as four 2x2 sub-pixel convolutions (GEMM_SUBPIX; 4/9 of the FLOPs).
+//   conv3x3 (pad 1, NHWC), conv1x1 / linear (plain GEMM, B K-major or MN-major), and nearest-2x
+//   upsample fused with the following conv3x3 as four 2x2 sub-pixel convolutions (GEMM_SUBPIX; 4/9
+//   of the FLOPs).
 //
-// Structure (persistent, warp-specialised, one CTA or one CTA pair per tile):
-//   warp 0      TMA producer: A tile (128 pixels x 64 channels, tap-shifted box; TMA OOB zero-fill
-//               provides the conv halo) + B tile (weights) into a STAGES-deep smem ring.
-//   warp 1      TMEM allocator; in the leader CTA one elected lane issues tcgen05.mma
-//               (M = 128*CG, N = BN, K = 16 per instruction) into a double-buffered TMEM accumulator.
-//   warps 2..5  epilogue: tcgen05.ld -> alpha/row-scale/bias/residual in fp32 -> fp16 store, plus
-//               GroupNorm-32 partial sums of the stored values (fp64 atomics) for the next norm.
-// CG = 2 runs the tile on a CTA pair (cta_group::2): each CTA stages half of A (its 128 rows) and
-// half of B (BN/2 rows); the leader's MMA reads both halves, halving smem operand traffic per SM.
+// Structure (persistent, warp-specialised, one CTA or one CTA pair per tile; DESIGN.md 4):
+//   warp 0      A producer (TMA): one halo box per 64-channel block that every tap reads through a
+//               row-shifted UMMA descriptor (TMA OOB zero-fill is the conv padding); plain 2-D boxes
+//               in GEMM mode; the extra K segment (a folded 1x1 shortcut) from a second map.
+//   warp 10     B producer (TMA): weight k-blocks into their own ring.
+//   warp 1      TMEM allocator; in the leader CTA ONE thread issues every tcgen05.mma
+//               (M = 128*CG, N = BN, K = 16) into a double-buffered TMEM accumulator.
+//   warps 2..9  epilogue, two warps per TMEM lane quarter: tcgen05.ld -> (scale) + bias (+ residual)
+//               in fp32 -> fp16 STG.256, GroupNorm-32 partial sums of the fp32 values (per lane,
+//               reduced at image changes, fp64 atomics), and the residual preload of the tile that
+//               will reuse the buffer (tcgen05.st).
+//   warps 11..14  (XF kernels only) GroupNorm + SiLU transform of each landed A halo.
+// CG = 2 runs the tile on a CTA pair (cta_group::2): each CTA stages its 128 A rows and half of B
+// (BN/2 rows); the leader's MMA reads both halves.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
