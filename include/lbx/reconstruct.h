@@ -103,6 +103,14 @@ lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, u
 lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, uint32_t w, uint8_t* out,
                     size_t cap, size_t* out_bytes);
 
+/* Device-side write path: LBLP mode-1 (lossless) pack of n fp16 NCHW latents already on the GPU
+ * (latents_dev, c x h x w each, w % 32 == 0).  Blob i is written at out_dev + i * stride (stride >=
+ * lbx_pack_bound(c, h, w), multiple of 4) and its size to sizes_dev[i] (uint32, device).  The bytes
+ * equal lbx_pack(..., mode 1, ...).  Asynchronous on `stream` (NULL = default stream). */
+size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w);
+lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint32_t h, uint32_t w, uint8_t* out_dev,
+                           size_t stride, uint32_t* sizes_dev, lbx_stream stream);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* lbx_last_error(void);
 

@@ -925,6 +925,33 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   return LBX_OK;
 }
 
+size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w) {
+  if (c == 0 || h == 0 || w == 0 || w % 32) return 0;
+  return lbx::lblp_pack_bound((int)c, (int)h, (int)w);
+}
+
+lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint32_t h, uint32_t w, uint8_t* out_dev,
+                           size_t stride, uint32_t* sizes_dev, lbx_stream stream) {
+  if (n == 0) return LBX_OK;
+  if (!latents_dev || !out_dev || !sizes_dev) return set_err(LBX_E_CONFIG, "lbx_pack_device: null pointer");
+  if (c == 0 || h == 0 || w == 0 || w % 32 || c > 65535 || h > 65535 || w > 65535)
+    return set_err(LBX_E_CONFIG, "lbx_pack_device: shape must be nonzero, <= 65535, w % 32 == 0");
+  if (stride < lbx::lblp_pack_bound((int)c, (int)h, (int)w) || stride % 4)
+    return set_err(LBX_E_CONFIG, "lbx_pack_device: stride must be >= lbx_pack_bound and a multiple of 4");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t rows = (size_t)n * c * h;
+  uint8_t* tmp = nullptr;
+  const size_t wbytes = (rows * (w / 32) + 15) & ~size_t(15);
+  if (cudaMallocAsync(reinterpret_cast<void**>(&tmp), wbytes + rows * 4, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "lbx_pack_device: cudaMallocAsync");
+  cudaError_t e = lbx::launch_lblp_pack(reinterpret_cast<const uint16_t*>(latents_dev), (int)n, (int)c, (int)h, (int)w,
+                                        out_dev, (long long)stride, sizes_dev, tmp,
+                                        reinterpret_cast<uint32_t*>(tmp + wbytes), s);
+  cudaFreeAsync(tmp, s);
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("lbx_pack_device: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
 lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
                            int H, int W, int impl, lbx_stream stream) {
   if (!x || !ss || !w || !b || !rgb || n <= 0 || H <= 0 || W <= 0)

@@ -61,4 +61,11 @@ void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaS
 void launch_lblp_unpack(const uint8_t* blobs, const unsigned long long* offs, const unsigned int* sizes, int n,
                         int C, int H, int W, __half* out, int* err, cudaStream_t s);
 
+// LBLP mode-1 pack of n device latents (fp16 NCHW [n][C][H][W], W % 32 == 0) into out + i*stride
+// (stride >= lblp_pack_bound, multiple of 4); sizes[i] = blob bytes.  Temporaries: widths_tmp
+// [n*C*H*W/32] bytes, row_bytes_tmp [n*C*H] uint32.  Byte-identical to the host packer.
+size_t lblp_pack_bound(int C, int H, int W);
+cudaError_t launch_lblp_pack(const uint16_t* x, int n, int C, int H, int W, uint8_t* out, long long stride,
+                             uint32_t* sizes, uint8_t* widths_tmp, uint32_t* row_bytes_tmp, cudaStream_t s);
+
 }  // namespace lbx

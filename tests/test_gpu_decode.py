@@ -120,3 +120,38 @@ def test_config_errors(lbx):
     with pytest.raises(lbx.LbxError) as e:
         dec.reconstruct_latents(z)  # n > max_batch
     assert e.value.status == lbx.E_CONFIG
+
+
+def test_flux_family_vs_oracle(lbx):
+    """FLUX-family constants (16 channels, scaling 0.3611, shift 0.1159) through the same decoder."""
+    import vae_ref
+    import weights_ref
+    z = weights_ref.make_latents("flux", 1, 64, 64, seed=21)
+    ref = vae_ref.decode(z, weights_ref.make_weights("flux", 0), "flux")
+    got = lbx.Decoder("flux", (64, 64), seed=0, max_batch=1).reconstruct_latents(z)
+    _check(_stats(got, ref), "flux 64x64->512^2")
+
+
+def test_explicit_weight_blob_equals_seed(lbx):
+    """desc.weights (an fp32 blob in canonical order) decodes bit-identically to the same
+    parameters generated from the seed inside the library; a wrong count is LBX_E_CONFIG."""
+    import weights_ref
+    params = lbx.generate_params("sd15", 3)
+    z = weights_ref.make_latents("sd15", 1, 64, 64, seed=4)
+    a = lbx.Decoder("sd15", (64, 64), seed=3, max_batch=1).reconstruct_latents(z)
+    b = lbx.Decoder("sd15", (64, 64), weights=params, max_batch=1).reconstruct_latents(z)
+    assert np.array_equal(a, b)
+    with pytest.raises(lbx.LbxError) as e:
+        lbx.Decoder("sd15", (64, 64), weights=params[:-1], max_batch=1)
+    assert e.value.status == lbx.E_CONFIG
+
+
+def test_max_batch_and_partial_batches(lbx):
+    """A decoder sized for 5 images decodes 1..5 of them; every image equals its solo decode."""
+    import weights_ref
+    z = weights_ref.make_latents("sd15", 5, 64, 64, seed=17)
+    dec = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=5)
+    full = dec.reconstruct_latents(z)
+    for n in (1, 2, 4):
+        part = dec.reconstruct_latents(z[:n])
+        assert np.array_equal(part, full[:n]), n
