@@ -3,7 +3,8 @@
 
 Workload (BASELINE.json configs[1], the config the metric is quoted on at N=1):
   config2: SD1.5-family decoder, 4x128x128 fp16 latents -> 1024x1024 uint8 RGB, batch 32 per GPU.
-  --config 4 selects configs[3] instead (16x128x128 SD3-family latents, batch 64 per GPU).
+  --config 4 selects configs[3] instead (16x128x128 SD3-family latents, batch 64 per GPU);
+  --config 3 is configs[2]: the same shape with the e2e leg fed quantized (LBLP q8) blobs.
 A step = one batched reconstruction of `batch` latents.  N>1 (torchrun, one rank per GPU): whole
 requests are sharded across GPUs (weak scaling: fixed batch per GPU), no data-path collective;
 timing is barrier + CUDA events, max over ranks.
@@ -43,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, choices=[2, 4], default=2)
+    ap.add_argument("--config", type=int, choices=[2, 3, 4], default=2)
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -55,6 +56,10 @@ def workload(args):
     if args.config == 2:
         fam, c, batch = "sd15", 4, 32
         name = "config2: sd15-family decoder, 4x128x128 fp16 latents -> 1024x1024 uint8 RGB"
+    elif args.config == 3:
+        fam, c, batch = "sd3", 16, 64
+        name = ("config3: compressed-latent path, sd3-family 16x128x128 latents stored as LBLP q8 "
+                "(quantized) blobs -> GPU unpack + decode -> 1024x1024 uint8 RGB")
     else:
         fam, c, batch = "sd3", 16, 64
         name = "config4: sd3-family decoder, 16x128x128 fp16 latents -> 1024x1024 uint8 RGB"
@@ -235,7 +240,8 @@ def main():
     # ---------------------------------------------------------------- end to end (host buffers)
     e2e = None
     if not args.no_e2e:
-        blobs = [lbx.pack(lat_np[i], 1) for i in range(batch)]  # LBLP lossless blobs in host memory
+        mode = 2 if args.config == 3 else 1  # config 3: quantized (q8) blobs; else lossless
+        blobs = [lbx.pack(lat_np[i], mode) for i in range(batch)]  # LBLP blobs in host memory
         out = torch.empty((batch, 1024, 1024, 3), dtype=torch.uint8, pin_memory=True).numpy()
         for _ in range(max(1, args.warmup)):
             dec.reconstruct(blobs, out, stream=sp)
@@ -250,7 +256,7 @@ def main():
         e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
         e2e = {"value": world * batch * args.steps / (e2e_ms / 1e3), "unit": "img/s",
                "h2d_bytes_per_step": int(sum(len(b) for b in blobs) + 12 * batch),
-               "d2h_bytes_per_step": int(out.nbytes), "path": "lbx_reconstruct: LBLP mode-1 blobs (host) -> "
+               "d2h_bytes_per_step": int(out.nbytes), "path": f"lbx_reconstruct: LBLP mode-{mode} blobs (host) -> "
                "H2D -> GPU unpack -> decode graph -> RGB D2H (pinned)"}
 
     # ---------------------------------------------------------------- per-launch profile / roofline

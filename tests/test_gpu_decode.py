@@ -155,3 +155,13 @@ def test_max_batch_and_partial_batches(lbx):
     for n in (1, 2, 4):
         part = dec.reconstruct_latents(z[:n])
         assert np.array_equal(part, full[:n]), n
+
+
+def test_config2_shape_sd15_1024_vs_oracle(lbx):
+    """The benchmarked shape itself (config 2: sd15 4x128x128 -> 1024^2), one image, live fp32 oracle."""
+    import vae_ref
+    import weights_ref
+    z = weights_ref.make_latents("sd15", 1, 128, 128, seed=2)
+    ref = vae_ref.decode(z, weights_ref.make_weights("sd15", 0), "sd15")
+    got = lbx.Decoder("sd15", (128, 128), seed=0, max_batch=1).reconstruct_latents(z)
+    _check(_stats(got, ref), "config2 sd15 128x128->1024^2")
