@@ -186,6 +186,9 @@ lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
  * tensor cores (fp32 SiLU), 2 = tensor cores with packed-half SiLU, 1 = CUDA cores (fp32). */
 lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
                            int H, int W, int impl, lbx_stream stream);
+/* Mid-block attention core without the L x L scores (csrc/attn_fa.cu): out [n][L][512] =
+ * softmax(Q K^T / sqrt(512)) V, Q/K/V = column blocks 0/512/1024 of qkv [n][L][1536] fp16; L % 128 == 0. */
+lbx_status lbx_op_attention(const void* qkv, void* out, int n, int L, lbx_stream stream);
 /* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
 lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
 /* GroupNorm finalize + apply; silu 0 = identity, 1 = fp32 SiLU, 2 = packed-half SiLU; y may alias x. */

@@ -28,7 +28,7 @@ SYMBOLS = [
     "lbx_param_count", "lbx_generate_params", "lbx_decoder_create", "lbx_decoder_destroy", "lbx_unpack", "lbx_decode",
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
-    "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device",
+    "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
 ]
 
 
@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_op_set_debug.argtypes = [i32, i32]
     L.lbx_op_gemm_desc.argtypes = [ctypes.POINTER(GemmDesc), vp]
     L.lbx_op_conv_out.argtypes = [vp, vp, vp, vp, vp, i32, i32, i32, i32, vp]
+    L.lbx_op_attention.argtypes = [vp, vp, i32, i32, vp]
     L.lbx_pack_bound.argtypes = [u32, u32, u32]
     L.lbx_pack_bound.restype = ctypes.c_size_t
     L.lbx_pack_device.argtypes = [vp, u32, u32, u32, u32, vp, ctypes.c_size_t, vp, vp]
@@ -261,6 +262,11 @@ def op_groupnorm(x, y, stats, gamma, beta, b, hw, c, silu=True, eps=1e-6, stream
 def op_conv_out(x, ss, w, b, rgb, n, h, w_, impl=0, stream=0):
     """Decoder tail (lbx_op_conv_out): impl 0 tensor cores, 2 tensor cores + packed-half SiLU, 1 CUDA cores."""
     check(lib().lbx_op_conv_out(x, ss, w, b, rgb, n, h, w_, impl, stream or None))
+
+
+def op_attention(qkv, out, n, L, stream=0):
+    """Flash-style attention core (lbx_op_attention): out = softmax(Q K^T / sqrt(512)) V."""
+    check(lib().lbx_op_attention(qkv, out, n, L, stream or None))
 
 
 def pack_bound(c: int, h: int, w: int) -> int:

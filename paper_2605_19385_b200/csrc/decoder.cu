@@ -925,6 +925,16 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   return LBX_OK;
 }
 
+lbx_status lbx_op_attention(const void* qkv, void* out, int n, int L, lbx_stream stream) {
+  if (!qkv || !out || n <= 0 || L <= 0 || L % 128) return set_err(LBX_E_CONFIG, "lbx_op_attention: bad argument");
+  cudaError_t e = lbx::launch_attn_fa(reinterpret_cast<const __half*>(qkv), reinterpret_cast<__half*>(out), n, L,
+                                      reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess)
+    return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
+                   std::string("lbx_op_attention: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
 size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w) {
   if (c == 0 || h == 0 || w == 0 || w % 32) return 0;
   return lbx::lblp_pack_bound((int)c, (int)h, (int)w);

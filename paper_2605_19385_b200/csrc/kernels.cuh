@@ -61,6 +61,10 @@ void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaS
 void launch_lblp_unpack(const uint8_t* blobs, const unsigned long long* offs, const unsigned int* sizes, int n,
                         int C, int H, int W, __half* out, int* err, cudaStream_t s);
 
+// Mid-block attention without the L x L scores (csrc/attn_fa.cu): out[n][L][512] =
+// softmax(Q K^T / sqrt(512)) V with Q, K, V the column blocks of qkv [n][L][1536]; L % 128 == 0.
+cudaError_t launch_attn_fa(const __half* qkv, __half* out, int n, int L, cudaStream_t s);
+
 // LBLP mode-1 pack of n device latents (fp16 NCHW [n][C][H][W], W % 32 == 0) into out + i*stride
 // (stride >= lblp_pack_bound, multiple of 4); sizes[i] = blob bytes.  Temporaries: widths_tmp
 // [n*C*H*W/32] bytes, row_bytes_tmp [n*C*H] uint32.  Byte-identical to the host packer.

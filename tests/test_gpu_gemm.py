@@ -289,3 +289,16 @@ def test_conv_out_tail(lbx, impl, n, H, W):
     print(f"\n[conv_out impl {impl} {n}x{H}x{W}] max|d|={d.max().item()} exact={exact:.4f}")
     assert d.max().item() <= 1
     assert exact >= (0.95 if impl == 2 else 0.97)
+
+
+@pytest.mark.parametrize("n,L,scale", [(1, 256, 1.0), (2, 512, 1.0), (1, 2048, 2.0), (2, 4096, 0.7)])
+def test_flash_attention_core(lbx, n, L, scale):
+    """CTA-pair flash attention (d split across the pair, partial scores and P exchanged through
+    DSMEM) against torch fp32 softmax(Q K^T / sqrt(512)) V on the same fp16 QKV buffer."""
+    qkv = _rand(n, L, 1536, scale=scale, seed=81)
+    out = torch.empty(n, L, 512, dtype=torch.half, device="cuda")
+    lbx.op_attention(qkv.data_ptr(), out.data_ptr(), n, L)
+    torch.cuda.synchronize()
+    q, k, v = qkv[..., :512].float(), qkv[..., 512:1024].float(), qkv[..., 1024:].float()
+    ref = torch.softmax(q @ k.transpose(1, 2) / 512 ** 0.5, dim=-1) @ v
+    _close(out, ref, rel=4e-3, abs_=2e-3)
