@@ -96,6 +96,7 @@ class Decoder {
   uint8_t* rgb = nullptr;
   int* err = nullptr;
   static constexpr int kMaxSites = 64;
+  int s_imgs = 1;                 // images whose attention scores fit the S buffer at once
 
   // blob staging
   uint8_t* blob_dev = nullptr;
@@ -323,7 +324,8 @@ lbx_status Decoder::alloc_arena() {
   const size_t nb = (size_t)max_batch;
   const size_t x_el = nb * hw * 64 * 256;  // max residual-stream tensor: 8h x 8w x 256
   const size_t h_el = nb * hw * 64 * 128;  // max conv1 output: 8h x 8w x 128 (>= QKV hw x 1536)
-  const size_t s_el = hw * hw;             // one image's attention scores
+  s_imgs = std::max(1, std::min(max_batch, 8));  // attention scores of up to 8 images at once
+  const size_t s_el = hw * hw * (size_t)s_imgs;
   const size_t vt_el = 512 * hw;
   size_t off = 0;
   auto slot = [&](size_t bytes) {
@@ -332,7 +334,7 @@ lbx_status Decoder::alloc_arena() {
     return o;
   };
   const size_t oX = slot(x_el * 2), oA = slot(x_el * 2), oH = slot(h_el * 2), oS = slot(s_el * 2),
-               oVt = slot(vt_el * 2), oR = slot(hw * 4), oSt = slot((size_t)kMaxSites * nb * 64 * 8),
+               oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oSt = slot((size_t)kMaxSites * nb * 64 * 8),
                oSs = slot(nb * 512 * 8), oLat = slot(nb * cl * hw * 2), oRgb = slot(nb * hw * 64 * 3),
                oErr = slot(64);
   LBX_CUDA_TRY(cudaMalloc(&arena, off));
@@ -553,28 +555,34 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     g.A = A_; g.lda = 512; g.Bw = wqkv; g.ldb = 512;
     g.out = Hb; g.ldo = 1536; g.bias = bqkv;
     if ((st = gemm(g, "attn.qkv")) != LBX_OK) return st;
-    for (int i = 0; i < n; ++i) {
-      const __half* base = Hb + (size_t)i * L * 1536;
+    // groups of up to s_imgs images: one scores GEMM, one softmax and one P.V launch per group
+    // (batched plain GEMMs; the P.V of a single image is only 128 pair-tiles, < 2 waves)
+    const int gsz = v_transpose_legacy() ? 1 : s_imgs;
+    for (int i0 = 0; i0 < n; i0 += gsz) {
+      const int g = std::min(gsz, n - i0);
+      const __half* base = Hb + (size_t)i0 * L * 1536;
       GemmArgs sq;
       sq.mode = GEMM_PLAIN;
-      sq.M = L; sq.N = L; sq.K = 512;
+      sq.M = g * L; sq.N = L; sq.K = 512;
       sq.A = base; sq.lda = 1536;
       sq.Bw = base + 512; sq.ldb = 1536;
       sq.out = S; sq.ldo = L;
       sq.alpha = 1.0f / std::sqrt(512.0f);
+      if (g > 1) { sq.batch_m = L; sq.batch_b = L; sq.b_rows_total = g * L; }
       if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
-      LBX_LAUNCH(launch_softmax_rows(S, rowscale, L, L, s), "attn.softmax", 4.0 * L * (double)L);
+      LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s), "attn.softmax", 4.0 * g * L * (double)L);
       GemmArgs pv;
       pv.mode = GEMM_PLAIN;
-      pv.M = L; pv.N = 512; pv.K = L;
+      pv.M = g * L; pv.N = 512; pv.K = L;
       pv.A = S; pv.lda = L;
       if (v_transpose_legacy()) {
         LBX_LAUNCH(launch_transpose(base + 1024, 1536, Vt, L, L, 512, s), "attn.v_transpose", 4.0 * L * 512.0);
         pv.Bw = Vt; pv.ldb = L;
       } else {  // V read in place from the QKV buffer as an MN-major B operand (no transpose)
         pv.Bw = base + 1024; pv.ldb = 1536; pv.b_mn_major = 1;
+        if (g > 1) { pv.batch_m = L; pv.batch_b = L; pv.b_rows_total = g * L; }
       }
-      pv.out = A_ + (size_t)i * L * 512; pv.ldo = 512;
+      pv.out = A_ + (size_t)i0 * L * 512; pv.ldo = 512;
       pv.row_scale = rowscale;
       if ((st = gemm(pv, "attn.pv")) != LBX_OK) return st;
     }

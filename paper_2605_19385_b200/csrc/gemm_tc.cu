@@ -63,6 +63,7 @@ struct KParams {
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
   int cmap;            // epilogue column chunks per warp: 1 contiguous (hsel*NCH + j), 0 interleaved
+  int batch_m, batch_b;  // batched plain GEMM: rows per image of A, B offset per image
   int halo_sub_bytes;  // smem pitch of one sub-tile's halo box (1024-aligned)
   int tmem_cols;       // 2 accumulator buffers x msub x BN (power of two <= 512)
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
@@ -290,7 +291,10 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       for (int t = cluster_id; t < p.tiles; t += nclusters) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
-        const int b_row = (p.mode == GEMM_SUBPIX ? phs * p.N : 0) + n_tile * BN + rank * C::B_ROWS;
+        const int bimg = p.batch_m ? (m_tile * 128 * p.msub * CG) / p.batch_m : 0;  // batched: image of the tile
+        const int b_row = (p.mode == GEMM_SUBPIX ? phs * p.N : 0) + n_tile * BN + rank * C::B_ROWS +
+                          (p.b_mn ? 0 : bimg * p.batch_b);
+        const int k_img = p.b_mn ? bimg * p.batch_b : 0;
         for (int j = 0; j < n_a; ++j) {
           for (int tp = 0; tp < per_a; ++tp) {
             ptx::mbar_wait(&b_empty[st], ph ^ 1);
@@ -299,8 +303,8 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
             uint8_t* dst = sB + st * C::B_BYTES;
             if (p.b_mn) {  // B_ROWS / 64 boxes of (64 N) x (64 K), one per 64-wide N atom
               for (int na = 0; na < C::B_ROWS / 64; ++na) {
-                if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0);
-                else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0);
+                if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0 + k_img);
+                else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst + na * 8192, b_row + na * 64, k0 + k_img);
               }
             } else if constexpr (CG == 1) {
               ptx::tma_load_2d(&tmB, &b_full[st], dst, k0, b_row);
@@ -878,12 +882,12 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     if (!make_map(&tmO, a.out, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
   }
   if (kp.b_mn) {  // B stored [K][N] (row stride ldb): boxes of 64 N x 64 K
-    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)a.K};
+    cuuint64_t dims[2] = {(cuuint64_t)a.N, (cuuint64_t)(a.b_rows_total ? a.b_rows_total : a.K)};
     cuuint64_t strides[1] = {(cuuint64_t)a.ldb * 2};
     cuuint32_t box[2] = {64, 64};
     if (!make_map(&tmB, a.Bw, 2, dims, strides, box)) return cudaErrorInvalidValue;
   } else {
-    const int brows = a.mode == GEMM_SUBPIX ? 4 * a.N : a.N;
+    const int brows = a.mode == GEMM_SUBPIX ? 4 * a.N : (a.b_rows_total ? a.b_rows_total : a.N);
     cuuint64_t dims[2] = {(cuuint64_t)(a.K + a.K2), (cuuint64_t)brows};
     cuuint64_t strides[1] = {(cuuint64_t)a.ldb * 2};
     cuuint32_t box[2] = {64, (cuuint32_t)Cf::B_ROWS};
@@ -962,6 +966,12 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
     kp.halo_rows = a.mode == GEMM_CONV3X3 ? 3 : 2;
     kp.halo = (g_halo_policy && kp.Ht == 1) ? 1 : 0;  // a tap's 128 rows must be contiguous in the halo
     kp.desc_base_mode = g_desc_base_mode;
+  }
+  if (a.batch_m) {  // batched plain GEMM: tiles never straddle images
+    if (a.mode != GEMM_PLAIN || a.K2 || a.batch_m % 256 || a.M % a.batch_m || a.b_rows_total <= 0)
+      return cudaErrorInvalidValue;
+    kp.batch_m = a.batch_m;
+    kp.batch_b = a.batch_b;
   }
   if (a.b_mn_major) {  // plain GEMM only, no extra K segment
     if (a.mode != GEMM_PLAIN || a.K2 || a.N % 64) return cudaErrorInvalidValue;

@@ -35,6 +35,10 @@ struct GemmArgs {
   const __half* Bw = nullptr;
   int ldb = 0;
   int b_mn_major = 0;
+  // batched plain GEMM over images: A / out rows of image i are [i*batch_m, (i+1)*batch_m) and
+  // image i's B starts batch_b rows (K-major: N rows; MN-major: K rows) further; b_rows_total is
+  // then the extent of B's row dimension (e.g. attention scores / P.V of a group of images)
+  int batch_m = 0, batch_b = 0, b_rows_total = 0;
   // epilogue
   __half* out = nullptr;
   int ldo = 0;
