@@ -796,7 +796,9 @@ static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to 
 static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
-static int g_rpf_policy = 1;       // 1: preload conv residuals into the TMEM accumulator (bit 10 clears)
+static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
+                                   // outputs (default; 256-wide: the epilogue read measured 10% faster
+                                   // on c256), 0 never (bit 10), 2 at every width (bit 20)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
 static int g_cmap_policy = 1;      // 1: contiguous epilogue column chunks per warp (bit 19 clears)
 static int g_tstore_policy = 0;    // TMA-store epilogue where it applies (bit 18 sets; measured equal
@@ -813,7 +815,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
-  g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : 1;
+  g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -987,7 +989,8 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   // phases), 16-byte aligned rows, no XF transform warps
   kp.tstore = (g_tstore_policy && a.mode != GEMM_SUBPIX && !a.gn_ss && !(reinterpret_cast<uintptr_t>(a.out) & 15) &&
                a.ldo % 8 == 0) ? 1 : 0;
-  kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy) ? 1 : 0;
+  kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy &&
+            (g_rpf_policy == 2 || a.N <= 128)) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
