@@ -111,6 +111,16 @@ size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w);
 lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint32_t h, uint32_t w, uint8_t* out_dev,
                            size_t stride, uint32_t* sizes_dev, lbx_stream stream);
 
+/* Return path (the paper PNG-encodes on CPU): PNG encode of n
+ * uint8 RGB images already on the GPU (rgb_dev, [n][h][w][3], e.g. lbx_decode's output).  PNG i is
+ * written at out_dev + i * stride (stride >= lbx_png_bound(h, w)) and its size to sizes_dev[i]
+ * (uint32, device).  8-bit RGB, per-row adaptive filter, zlib/DEFLATE with dynamic Huffman codes
+ * (stored where smaller); lossless: any PNG decoder returns rgb exactly.  w <= 8192, h <= 65535.
+ * Asynchronous on `stream`. */
+size_t lbx_png_bound(uint32_t h, uint32_t w);
+lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
+                                 size_t stride, uint32_t* sizes_dev, lbx_stream stream);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* lbx_last_error(void);
 
@@ -176,7 +186,8 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * selects the register-staged GroupNorm apply instead of the bulk-copy (1-D TMA) one; 9 transposes the
  * attention's V with a kernel instead of reading it in place as an MN-major B operand; 10 adds conv
  * residuals in the epilogue instead of preloading them into the TMEM accumulator (default: preload for
- * 128-wide outputs, epilogue add for wider ones; bit 20 preloads at every width); 12-15 are
+ * 128-wide outputs, epilogue add for wider ones; bit 20 preloads at every width; bit 21 L2-prefetches
+ * the next preload's rows); 12-15 are
  * epilogue ablations (wrong results: skip all work / keep only TMEM loads / no stores / no
  * statistics); bits 16-17 = 1 + epilogue store mode (0 STG.128, 1 STG.256 = default, 2 streaming); 18
  * stages epilogue chunks in smem and TMA-stores them (measured equal to STG.256).

@@ -970,6 +970,29 @@ lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint
   return LBX_OK;
 }
 
+size_t lbx_png_bound(uint32_t h, uint32_t w) {
+  if (h == 0 || w == 0 || w > 8192 || h > 65535) return 0;
+  return lbx::png_bound((int)h, (int)w);
+}
+
+lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
+                                 size_t stride, uint32_t* sizes_dev, lbx_stream stream) {
+  if (n == 0) return LBX_OK;
+  if (!rgb_dev || !out_dev || !sizes_dev) return set_err(LBX_E_CONFIG, "lbx_png_encode_device: null pointer");
+  if (h == 0 || w == 0 || w > 8192 || h > 65535)
+    return set_err(LBX_E_CONFIG, "lbx_png_encode_device: shape must be nonzero, w <= 8192, h <= 65535");
+  if (stride < lbx::png_bound((int)h, (int)w))
+    return set_err(LBX_E_CONFIG, "lbx_png_encode_device: stride must be >= lbx_png_bound(h, w)");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* work = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&work), lbx::png_workspace((int)n, (int)h, (int)w), s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "lbx_png_encode_device: cudaMallocAsync");
+  cudaError_t e = lbx::launch_png_encode(rgb_dev, (int)n, (int)h, (int)w, out_dev, (long long)stride, sizes_dev, work, s);
+  cudaFreeAsync(work, s);
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("lbx_png_encode_device: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
 lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
                            int H, int W, int impl, lbx_stream stream) {
   if (!x || !ss || !w || !b || !rgb || n <= 0 || H <= 0 || W <= 0)

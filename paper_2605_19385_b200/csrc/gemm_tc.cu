@@ -59,6 +59,7 @@ struct KParams {
   int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
   int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
+  int rpf_pf;          // 1: L2-prefetch the next preload's rows before waiting for the accumulator
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
@@ -87,6 +88,7 @@ struct Cfg {
 };
 
 __device__ __forceinline__ int g_store_mode_dev(const KParams& p) { return p.store_mode; }
+__device__ __forceinline__ int g_rpf_l2pf_dev(const KParams& p) { return p.rpf_pf; }
 
 __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile, int& n_tile, int& phase) {
   n_tile = t % p.n_tiles;
@@ -556,6 +558,18 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         else ptx::mbar_arrive_cluster_relaxed(&tempty[buf], 0);
       }
     };
+    // L2 prefetch of the rows the next preload reads, issued before the wait for the accumulator
+    auto prefetch_resid = [&](int tn) {
+      if (tn >= p.tiles || !g_rpf_l2pf_dev(p)) return;
+      int mt, nt, phn;
+      tile_coords(p, tn, mt, nt, phn);
+      for (int sub = 0; sub < p.msub; ++sub) {
+        const long long mrow = tile_row0(p, mt, (int)rank, CG, sub) + row;
+        const __half* rb = p.resid + mrow * p.ldr + nt * BN + cbase * 32;
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(rb + j * 32 * cstep));
+      }
+    };
     if (p.rpf) {
       prefill(cluster_id, 0);
       prefill(cluster_id + nclusters, 1);
@@ -577,6 +591,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         __syncwarp();
         bias_ntile = n_tile;
       }
+      if (p.rpf) prefetch_resid(t + 2 * nclusters);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       for (int sub = 0; sub < (p.epi_skip == 1 ? 0 : p.msub); ++sub) {
@@ -799,6 +814,8 @@ static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel inst
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
+static int g_rpf_pf = 0;           // 1: L2 prefetch ahead of the residual preload (bit 21 sets;
+                                   // measured neutral under the power cap)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
 static int g_cmap_policy = 1;      // 1: contiguous epilogue column chunks per warp (bit 19 clears)
 static int g_tstore_policy = 0;    // TMA-store epilogue where it applies (bit 18 sets; measured equal
@@ -816,6 +833,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
+  g_rpf_pf = (halo_policy >> 21) & 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -991,6 +1009,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
                a.ldo % 8 == 0) ? 1 : 0;
   kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy &&
             (g_rpf_policy == 2 || a.N <= 128)) ? 1 : 0;
+  kp.rpf_pf = g_rpf_pf;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||

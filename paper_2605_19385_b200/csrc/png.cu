@@ -1,0 +1,746 @@
+// PNG encode of decoded RGB on the GPU -- SURVEY.md 8(f) item 3: the paper encodes the returned
+// image as PNG in a CPU compute pool (~10 ms network for the PNG); here
+// the uint8 RGB the decoder leaves in HBM is encoded where it lies and only the PNG crosses PCIe.
+//
+// Format (PNG 1.2 / RFC 1950 zlib / RFC 1951 DEFLATE): signature, IHDR (8-bit RGB, no interlace),
+// one IDAT chunk per strip of R rows, IEND.  The zlib stream is the concatenation of the strips'
+// DEFLATE data: every strip is one block (dynamic Huffman, or stored when that is smaller); a
+// non-final strip ends with an empty stored block (a "sync flush") so the next strip starts on a
+// byte boundary, and its matches may reach back into the previous strip's last row (the inflater
+// keeps a 32 KB window across blocks).
+//
+//   K-a png_strip_kernel   one CTA per strip: per-row filter choice (the minimum sum of |signed
+//                          residual| over the five PNG filters, the libpng heuristic), LZ77 parse
+//                          (256 independent segments, greedy, distances {1, 3, 6, row}), Huffman
+//                          code construction (length-limited 15 / 7), bit packing through
+//                          per-thread offsets from a block scan; Adler-32 partials of the strip.
+//   K-b png_image_kernel   one CTA per image: Adler-32 combine, chunk offsets (scan), signature,
+//                          IHDR, IEND, total size.
+//   K-c png_chunk_kernel   one CTA per strip: copy the strip's data to its chunk and CRC-32 it
+//                          (per-thread segments combined by multiplication by x^(8n) mod P).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace lbx {
+
+namespace {
+
+constexpr int kT = 256;                 // threads per CTA
+constexpr int kMaxStripBytes = 32768;   // filtered bytes per strip
+constexpr uint32_t kAdler = 65521u;
+constexpr uint32_t kCrcPoly = 0xEDB88320u;
+
+struct StripMeta {
+  uint32_t bytes;  // zlib bytes of the strip (incl. the 4 Adler-32 bytes of the last strip)
+  uint32_t a, b;   // Adler-32 partials of the strip's filtered bytes (mod 65521)
+  uint32_t rsv;
+};
+
+struct PngGeom {
+  int n, H, W;
+  int RS;       // filtered row bytes, 3W + 1
+  int R;        // rows per strip
+  int nstrips;  // strips per image
+  int cap;      // scratch bytes per strip
+  int G;        // parse segment bytes per thread
+  // dynamic smem layout (bytes): tokens alias the raw rows (dead after filtering)
+  int off_filt, off_ow, off_tab, smem;
+};
+
+__host__ __device__ inline int strip_rows(const PngGeom& g, int s) {
+  const int r = g.H - s * g.R;
+  return r < g.R ? r : g.R;
+}
+
+// --------------------------------------------------------------------------- DEFLATE symbol maps
+__device__ __forceinline__ void len_sym(int len, int& code, int& nb, int& ev) {  // RFC 1951 3.2.5
+  if (len <= 10) { code = 254 + len; nb = 0; ev = 0; return; }
+  if (len == 258) { code = 285; nb = 0; ev = 0; return; }
+  const int l = len - 3;
+  nb = 29 - __clz(l);  // floor(log2 l) - 2
+  code = 257 + 4 * (nb + 1) + ((l >> nb) & 3);
+  ev = l & ((1 << nb) - 1);
+}
+__device__ __forceinline__ void dist_sym(int d, int& code, int& nb, int& ev) {
+  const int v = d - 1;
+  if (v < 4) { code = v; nb = 0; ev = 0; return; }
+  nb = 30 - __clz(v);  // floor(log2 v) - 1
+  code = 2 * (nb + 1) + ((v >> nb) & 1);
+  ev = v & ((1 << nb) - 1);
+}
+
+__device__ __forceinline__ uint32_t rev_bits(uint32_t c, int n) { return __brev(c) >> (32 - n); }
+
+// --------------------------------------------------------------------------- Huffman construction
+// Single-thread: code lengths (<= L) for `n` symbols with frequencies `freq`, given `order` = the
+// m used symbols sorted by (freq, symbol) ascending.  Two-queue Huffman over the sorted leaves, then
+// the Kraft repair that moves overlong codes to L and splits shorter ones, then lengths handed
+// out longest-first to the least frequent symbols.  Fewer than two used symbols get dummies so
+// every code is complete (zlib's inflate rejects incomplete code-length codes).
+struct HuffWork {
+  uint32_t w[320];
+  uint16_t par[640];
+  uint8_t depth[640];
+};
+
+__device__ void huff_lengths(const uint32_t* freq, int n, uint16_t* order, int m, int L, uint8_t* lens,
+                             HuffWork& hw) {
+  for (int i = 0; i < n; ++i) lens[i] = 0;
+  if (m < 2) {
+    const int a = m == 1 ? order[0] : 0;
+    lens[a] = 1;
+    lens[a == 0 ? 1 : 0] = 1;
+    return;
+  }
+  // leaves 0..m-1, internal nodes m..2m-2; weights of internal nodes in hw.w
+  int li = 0, ii = 0, ni = 0;
+  auto take = [&](uint32_t& wt) -> int {
+    if (li < m && (ii >= ni || freq[order[li]] <= hw.w[ii])) { wt = freq[order[li]]; return li++; }
+    wt = hw.w[ii];
+    return m + ii++;
+  };
+  for (int k = 0; k < m - 1; ++k) {
+    uint32_t wa, wb;
+    const int a = take(wa), b = take(wb);
+    hw.w[ni] = wa + wb;
+    hw.par[a] = (uint16_t)(m + ni);
+    hw.par[b] = (uint16_t)(m + ni);
+    ++ni;
+  }
+  const int root = m + ni - 1;
+  hw.depth[root] = 0;
+  int cnt[33];
+  for (int i = 0; i <= 32; ++i) cnt[i] = 0;
+  for (int v = root - 1; v >= 0; --v) {
+    const int d = hw.depth[hw.par[v]] + 1;
+    hw.depth[v] = (uint8_t)(d > 32 ? 32 : d);
+    if (v < m) ++cnt[d > L ? L : d];
+  }
+  uint32_t total = 0;
+  for (int i = 1; i <= L; ++i) total += (uint32_t)cnt[i] << (L - i);
+  while (total > (1u << L)) {
+    --cnt[L];
+    for (int i = L - 1; i > 0; --i)
+      if (cnt[i]) { --cnt[i]; cnt[i + 1] += 2; break; }
+    --total;
+  }
+  int idx = 0;
+  for (int len = L; len >= 1; --len)
+    for (int c = 0; c < cnt[len]; ++c) lens[order[idx++]] = (uint8_t)len;
+}
+
+// canonical codes (RFC 1951 3.2.2), stored bit-reversed for the LSB-first bit stream
+__device__ void huff_codes(const uint8_t* lens, int n, uint16_t* codes) {
+  int cnt[16] = {0};
+  for (int i = 0; i < n; ++i) ++cnt[lens[i]];
+  cnt[0] = 0;
+  int next[16];
+  int code = 0;
+  for (int b = 1; b < 16; ++b) {
+    code = (code + cnt[b - 1]) << 1;
+    next[b] = code;
+  }
+  for (int i = 0; i < n; ++i)
+    codes[i] = lens[i] ? (uint16_t)rev_bits((uint32_t)next[lens[i]]++, lens[i]) : (uint16_t)0;
+}
+
+// LSB-first bit writer into a zeroed word buffer (words shared with neighbours: atomicOr)
+struct BitW {
+  uint32_t* w;
+  uint32_t pos;  // word index
+  uint64_t acc;
+  int nacc;
+  __device__ BitW(uint32_t* words, uint32_t bit) : w(words), pos(bit >> 5), acc(0), nacc((int)(bit & 31)) {}
+  __device__ __forceinline__ void put(uint32_t v, int n) {
+    acc |= (uint64_t)v << nacc;
+    nacc += n;
+    if (nacc >= 32) {
+      atomicOr(&w[pos++], (uint32_t)acc);
+      acc >>= 32;
+      nacc -= 32;
+    }
+  }
+  __device__ __forceinline__ void flush() {
+    if (nacc > 0) atomicOr(&w[pos], (uint32_t)acc);
+  }
+};
+
+__device__ __forceinline__ int paeth(int a, int b, int c) {
+  const int p = a + b - c, pa = abs(p - a), pb = abs(p - b), pc = abs(p - c);
+  return (pa <= pb && pa <= pc) ? a : (pb <= pc ? b : c);
+}
+
+__device__ __forceinline__ uint8_t filt_byte(int type, int x, int a, int b, int c) {
+  switch (type) {
+    case 0: return (uint8_t)x;
+    case 1: return (uint8_t)(x - a);
+    case 2: return (uint8_t)(x - b);
+    case 3: return (uint8_t)(x - ((a + b) >> 1));
+    default: return (uint8_t)(x - paeth(a, b, c));
+  }
+}
+
+__device__ __forceinline__ uint32_t block_sum_u32(uint32_t v, uint32_t* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  uint32_t s = 0;
+  for (int i = 0; i < kT / 32; ++i) s += red[i];
+  return s;
+}
+
+// exclusive block scan of per-thread values; returns this thread's prefix, *total the sum
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* red, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  __syncthreads();
+  if (lane == 31) red[wid] = inc;
+  __syncthreads();
+  uint32_t before = 0, all = 0;
+  for (int i = 0; i < kT / 32; ++i) {
+    if (i < wid) before += red[i];
+    all += red[i];
+  }
+  *total = all;
+  return before + inc - v;
+}
+
+struct StripTables {
+  uint32_t lfreq[286 + 30];  // literal/length then distance frequencies
+  uint32_t cfreq[19];
+  uint16_t order[320];
+  uint16_t corder[19];
+  uint8_t llen[286 + 30];
+  uint8_t clen[19];
+  uint16_t lcode[286 + 30];
+  uint16_t ccode[19];
+  uint16_t rle[320];   // code-length RLE symbols (sym | extra << 5)
+  uint32_t red[kT / 32];
+  uint32_t scal[8];    // 0 nrle, 1 hlit, 2 hdist, 3 hclen, 4 header bits, 5 m_lit, 6 m_dist
+  uint16_t ntok[kT];
+  HuffWork hw;
+  unsigned long long ab[2][kT / 32];
+  uint32_t fsum[5][kT / 32];
+};
+
+__global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict__ rgb, PngGeom g,
+                                                       uint8_t* __restrict__ scratch, StripMeta* __restrict__ meta) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int t = threadIdx.x;
+  const int img = blockIdx.x / g.nstrips, s = blockIdx.x - img * g.nstrips;
+  const int y0 = s * g.R, rows = strip_rows(g, s);
+  const int rb = 3 * g.W, RS = g.RS;
+  const int S = rows * RS;
+  const bool first = s == 0, last = s == g.nstrips - 1;
+  uint8_t* raw = sm;                       // rows y0-2 .. y0+rows-1 (3W bytes each)
+  uint16_t* tok = reinterpret_cast<uint16_t*>(sm);  // LZ77 tokens, once the raw rows are filtered
+  uint8_t* filt = sm + g.off_filt;         // row y0-1 then the strip's rows (RS bytes each)
+  uint32_t* ow = reinterpret_cast<uint32_t*>(sm + g.off_ow);  // the strip's zlib bytes
+  StripTables& T = *reinterpret_cast<StripTables*>(sm + g.off_tab);
+
+  // ---- 1. raw rows into smem (rows before the image are zero)
+  const uint8_t* src = rgb + (size_t)img * g.H * rb;
+  const int nraw = rows + 2;
+  if ((rb & 15) == 0) {
+    const int per = rb / 16;
+    for (int i = t; i < nraw * per; i += kT) {
+      const int r = i / per, c = i - r * per, y = y0 - 2 + r;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (y >= 0) v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)y * rb) + c);
+      reinterpret_cast<uint4*>(raw + r * rb)[c] = v;
+    }
+  } else {
+    for (int i = t; i < nraw * rb; i += kT) {
+      const int r = i / rb, c = i - r * rb, y = y0 - 2 + r;
+      raw[i] = y >= 0 ? src[(size_t)y * rb + c] : (uint8_t)0;
+    }
+  }
+  for (int i = t; i < 286 + 30; i += kT) T.lfreq[i] = 0;
+  if (t < 19) T.cfreq[t] = 0;
+  __syncthreads();
+
+  // ---- 2. filter rows y0-1 (history, when it exists) .. y0+rows-1
+  for (int fr = (y0 > 0 ? 0 : 1); fr <= rows; ++fr) {
+    const uint8_t* cur = raw + (fr + 1) * rb;  // image row y0-1+fr
+    const uint8_t* up = raw + fr * rb;         // zeros above row 0
+    uint32_t sum[5] = {0, 0, 0, 0, 0};
+    for (int i = t; i < rb; i += kT) {
+      const int x = cur[i], a = i >= 3 ? cur[i - 3] : 0, b = up[i], c = i >= 3 ? up[i - 3] : 0;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) sum[k] += (uint32_t)abs((int)(int8_t)filt_byte(k, x, a, b, c));
+    }
+    const int lane = t & 31, wid = t >> 5;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+#pragma unroll
+      for (int o = 16; o; o >>= 1) sum[k] += __shfl_xor_sync(0xffffffffu, sum[k], o);
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) T.fsum[k][wid] = sum[k];
+    }
+    __syncthreads();
+    int best = 0;
+    uint32_t bsum = 0xffffffffu;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      uint32_t tot = 0;
+      for (int w = 0; w < kT / 32; ++w) tot += T.fsum[k][w];
+      if (tot < bsum) { bsum = tot; best = k; }  // ties: the lower filter type
+    }
+    uint8_t* out = filt + fr * RS;
+    if (t == 0) out[0] = (uint8_t)best;
+    for (int i = t; i < rb; i += kT) {
+      const int x = cur[i], a = i >= 3 ? cur[i - 3] : 0, b = up[i], c = i >= 3 ? up[i - 3] : 0;
+      out[1 + i] = filt_byte(best, x, a, b, c);
+    }
+  }
+  __syncthreads();
+  const uint8_t* f = filt + RS;  // the strip's bytes; f[-RS..-1] is the previous row when y0 > 0
+
+  // ---- 3. Adler-32 partials: a = sum x_j, b = sum (S - j) x_j
+  {
+    unsigned long long a = 0, b = 0;
+    for (int j = t; j < S; j += kT) {
+      a += f[j];
+      b += (unsigned long long)(S - j) * f[j];
+    }
+    const int lane = t & 31, wid = t >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) { T.ab[0][wid] = a; T.ab[1][wid] = b; }
+  }
+
+  // ---- 4. LZ77 parse: thread t owns [t*G, min((t+1)*G, S)), greedy, matches end inside it
+  const int dists[4] = {1, 3, 6, RS};
+  const int lo = y0 > 0 ? -RS : 0;
+  int nt = 0;
+  {
+    const int p0 = t * g.G, p1 = min(p0 + g.G, S);
+    uint16_t* tk = tok + t * g.G;
+    for (int p = p0; p < p1;) {
+      const int maxl = min(258, p1 - p);
+      int bl = 0, bd = 0;
+      if (maxl >= 3) {
+#pragma unroll
+        for (int di = 0; di < 4; ++di) {
+          const int d = dists[di];
+          if (p - d < lo) continue;
+          int l = 0;
+          while (l < maxl && f[p + l] == f[p + l - d]) ++l;
+          if (l > bl) { bl = l; bd = di; }
+        }
+      }
+      if (bl >= 3) {
+        tk[nt++] = (uint16_t)(0x8000u | (bd << 8) | (bl - 3));
+        int c, nb, ev;
+        len_sym(bl, c, nb, ev);
+        atomicAdd(&T.lfreq[c], 1u);
+        dist_sym(dists[bd], c, nb, ev);
+        atomicAdd(&T.lfreq[286 + c], 1u);
+        p += bl;
+      } else {
+        tk[nt++] = f[p];
+        atomicAdd(&T.lfreq[f[p]], 1u);
+        ++p;
+      }
+    }
+    T.ntok[t] = (uint16_t)nt;
+  }
+  __syncthreads();
+  if (t == 0) T.lfreq[256] = 1;  // end of block
+  __syncthreads();
+
+  // ---- 5. sort the used literal/length and distance symbols by (freq, symbol): rank by counting
+  for (int sym = t; sym < 286 + 30; sym += kT) {
+    const uint32_t fs = T.lfreq[sym];
+    if (!fs) continue;
+    const int b0 = sym < 286 ? 0 : 286, b1 = sym < 286 ? 286 : 316;
+    int rank = 0;
+    for (int u = b0; u < b1; ++u) {
+      const uint32_t fu = T.lfreq[u];
+      rank += fu && (fu < fs || (fu == fs && u < sym));
+    }
+    T.order[b0 + rank] = (uint16_t)sym;
+  }
+  {
+    uint32_t ml = 0, md = 0;
+    for (int sym = t; sym < 286 + 30; sym += kT)
+      if (T.lfreq[sym]) { if (sym < 286) ++ml; else ++md; }
+    ml = block_sum_u32(ml, T.red);
+    md = block_sum_u32(md, T.red);
+    if (t == 0) { T.scal[5] = ml; T.scal[6] = md; }
+  }
+  __syncthreads();
+
+  // ---- 6. codes and the block header (thread 0)
+  if (t == 0) {
+    const int ml = (int)T.scal[5], md = (int)T.scal[6];
+    for (int i = 0; i < md; ++i) T.order[286 + i] -= 286;  // distance symbols relative to 0
+    huff_lengths(T.lfreq, 286, T.order, ml, 15, T.llen, T.hw);
+    huff_lengths(T.lfreq + 286, 30, T.order + 286, md, 15, T.llen + 286, T.hw);
+    huff_codes(T.llen, 286, T.lcode);
+    huff_codes(T.llen + 286, 30, T.lcode + 286);
+    int hlit = 286, hdist = 30;
+    while (hlit > 257 && !T.llen[hlit - 1]) --hlit;
+    while (hdist > 1 && !T.llen[286 + hdist - 1]) --hdist;
+    // run-length code the hlit + hdist code lengths (RFC 1951 3.2.7)
+    const int nl = hlit + hdist;
+    auto seq = [&](int i) -> int { return i < hlit ? T.llen[i] : T.llen[286 + i - hlit]; };
+    int nr = 0;
+    for (int i = 0; i < nl;) {
+      const int v = seq(i);
+      int run = 1;
+      while (i + run < nl && seq(i + run) == v) ++run;
+      if (v == 0) {
+        int r = run;
+        while (r >= 11) { const int k = r < 138 ? r : 138; T.rle[nr++] = (uint16_t)(18 | ((k - 11) << 5)); r -= k; }
+        if (r >= 3) { T.rle[nr++] = (uint16_t)(17 | ((r - 3) << 5)); r = 0; }
+        while (r-- > 0) T.rle[nr++] = 0;
+      } else {
+        T.rle[nr++] = (uint16_t)v;
+        int r = run - 1;
+        while (r >= 3) { const int k = r < 6 ? r : 6; T.rle[nr++] = (uint16_t)(16 | ((k - 3) << 5)); r -= k; }
+        while (r-- > 0) T.rle[nr++] = (uint16_t)v;
+      }
+      i += run;
+    }
+    for (int i = 0; i < nr; ++i) ++T.cfreq[T.rle[i] & 31];
+    int mc = 0;
+    for (int sym = 0; sym < 19; ++sym)  // insertion sort of the used code-length symbols
+      if (T.cfreq[sym]) {
+        int j = mc++;
+        while (j > 0 && (T.cfreq[T.corder[j - 1]] > T.cfreq[sym])) { T.corder[j] = T.corder[j - 1]; --j; }
+        T.corder[j] = (uint16_t)sym;
+      }
+    huff_lengths(T.cfreq, 19, T.corder, mc, 7, T.clen, T.hw);
+    huff_codes(T.clen, 19, T.ccode);
+    const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && !T.clen[kOrd[hclen - 1]]) --hclen;
+    uint32_t bits = 3 + 5 + 5 + 4 + 3 * hclen;
+    for (int i = 0; i < nr; ++i) {
+      const int sym = T.rle[i] & 31;
+      bits += T.clen[sym] + (sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0);
+    }
+    T.scal[0] = (uint32_t)nr; T.scal[1] = (uint32_t)hlit; T.scal[2] = (uint32_t)hdist;
+    T.scal[3] = (uint32_t)hclen; T.scal[4] = bits;
+  }
+  __syncthreads();
+
+  // ---- 7. token bits, offsets, dynamic vs stored
+  const int dcode[4] = {0, 2, 4, 0};
+  int dc3, dnb3, dev3;
+  dist_sym(RS, dc3, dnb3, dev3);
+  auto tok_bits = [&](uint16_t v) -> uint32_t {
+    if (!(v & 0x8000u)) return T.llen[v];
+    int c, nb, ev;
+    len_sym((v & 255) + 3, c, nb, ev);
+    const int di = (v >> 8) & 3;
+    const int dc = di == 3 ? dc3 : dcode[di], dnb = di == 3 ? dnb3 : (di == 2 ? 1 : 0);
+    return T.llen[c] + nb + T.llen[286 + dc] + dnb;
+  };
+  uint32_t mybits = 0;
+  const uint16_t* tk = tok + t * g.G;
+  for (int k = 0; k < nt; ++k) mybits += tok_bits(tk[k]);
+  uint32_t tbits;
+  const uint32_t myoff = block_scan_u32(mybits, T.red, &tbits);
+  const uint32_t pre = first ? 16u : 0u;  // zlib header
+  const uint32_t dyn_end = pre + T.scal[4] + tbits + T.llen[256];  // bit after the end-of-block code
+  const uint32_t dyn_bytes = (last ? (dyn_end + 7) / 8 : (dyn_end + 3 + 7) / 8 + 4) + (last ? 4 : 0);
+  const uint32_t sto_bytes = pre / 8 + 5 + (uint32_t)S + (last ? 4 : 0);
+  const bool dyn = dyn_bytes < sto_bytes;
+  const uint32_t bytes = dyn ? dyn_bytes : sto_bytes;
+  const int nw = (int)(bytes + 3) / 4 + 1;
+  __syncthreads();
+  for (int i = t; i < nw; i += kT) ow[i] = 0;
+  __syncthreads();
+
+  // ---- 8. write
+  if (dyn) {
+    if (t == 0) {
+      BitW w(ow, 0);
+      if (first) { w.put(0x78, 8); w.put(0x5E, 8); }
+      w.put(last ? 1u : 0u, 1);
+      w.put(2, 2);
+      w.put(T.scal[1] - 257, 5);
+      w.put(T.scal[2] - 1, 5);
+      w.put(T.scal[3] - 4, 4);
+      const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+      for (int i = 0; i < (int)T.scal[3]; ++i) w.put(T.clen[kOrd[i]], 3);
+      for (int i = 0; i < (int)T.scal[0]; ++i) {
+        const int sym = T.rle[i] & 31, ex = T.rle[i] >> 5;
+        w.put(T.ccode[sym], T.clen[sym]);
+        if (sym == 16) w.put(ex, 2);
+        else if (sym == 17) w.put(ex, 3);
+        else if (sym == 18) w.put(ex, 7);
+      }
+      w.flush();
+    }
+    {
+      BitW w(ow, pre + T.scal[4] + myoff);
+      for (int k = 0; k < nt; ++k) {
+        const uint16_t v = tk[k];
+        if (!(v & 0x8000u)) {
+          w.put(T.lcode[v], T.llen[v]);
+        } else {
+          int c, nb, ev;
+          len_sym((v & 255) + 3, c, nb, ev);
+          w.put(T.lcode[c], T.llen[c]);
+          if (nb) w.put((uint32_t)ev, nb);
+          const int di = (v >> 8) & 3;
+          const int d = di == 0 ? 1 : di == 1 ? 3 : di == 2 ? 6 : RS;
+          dist_sym(d, c, nb, ev);
+          w.put(T.lcode[286 + c], T.llen[286 + c]);
+          if (nb) w.put((uint32_t)ev, nb);
+        }
+      }
+      w.flush();
+    }
+    __syncthreads();
+    if (t == 0) {
+      BitW w(ow, dyn_end - T.llen[256]);
+      w.put(T.lcode[256], T.llen[256]);
+      if (!last) w.put(0, 3);  // empty stored block: BFINAL 0, BTYPE 00, then pad + 00 00 FF FF
+      w.flush();
+      if (!last) {
+        uint8_t* ob = reinterpret_cast<uint8_t*>(ow);
+        const uint32_t e = (dyn_end + 3 + 7) / 8;
+        ob[e] = 0; ob[e + 1] = 0; ob[e + 2] = 0xFF; ob[e + 3] = 0xFF;
+      }
+    }
+  } else {
+    uint8_t* ob = reinterpret_cast<uint8_t*>(ow);
+    const int h = (int)pre / 8;
+    if (t == 0) {
+      if (first) { ob[0] = 0x78; ob[1] = 0x5E; }
+      ob[h] = last ? 1 : 0;  // BFINAL, BTYPE 00, padding
+      ob[h + 1] = (uint8_t)(S & 255); ob[h + 2] = (uint8_t)(S >> 8);
+      ob[h + 3] = (uint8_t)(~S & 255); ob[h + 4] = (uint8_t)((~S >> 8) & 255);
+    }
+    __syncthreads();
+    for (int j = t; j < S; j += kT) ob[h + 5 + j] = f[j];
+  }
+  __syncthreads();
+
+  // ---- 9. out to the strip's scratch slot; meta
+  uint8_t* dst = scratch + (size_t)blockIdx.x * g.cap;
+  const int nvec = ((int)bytes + 15) / 16;
+  for (int i = t; i < nvec; i += kT) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(ow)[i];
+  if (t == 0) {
+    unsigned long long a = 0, b = 0;
+    for (int w = 0; w < kT / 32; ++w) { a += T.ab[0][w]; b += T.ab[1][w]; }
+    StripMeta m;
+    m.bytes = bytes;
+    m.a = (uint32_t)(a % kAdler);
+    m.b = (uint32_t)(b % kAdler);
+    m.rsv = dyn ? 1u : 0u;
+    meta[blockIdx.x] = m;
+  }
+}
+
+// --------------------------------------------------------------------------- CRC-32
+__device__ __forceinline__ uint32_t crc_mulmod(uint32_t a, uint32_t b) {  // a*b mod P, reflected
+  if (!a) return 0;
+  uint32_t m = 1u << 31, p = 0;
+  for (;;) {
+    if (a & m) {
+      p ^= b;
+      if (!(a & (m - 1))) break;
+    }
+    m >>= 1;
+    b = (b & 1) ? (b >> 1) ^ kCrcPoly : b >> 1;
+  }
+  return p;
+}
+__device__ uint32_t crc_x8n(unsigned long long n) {  // x^(8n) mod P
+  uint32_t r = 1u << 31, base = 1u << 23;             // x^0, x^8
+  while (n) {
+    if (n & 1) r = crc_mulmod(base, r);
+    base = crc_mulmod(base, base);
+    n >>= 1;
+  }
+  return r;
+}
+__device__ __forceinline__ void crc_table(uint32_t* tab) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    uint32_t c = (uint32_t)i;
+    for (int k = 0; k < 8; ++k) c = (c & 1) ? (c >> 1) ^ kCrcPoly : c >> 1;
+    tab[i] = c;
+  }
+}
+__device__ __forceinline__ uint32_t crc_raw(const uint32_t* tab, uint32_t c, const uint8_t* p, int n) {
+  for (int i = 0; i < n; ++i) c = (c >> 8) ^ tab[(c ^ p[i]) & 255];
+  return c;
+}
+
+__device__ __forceinline__ void put_be32(uint8_t* p, uint32_t v) {
+  p[0] = (uint8_t)(v >> 24); p[1] = (uint8_t)(v >> 16); p[2] = (uint8_t)(v >> 8); p[3] = (uint8_t)v;
+}
+
+// --------------------------------------------------------------------------- K-b: per image
+__global__ void __launch_bounds__(kT) png_image_kernel(PngGeom g, uint8_t* __restrict__ scratch,
+                                                       const StripMeta* __restrict__ meta, uint32_t* __restrict__ offs,
+                                                       uint8_t* __restrict__ out, long long stride,
+                                                       uint32_t* __restrict__ sizes) {
+  __shared__ uint32_t tab[256];
+  __shared__ uint32_t red[kT / 32];
+  __shared__ unsigned long long ared[2][kT / 32];
+  crc_table(tab);
+  const int img = blockIdx.x, t = threadIdx.x, ns = g.nstrips;
+  const StripMeta* mi = meta + (size_t)img * ns;
+  const unsigned long long N = (unsigned long long)g.H * g.RS;
+  // Adler-32 of the whole filtered stream: A = 1 + sum a_s, B = N + sum (b_s + (N - o_s - S_s) a_s)
+  unsigned long long A = 0, B = 0;
+  const int per = (ns + kT - 1) / kT, s0 = t * per;
+  uint32_t mine = 0;
+  for (int s = s0; s < s0 + per && s < ns; ++s) {
+    const unsigned long long o = (unsigned long long)s * g.R * g.RS, Ss = (unsigned long long)strip_rows(g, s) * g.RS;
+    A += mi[s].a;
+    B += mi[s].b + ((N - o - Ss) % kAdler) * mi[s].a % kAdler;
+    mine += 12u + mi[s].bytes;
+  }
+  {
+    const int lane = t & 31, wid = t >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      A += __shfl_xor_sync(0xffffffffu, A, o);
+      B += __shfl_xor_sync(0xffffffffu, B, o);
+    }
+    if (lane == 0) { ared[0][wid] = A; ared[1][wid] = B; }
+  }
+  uint32_t total;
+  uint32_t off = 33u + block_scan_u32(mine, red, &total);  // after signature + IHDR
+  for (int s = s0; s < s0 + per && s < ns; ++s) {
+    offs[(size_t)img * ns + s] = off;
+    off += 12u + mi[s].bytes;
+  }
+  uint8_t* o = out + (size_t)img * stride;
+  if (t == 0) {
+    unsigned long long a = 1, b = N % kAdler;
+    for (int w = 0; w < kT / 32; ++w) { a += ared[0][w]; b += ared[1][w]; }
+    const uint32_t adler = (uint32_t)((b % kAdler) << 16 | (a % kAdler));
+    put_be32(scratch + ((size_t)img * ns + ns - 1) * g.cap + mi[ns - 1].bytes - 4, adler);
+    const uint8_t sig[8] = {0x89, 'P', 'N', 'G', 0x0D, 0x0A, 0x1A, 0x0A};
+    for (int i = 0; i < 8; ++i) o[i] = sig[i];
+    uint8_t ih[17] = {'I', 'H', 'D', 'R'};
+    put_be32(ih + 4, (uint32_t)g.W);
+    put_be32(ih + 8, (uint32_t)g.H);
+    ih[12] = 8; ih[13] = 2; ih[14] = 0; ih[15] = 0; ih[16] = 0;  // 8-bit RGB, deflate, adaptive, no interlace
+    put_be32(o + 8, 13);
+    for (int i = 0; i < 17; ++i) o[12 + i] = ih[i];
+    put_be32(o + 29, ~crc_raw(tab, 0xFFFFFFFFu, ih, 17));
+    const uint32_t e = 33u + total;
+    const uint8_t iend[12] = {0, 0, 0, 0, 'I', 'E', 'N', 'D', 0xAE, 0x42, 0x60, 0x82};
+    for (int i = 0; i < 12; ++i) o[e + i] = iend[i];
+    sizes[img] = e + 12u;
+  }
+}
+
+// --------------------------------------------------------------------------- K-c: per strip
+__global__ void __launch_bounds__(kT) png_chunk_kernel(PngGeom g, const uint8_t* __restrict__ scratch,
+                                                       const StripMeta* __restrict__ meta,
+                                                       const uint32_t* __restrict__ offs, uint8_t* __restrict__ out,
+                                                       long long stride) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint32_t tab[256];
+  __shared__ uint32_t xr[kT / 32];
+  crc_table(tab);
+  const int t = threadIdx.x, img = blockIdx.x / g.nstrips;
+  const uint32_t d = meta[blockIdx.x].bytes, L = d + 4;  // CRC covers "IDAT" + data
+  uint8_t* buf = sm;                                      // "IDAT" at 12..15, data from 16
+  const uint8_t* src = scratch + (size_t)blockIdx.x * g.cap;
+  for (int i = t; i < (int)(d + 15) / 16; i += kT)
+    reinterpret_cast<uint4*>(buf + 16)[i] = reinterpret_cast<const uint4*>(src)[i];
+  if (t == 0) { buf[12] = 'I'; buf[13] = 'D'; buf[14] = 'A'; buf[15] = 'T'; }
+  __syncthreads();
+  const uint8_t* c0 = buf + 12;
+  const uint32_t seg = (L + kT - 1) / kT, b0 = min(L, t * seg), b1 = min(L, b0 + seg);
+  uint32_t c = crc_raw(tab, 0u, c0 + b0, (int)(b1 - b0));
+  c = crc_mulmod(crc_x8n(L - b1), c);  // shift past the bytes after this segment
+  if (t == 0) c ^= crc_mulmod(crc_x8n(L), 0xFFFFFFFFu);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+  if ((t & 31) == 0) xr[t >> 5] = c;
+  __syncthreads();
+  uint8_t* o = out + (size_t)img * stride + offs[blockIdx.x];
+  for (uint32_t i = t; i < L; i += kT) o[4 + i] = c0[i];
+  if (t == 0) {
+    uint32_t x = 0;
+    for (int w = 0; w < kT / 32; ++w) x ^= xr[w];
+    put_be32(o, d);
+    put_be32(o + 8 + d, ~x);
+  }
+}
+
+PngGeom png_geom(int n, int H, int W) {
+  PngGeom g{};
+  g.n = n; g.H = H; g.W = W;
+  g.RS = 3 * W + 1;
+  g.R = kMaxStripBytes / g.RS;
+  if (g.R > 8) g.R = 8;
+  if (g.R < 1) g.R = 1;
+  g.nstrips = (H + g.R - 1) / g.R;
+  const int S = g.R * g.RS;
+  g.cap = ((S + 16 + 15) & ~15) + 16;
+  g.G = (S + kT - 1) / kT;
+  const int raw = ((g.R + 2) * 3 * W + 15) & ~15, tok = (kT * g.G * 2 + 15) & ~15;
+  g.off_filt = raw > tok ? raw : tok;
+  g.off_ow = g.off_filt + (((g.R + 1) * g.RS + 15) & ~15);
+  g.off_tab = g.off_ow + ((S + 32) & ~15) + 16;
+  g.smem = g.off_tab + (int)((sizeof(StripTables) + 15) & ~size_t(15));
+  return g;
+}
+
+}  // namespace
+
+size_t png_bound(int H, int W) {
+  if (H <= 0 || W <= 0) return 0;
+  const PngGeom g = png_geom(1, H, W);
+  return 45 + (size_t)g.nstrips * (12 + (size_t)g.cap);
+}
+
+size_t png_workspace(int n, int H, int W) {
+  const PngGeom g = png_geom(n, H, W);
+  const size_t ns = (size_t)n * g.nstrips;
+  return ns * g.cap + ns * sizeof(StripMeta) + ns * 4 + 256;
+}
+
+cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* out, long long stride,
+                              uint32_t* sizes, uint8_t* work, cudaStream_t s) {
+  if (n <= 0 || H <= 0 || W <= 0 || W > 8192 || H > 65535 || (size_t)stride < png_bound(H, W)) return cudaErrorInvalidValue;
+  const PngGeom g = png_geom(n, H, W);
+  static int attr_set = 0;
+  if (attr_set < g.smem) {
+    cudaError_t e = cudaFuncSetAttribute(png_strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(png_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.cap + 32);
+    if (e != cudaSuccess) return e;
+    attr_set = g.smem;
+  }
+  const size_t ns = (size_t)n * g.nstrips;
+  uint8_t* scratch = work;
+  StripMeta* meta = reinterpret_cast<StripMeta*>(work + ns * g.cap);
+  uint32_t* offs = reinterpret_cast<uint32_t*>(meta + ns);
+  png_strip_kernel<<<(unsigned)ns, kT, g.smem, s>>>(rgb, g, scratch, meta);
+  png_image_kernel<<<n, kT, 0, s>>>(g, scratch, meta, offs, out, stride, sizes);
+  png_chunk_kernel<<<(unsigned)ns, kT, g.cap + 32, s>>>(g, scratch, meta, offs, out, stride);
+  return cudaGetLastError();
+}
+
+}  // namespace lbx
