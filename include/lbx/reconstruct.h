@@ -118,6 +118,12 @@ lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint
  * (stored where smaller); lossless: any PNG decoder returns rgb exactly.  w <= 8192, h <= 65535.
  * Asynchronous on `stream`. */
 size_t lbx_png_bound(uint32_t h, uint32_t w);
+/* lbx_reconstruct with the return path on the GPU: host blobs -> unpack -> decode -> PNG encode ->
+ * only the PNG bytes cross PCIe.  PNG i is written at png_host + (png_sizes[0] + ... + png_sizes[i-1])
+ * and its length to png_sizes[i].  cap = bytes available at png_host; n * lbx_png_bound(8*latent_h,
+ * 8*latent_w) always suffices; if the PNGs need more, LBX_E_CONFIG (sizes still returned). */
+lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                               uint8_t* png_host, size_t cap, size_t* png_sizes, lbx_stream stream);
 lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
                                  size_t stride, uint32_t* sizes_dev, lbx_stream stream);
 

@@ -29,7 +29,7 @@ SYMBOLS = [
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
     "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
-    "lbx_png_bound", "lbx_png_encode_device",
+    "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png",
 ]
 
 
@@ -113,6 +113,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_png_bound.argtypes = [u32, u32]
     L.lbx_png_bound.restype = ctypes.c_size_t
     L.lbx_png_encode_device.argtypes = [vp, u32, u32, u32, vp, ctypes.c_size_t, vp, vp]
+    L.lbx_reconstruct_png.argtypes = [vp, vp, vp, u32, vp, ctypes.c_size_t, vp, vp]
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error", "lbx_pack_bound", "lbx_png_bound"):
             getattr(L, name).restype = ctypes.c_int
@@ -217,6 +218,23 @@ class Decoder:
         arr, sizes, keep = _blob_arrays(blobs)
         check(lib().lbx_reconstruct(self._h, arr, sizes, n, out.ctypes.data, stream or None))
         return out
+
+    def reconstruct_png(self, blobs, out: np.ndarray | None = None, stream: int = 0, copy: bool = True) -> list:
+        """lbx_reconstruct_png: LBLP blobs -> PNG files, encoded on the GPU.  Returns bytes objects, or
+        (copy=False) uint8 views into `out`."""
+        n = len(blobs)
+        h, w = self.out_hw
+        if out is None:
+            out = np.empty(n * png_bound(h, w), np.uint8)
+        arr, sizes, keep = _blob_arrays(blobs)
+        psz = (ctypes.c_size_t * max(n, 1))()
+        check(lib().lbx_reconstruct_png(self._h, arr, sizes, n, out.ctypes.data, out.nbytes, psz, stream or None))
+        res, off = [], 0
+        for i in range(n):
+            v = out[off:off + psz[i]]
+            res.append(v.tobytes() if copy else v)
+            off += psz[i]
+        return res
 
     def reconstruct_latents(self, latents: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """fp16 NCHW latents (host) -> uint8 RGB (n, 8h, 8w, 3)."""

@@ -108,6 +108,12 @@ class Decoder {
   unsigned long long* offs_host = nullptr;  // pinned [max_batch] offsets + sizes
   int* err_host = nullptr;
 
+  // return path (lbx_reconstruct_png), allocated on first use
+  uint8_t* png_dev = nullptr;    // max_batch PNGs back to back
+  uint8_t* png_work = nullptr;   // png_workspace(max_batch)
+  uint32_t* png_sizes = nullptr;
+  uint32_t* png_sizes_host = nullptr;  // pinned
+
   std::map<std::tuple<int, const void*, const void*>, cudaGraphExec_t> graphs;
   std::map<int, int> launch_counts;
   struct ProfRec {
@@ -130,6 +136,12 @@ class Decoder {
     if (blob_dev) cudaFree(blob_dev);
     if (blob_host) cudaFreeHost(blob_host);
     if (offs_host) cudaFreeHost(offs_host);
+    if (png_dev) cudaFree(png_dev);
+    if (png_work) cudaFree(png_work);
+    if (png_sizes) cudaFree(png_sizes);
+    if (png_sizes_host) cudaFreeHost(png_sizes_host);
+    png_dev = png_work = nullptr;
+    png_sizes = png_sizes_host = nullptr;
     if (stream) cudaStreamDestroy(stream);
     wblock = arena = nullptr;
     blob_dev = blob_host = nullptr;
@@ -859,6 +871,49 @@ lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, cons
   lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
   if (st != LBX_OK) return st;
   return finish_reconstruct(d, n, nullptr, s, rgb_hosts);
+}
+
+lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                               uint8_t* png_host, size_t cap, size_t* png_sizes, lbx_stream stream) {
+  if (!dec || !png_host || !png_sizes) return set_err(LBX_E_CONFIG, "lbx_reconstruct_png: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0) return LBX_OK;
+  if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
+  cudaSetDevice(d.desc.device);
+  cudaStream_t s = pick(dec, stream);
+  const int H = 8 * d.h, W = 8 * d.w;
+  if (!d.png_dev) {
+    const size_t out_bytes = (size_t)d.max_batch * lbx::png_bound(H, W);
+    if (cudaMalloc(&d.png_dev, out_bytes) != cudaSuccess ||
+        cudaMalloc(&d.png_work, lbx::png_workspace(d.max_batch, H, W)) != cudaSuccess ||
+        cudaMalloc(&d.png_sizes, 4 * (size_t)d.max_batch) != cudaSuccess ||
+        cudaMallocHost(&d.png_sizes_host, 4 * (size_t)d.max_batch) != cudaSuccess)
+      return set_err(LBX_E_CUDA, "lbx_reconstruct_png: PNG buffers");
+  }
+  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  if (st != LBX_OK) return st;
+  if ((st = d.run((int)n, d.lat, d.rgb, s)) != LBX_OK) return st;
+  cudaError_t e = lbx::launch_png_encode(d.rgb, (int)n, H, W, d.png_dev, 0, d.png_sizes, d.png_work, s, true);
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("lbx_reconstruct_png: ") + cudaGetErrorString(e));
+  if (cudaMemcpyAsync(d.png_sizes_host, d.png_sizes, 4 * (size_t)n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemcpyAsync(d.err_host, d.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "D2H of PNG sizes failed");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return set_err(LBX_E_CUDA, std::string("reconstruct_png: ") + cudaGetErrorString(e));
+  if (*d.err_host) {
+    cudaMemset(d.err, 0, 4);
+    return set_err(LBX_E_FORMAT, "device unpack reported a malformed blob (code " + std::to_string(*d.err_host) + ")");
+  }
+  size_t total = 0;
+  for (uint32_t i = 0; i < n; ++i) total += (png_sizes[i] = d.png_sizes_host[i]);
+  if (total > cap)
+    return set_err(LBX_E_CONFIG, "cap: the PNGs need " + std::to_string(total) + " bytes (sizes returned)");
+  if (cudaMemcpyAsync(png_host, d.png_dev, total, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return set_err(LBX_E_CUDA, "D2H of PNGs failed");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess)
+    return set_err(LBX_E_CUDA, std::string("reconstruct_png: ") + cudaGetErrorString(e));
+  return LBX_OK;
 }
 
 lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,

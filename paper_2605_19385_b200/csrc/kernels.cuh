@@ -73,10 +73,12 @@ cudaError_t launch_lblp_pack(const uint16_t* x, int n, int C, int H, int W, uint
                              uint32_t* sizes, uint8_t* widths_tmp, uint32_t* row_bytes_tmp, cudaStream_t s);
 
 // PNG encode (csrc/png.cu) of n uint8 RGB images [n][H][W][3] into out + i*stride (stride >=
-// png_bound(H, W)); sizes[i] = PNG bytes.  `work` >= png_workspace(n, H, W) bytes of device scratch.
+// png_bound(H, W)) or, when `contiguous`, back to back from out (image i at the sum of the earlier
+// sizes; out must hold n * png_bound); sizes[i] = PNG bytes.  `work` >= png_workspace(n, H, W)
+// bytes of device scratch.
 size_t png_bound(int H, int W);
 size_t png_workspace(int n, int H, int W);
 cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* out, long long stride,
-                              uint32_t* sizes, uint8_t* work, cudaStream_t s);
+                              uint32_t* sizes, uint8_t* work, cudaStream_t s, bool contiguous = false);
 
 }  // namespace lbx

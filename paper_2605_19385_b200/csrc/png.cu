@@ -14,8 +14,8 @@
 //                          (256 independent segments, greedy, distances {1, 3, 6, row}), Huffman
 //                          code construction (length-limited 15 / 7), bit packing through
 //                          per-thread offsets from a block scan; Adler-32 partials of the strip.
-//   K-b png_image_kernel   one CTA per image: Adler-32 combine, chunk offsets (scan), signature,
-//                          IHDR, IEND, total size.
+//   K-b png_image_kernel   one CTA per image: Adler-32 combine, chunk offsets (scan), total size.
+//   K-b2 png_frame_kernel  image bases (strided, or packed back to back), signature, IHDR, IEND.
 //   K-c png_chunk_kernel   one CTA per strip: copy the strip's data to its chunk and CRC-32 it
 //                          (per-thread segments combined by multiplication by x^(8n) mod P).
 #include <cuda_runtime.h>
@@ -46,8 +46,10 @@ struct PngGeom {
   int nstrips;  // strips per image
   int cap;      // scratch bytes per strip
   int G;        // parse segment bytes per thread
-  // dynamic smem layout (bytes): tokens alias the raw rows (dead after filtering)
-  int off_filt, off_ow, off_tab, smem;
+  int MC;       // LZ77 matches kept per parse segment
+  // dynamic smem layout (bytes): raw rows, then Huffman work arrays, then the output words share
+  // offset 0 (each dead before the next); filtered rows, match lists and tables follow
+  int off_filt, off_ml, off_tab, smem;
 };
 
 __host__ __device__ inline int strip_rows(const PngGeom& g, int s) {
@@ -75,76 +77,101 @@ __device__ __forceinline__ void dist_sym(int d, int& code, int& nb, int& ev) {
 __device__ __forceinline__ uint32_t rev_bits(uint32_t c, int n) { return __brev(c) >> (32 - n); }
 
 // --------------------------------------------------------------------------- Huffman construction
-// Single-thread: code lengths (<= L) for `n` symbols with frequencies `freq`, given `order` = the
-// m used symbols sorted by (freq, symbol) ascending.  Two-queue Huffman over the sorted leaves, then
-// the Kraft repair that moves overlong codes to L and splits shorter ones, then lengths handed
-// out longest-first to the least frequent symbols.  Fewer than two used symbols get dummies so
-// every code is complete (zlib's inflate rejects incomplete code-length codes).
+// The literal/length (286 symbols) and distance (30) codes are built in phases spread over the CTA,
+// so that only the inherently sequential part -- the two-queue merge of the rank-sorted leaves and
+// the depths of the m-1 internal nodes -- runs on a single thread (a different warp per alphabet):
+//   rank sort (all threads) -> merge (1 thread per alphabet) -> leaf depths and per-length counts
+//   (all) -> Kraft repair of the counts to <= 15 bits (1 thread) -> lengths by frequency rank and
+//   canonical codes (all).
+// Fewer than two used symbols get a dummy second code so every code is complete (zlib's inflate
+// rejects incomplete codes other than a single distance code).
+template <int N>
+struct Alpha {
+  uint32_t wl[N];  // leaf weights in rank order
+  uint32_t wi[N];  // internal node weights
+  uint16_t pl[N];  // parent (internal index) of each leaf
+  uint16_t pi[N];  // parent of each internal node
+  uint8_t di[N];   // internal node depth (saturating)
+};
 struct HuffWork {
-  uint32_t w[320];
-  uint16_t par[640];
-  uint8_t depth[640];
+  Alpha<286> lit;
+  Alpha<30> dst;
 };
 
-__device__ void huff_lengths(const uint32_t* freq, int n, uint16_t* order, int m, int L, uint8_t* lens,
-                             HuffWork& hw) {
-  for (int i = 0; i < n; ++i) lens[i] = 0;
-  if (m < 2) {
-    const int a = m == 1 ? order[0] : 0;
-    lens[a] = 1;
-    lens[a == 0 ? 1 : 0] = 1;
-    return;
-  }
-  // leaves 0..m-1, internal nodes m..2m-2; weights of internal nodes in hw.w
+__device__ void huff_merge(const uint32_t* wl, uint32_t* wi, uint16_t* pl, uint16_t* pi, uint8_t* di, int m) {
   int li = 0, ii = 0, ni = 0;
-  auto take = [&](uint32_t& wt) -> int {
-    if (li < m && (ii >= ni || freq[order[li]] <= hw.w[ii])) { wt = freq[order[li]]; return li++; }
-    wt = hw.w[ii];
-    return m + ii++;
-  };
+  uint32_t hl = wl[0], hi = 0;  // queue heads
   for (int k = 0; k < m - 1; ++k) {
-    uint32_t wa, wb;
-    const int a = take(wa), b = take(wb);
-    hw.w[ni] = wa + wb;
-    hw.par[a] = (uint16_t)(m + ni);
-    hw.par[b] = (uint16_t)(m + ni);
-    ++ni;
+    uint32_t w2 = 0;
+#pragma unroll
+    for (int pick = 0; pick < 2; ++pick) {
+      if (li < m && (ii >= ni || hl <= hi)) {
+        w2 += hl;
+        pl[li++] = (uint16_t)ni;
+        hl = li < m ? wl[li] : 0u;
+      } else {
+        w2 += hi;
+        pi[ii++] = (uint16_t)ni;
+        hi = ii < ni ? wi[ii] : 0u;
+      }
+    }
+    wi[ni++] = w2;
+    if (ii == ni - 1) hi = w2;
   }
-  const int root = m + ni - 1;
-  hw.depth[root] = 0;
-  int cnt[33];
-  for (int i = 0; i <= 32; ++i) cnt[i] = 0;
-  for (int v = root - 1; v >= 0; --v) {
-    const int d = hw.depth[hw.par[v]] + 1;
-    hw.depth[v] = (uint8_t)(d > 32 ? 32 : d);
-    if (v < m) ++cnt[d > L ? L : d];
+  di[ni - 1] = 0;  // root; parents have larger indices
+  for (int j = ni - 2; j >= 0; --j) {
+    const int d = di[pi[j]] + 1;
+    di[j] = (uint8_t)(d > 255 ? 255 : d);
   }
+}
+
+// Kraft repair of per-length counts (cnt[1..L], overlong codes already counted at L), then the
+// canonical first code of every length (RFC 1951 3.2.2)
+__device__ void huff_repair(uint32_t* cnt, uint32_t* next, int L) {
   uint32_t total = 0;
-  for (int i = 1; i <= L; ++i) total += (uint32_t)cnt[i] << (L - i);
+  for (int i = 1; i <= L; ++i) total += cnt[i] << (L - i);
   while (total > (1u << L)) {
     --cnt[L];
     for (int i = L - 1; i > 0; --i)
       if (cnt[i]) { --cnt[i]; cnt[i + 1] += 2; break; }
     --total;
   }
-  int idx = 0;
-  for (int len = L; len >= 1; --len)
-    for (int c = 0; c < cnt[len]; ++c) lens[order[idx++]] = (uint8_t)len;
-}
-
-// canonical codes (RFC 1951 3.2.2), stored bit-reversed for the LSB-first bit stream
-__device__ void huff_codes(const uint8_t* lens, int n, uint16_t* codes) {
-  int cnt[16] = {0};
-  for (int i = 0; i < n; ++i) ++cnt[lens[i]];
-  cnt[0] = 0;
-  int next[16];
-  int code = 0;
-  for (int b = 1; b < 16; ++b) {
-    code = (code + cnt[b - 1]) << 1;
+  uint32_t code = 0;
+  next[0] = 0;
+  for (int b = 1; b <= L; ++b) {
+    code = (code + (b > 1 ? cnt[b - 1] : 0u)) << 1;
     next[b] = code;
   }
-  for (int i = 0; i < n; ++i)
-    codes[i] = lens[i] ? (uint16_t)rev_bits((uint32_t)next[lens[i]]++, lens[i]) : (uint16_t)0;
+}
+
+// small alphabets (the 19 code-length symbols): all on one thread
+__device__ void huff_small(const uint32_t* freq, int n, const uint16_t* order, int m, int L, uint8_t* lens,
+                           uint16_t* codes) {
+  uint32_t w[20], wi[20];
+  uint16_t pl[20], pi[20];
+  uint8_t di[20];
+  for (int i = 0; i < n; ++i) lens[i] = 0;
+  uint32_t cnt[16] = {0}, next[16];
+  if (m < 2) {
+    const int a = m == 1 ? order[0] : 0;
+    lens[a] = 1;
+    lens[a == 0 ? 1 : 0] = 1;
+    cnt[1] = 2;
+  } else {
+    for (int i = 0; i < m; ++i) w[i] = freq[order[i]];
+    huff_merge(w, wi, pl, pi, di, m);
+    for (int i = 0; i < m; ++i) {
+      const int d = di[pl[i]] + 1;
+      ++cnt[d > L ? L : d];
+    }
+  }
+  huff_repair(cnt, next, L);
+  if (m >= 2) {
+    int r = 0;
+    for (int len = L; len >= 1; --len)
+      for (uint32_t c = 0; c < cnt[len]; ++c) lens[order[r++]] = (uint8_t)len;
+  }
+  for (int i = 0; i < n; ++i) codes[i] = lens[i] ? (uint16_t)rev_bits(next[lens[i]]++, lens[i]) : (uint16_t)0;
 }
 
 // LSB-first bit writer into a zeroed word buffer (words shared with neighbours: atomicOr)
@@ -219,7 +246,9 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t* red, ui
 struct StripTables {
   uint32_t lfreq[286 + 30];  // literal/length then distance frequencies
   uint32_t cfreq[19];
-  uint16_t order[320];
+  uint32_t cnt[2][16];       // code lengths per length (literal/length, distance)
+  uint32_t next[2][16];      // canonical first code per length
+  uint16_t order[320];       // used symbols by (freq, symbol): literal/length at 0, distance at 286
   uint16_t corder[19];
   uint8_t llen[286 + 30];
   uint8_t clen[19];
@@ -228,11 +257,13 @@ struct StripTables {
   uint16_t rle[320];   // code-length RLE symbols (sym | extra << 5)
   uint32_t red[kT / 32];
   uint32_t scal[8];    // 0 nrle, 1 hlit, 2 hdist, 3 hclen, 4 header bits, 5 m_lit, 6 m_dist
-  uint16_t ntok[kT];
-  HuffWork hw;
+  uint8_t nmatch[kT];
   unsigned long long ab[2][kT / 32];
   uint32_t fsum[5][kT / 32];
 };
+
+// short match distances (1, 3, 6 bytes back); the fourth candidate is the row above (RS)
+__device__ __forceinline__ int short_dist(int di) { return di == 0 ? 1 : di == 1 ? 3 : 6; }
 
 __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict__ rgb, PngGeom g,
                                                        uint8_t* __restrict__ scratch, StripMeta* __restrict__ meta) {
@@ -243,10 +274,11 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   const int rb = 3 * g.W, RS = g.RS;
   const int S = rows * RS;
   const bool first = s == 0, last = s == g.nstrips - 1;
-  uint8_t* raw = sm;                       // rows y0-2 .. y0+rows-1 (3W bytes each)
-  uint16_t* tok = reinterpret_cast<uint16_t*>(sm);  // LZ77 tokens, once the raw rows are filtered
-  uint8_t* filt = sm + g.off_filt;         // row y0-1 then the strip's rows (RS bytes each)
-  uint32_t* ow = reinterpret_cast<uint32_t*>(sm + g.off_ow);  // the strip's zlib bytes
+  uint8_t* raw = sm;                        // rows y0-2 .. y0+rows-1 (3W bytes each), until filtered
+  HuffWork& hw = *reinterpret_cast<HuffWork*>(sm);   // then the Huffman work arrays
+  uint32_t* ow = reinterpret_cast<uint32_t*>(sm);    // then the strip's zlib bytes
+  uint8_t* filt = sm + g.off_filt;          // row y0-1 then the strip's rows (RS bytes each)
+  uint32_t* mlist = reinterpret_cast<uint32_t*>(sm + g.off_ml);  // per-thread LZ77 matches
   StripTables& T = *reinterpret_cast<StripTables*>(sm + g.off_tab);
 
   // ---- 1. raw rows into smem (rows before the image are zero)
@@ -268,6 +300,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   }
   for (int i = t; i < 286 + 30; i += kT) T.lfreq[i] = 0;
   if (t < 19) T.cfreq[t] = 0;
+  if (t < 32) { T.cnt[t >> 4][t & 15] = 0; }
   __syncthreads();
 
   // ---- 2. filter rows y0-1 (history, when it exists) .. y0+rows-1
@@ -326,48 +359,64 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     if (lane == 0) { T.ab[0][wid] = a; T.ab[1][wid] = b; }
   }
 
-  // ---- 4. LZ77 parse: thread t owns [t*G, min((t+1)*G, S)), greedy, matches end inside it
-  const int dists[4] = {1, 3, 6, RS};
+  // ---- 4. LZ77 parse: thread t > 0 owns [(t-1)*G, t*G) of the strip, greedy, matches end inside it and
+  // at most MC per segment.  The bytes 1..6 before p sit in a register window, so a literal costs
+  // two shared loads (f[p], f[p - RS]); only a first-byte hit runs the extension loop.
   const int lo = y0 > 0 ? -RS : 0;
-  int nt = 0;
+  // (thread 0 has no segment: it builds the block header while the others count their bits)
+  const int p0 = t ? min((t - 1) * g.G, S) : S, p1 = t ? min(p0 + g.G, S) : S;
+  uint32_t* ml = mlist + t * g.MC;
   {
-    const int p0 = t * g.G, p1 = min(p0 + g.G, S);
-    uint16_t* tk = tok + t * g.G;
+    auto window = [&](int p) -> uint64_t {
+      uint64_t w = 0;
+#pragma unroll
+      for (int k = 1; k <= 6; ++k)
+        if (p - k >= lo) w |= (uint64_t)f[p - k] << (8 * (k - 1));
+      return w;
+    };
+    int nm = 0;
+    uint64_t back = window(p0);
     for (int p = p0; p < p1;) {
+      const int x = f[p];
       const int maxl = min(258, p1 - p);
       int bl = 0, bd = 0;
-      if (maxl >= 3) {
+      if (maxl >= 3 && nm < g.MC) {
 #pragma unroll
         for (int di = 0; di < 4; ++di) {
-          const int d = dists[di];
+          const int d = di < 3 ? short_dist(di) : RS;
           if (p - d < lo) continue;
-          int l = 0;
+          const int y = di < 3 ? (int)((back >> (8 * (d - 1))) & 255u) : f[p - d];
+          if (y != x) continue;
+          int l = 1;
           while (l < maxl && f[p + l] == f[p + l - d]) ++l;
           if (l > bl) { bl = l; bd = di; }
         }
       }
       if (bl >= 3) {
-        tk[nt++] = (uint16_t)(0x8000u | (bd << 8) | (bl - 3));
+        ml[nm++] = (uint32_t)(p - p0) << 16 | (uint32_t)bd << 8 | (uint32_t)(bl - 3);
         int c, nb, ev;
         len_sym(bl, c, nb, ev);
         atomicAdd(&T.lfreq[c], 1u);
-        dist_sym(dists[bd], c, nb, ev);
+        dist_sym(bd < 3 ? short_dist(bd) : RS, c, nb, ev);
         atomicAdd(&T.lfreq[286 + c], 1u);
         p += bl;
+        back = window(p);
       } else {
-        tk[nt++] = f[p];
-        atomicAdd(&T.lfreq[f[p]], 1u);
+        atomicAdd(&T.lfreq[x], 1u);
+        back = ((back << 8) | (uint64_t)x) & 0xFFFFFFFFFFFFull;
         ++p;
       }
     }
-    T.ntok[t] = (uint16_t)nt;
+    T.nmatch[t] = (uint8_t)nm;
   }
   __syncthreads();
   if (t == 0) T.lfreq[256] = 1;  // end of block
   __syncthreads();
 
-  // ---- 5. sort the used literal/length and distance symbols by (freq, symbol): rank by counting
+  // ---- 5. rank sort of the used symbols by (freq, symbol); zero the lengths
+  uint32_t ml_cnt = 0, md_cnt = 0;
   for (int sym = t; sym < 286 + 30; sym += kT) {
+    T.llen[sym] = 0;
     const uint32_t fs = T.lfreq[sym];
     if (!fs) continue;
     const int b0 = sym < 286 ? 0 : 286, b1 = sym < 286 ? 286 : 316;
@@ -376,30 +425,73 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
       const uint32_t fu = T.lfreq[u];
       rank += fu && (fu < fs || (fu == fs && u < sym));
     }
-    T.order[b0 + rank] = (uint16_t)sym;
+    T.order[b0 + rank] = (uint16_t)(sym - b0);
+    if (sym < 286) ++ml_cnt; else ++md_cnt;
   }
-  {
-    uint32_t ml = 0, md = 0;
-    for (int sym = t; sym < 286 + 30; sym += kT)
-      if (T.lfreq[sym]) { if (sym < 286) ++ml; else ++md; }
-    ml = block_sum_u32(ml, T.red);
-    md = block_sum_u32(md, T.red);
-    if (t == 0) { T.scal[5] = ml; T.scal[6] = md; }
-  }
+  const int m_l = (int)block_sum_u32(ml_cnt, T.red);
+  const int m_d = (int)block_sum_u32(md_cnt, T.red);
+  for (int r = t; r < m_l; r += kT) hw.lit.wl[r] = T.lfreq[T.order[r]];
+  if (t < m_d) hw.dst.wl[t] = T.lfreq[286 + T.order[286 + t]];
   __syncthreads();
 
-  // ---- 6. codes and the block header (thread 0)
-  if (t == 0) {
-    const int ml = (int)T.scal[5], md = (int)T.scal[6];
-    for (int i = 0; i < md; ++i) T.order[286 + i] -= 286;  // distance symbols relative to 0
-    huff_lengths(T.lfreq, 286, T.order, ml, 15, T.llen, T.hw);
-    huff_lengths(T.lfreq + 286, 30, T.order + 286, md, 15, T.llen + 286, T.hw);
-    huff_codes(T.llen, 286, T.lcode);
-    huff_codes(T.llen + 286, 30, T.lcode + 286);
+  // ---- 6. code lengths and codes
+  if (t == 0 && m_l >= 2) huff_merge(hw.lit.wl, hw.lit.wi, hw.lit.pl, hw.lit.pi, hw.lit.di, m_l);
+  if (t == 32 && m_d >= 2) huff_merge(hw.dst.wl, hw.dst.wi, hw.dst.pl, hw.dst.pi, hw.dst.di, m_d);
+  __syncthreads();
+  for (int r = t; r < m_l; r += kT) {
+    const int d = hw.lit.di[hw.lit.pl[r]] + 1;
+    atomicAdd(&T.cnt[0][d > 15 ? 15 : d], 1u);
+  }
+  if (t < m_d && m_d >= 2) {
+    const int d = hw.dst.di[hw.dst.pl[t]] + 1;
+    atomicAdd(&T.cnt[1][d > 15 ? 15 : d], 1u);
+  }
+  __syncthreads();
+  if (t == 0 || t == 32) {
+    const int k = t ? 1 : 0, m = k ? m_d : m_l;
+    if (m < 2) {  // dummy second code (only the distance alphabet can get here)
+      const int a = m == 1 ? T.order[286 * k] : 0;
+      T.llen[286 * k + a] = 1;
+      T.llen[286 * k + (a == 0 ? 1 : 0)] = 1;
+      T.cnt[k][1] = 2;
+    }
+    huff_repair(T.cnt[k], T.next[k], 15);
+  }
+  __syncthreads();
+  // lengths by rank: the least frequent symbols take the longest lengths
+  for (int i = t; i < 316; i += kT) {
+    const int k = i < 286 ? 0 : 1, r = i - 286 * k, m = k ? m_d : m_l;
+    if (m < 2 || r >= m) continue;
+    uint32_t acc = 0;
+    for (int len = 15; len >= 1; --len) {
+      acc += T.cnt[k][len];
+      if ((uint32_t)r < acc) { T.llen[286 * k + T.order[286 * k + r]] = (uint8_t)len; break; }
+    }
+  }
+  __syncthreads();
+  // canonical codes: next[len] + the number of lower symbols with the same length
+  for (int i = t; i < 316; i += kT) {
+    const int k = i < 286 ? 0 : 1, b0 = 286 * k;
+    const int len = T.llen[i];
+    uint16_t code = 0;
+    if (len) {
+      uint32_t c = T.next[k][len];
+      for (int u = b0; u < i; ++u) c += T.llen[u] == len;
+      code = (uint16_t)rev_bits(c, len);
+    }
+    T.lcode[i] = code;
+  }
+  __syncthreads();
+  // ---- 7. block header (thread 0) || token bits (the rest); offsets; dynamic vs stored
+  int dcs[4], dns[4], dvs[4];
+#pragma unroll
+  for (int di = 0; di < 4; ++di) dist_sym(di < 3 ? short_dist(di) : RS, dcs[di], dns[di], dvs[di]);
+  const int nm = T.nmatch[t];
+  uint32_t mybits = 0;
+  if (t == 0) {  // header: run-length coded code lengths (RFC 1951 3.2.7) and their own code
     int hlit = 286, hdist = 30;
     while (hlit > 257 && !T.llen[hlit - 1]) --hlit;
     while (hdist > 1 && !T.llen[286 + hdist - 1]) --hdist;
-    // run-length code the hlit + hdist code lengths (RFC 1951 3.2.7)
     const int nl = hlit + hdist;
     auto seq = [&](int i) -> int { return i < hlit ? T.llen[i] : T.llen[286 + i - hlit]; };
     int nr = 0;
@@ -428,8 +520,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
         while (j > 0 && (T.cfreq[T.corder[j - 1]] > T.cfreq[sym])) { T.corder[j] = T.corder[j - 1]; --j; }
         T.corder[j] = (uint16_t)sym;
       }
-    huff_lengths(T.cfreq, 19, T.corder, mc, 7, T.clen, T.hw);
-    huff_codes(T.clen, 19, T.ccode);
+    huff_small(T.cfreq, 19, T.corder, mc, 7, T.clen, T.ccode);
     const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
     int hclen = 19;
     while (hclen > 4 && !T.clen[kOrd[hclen - 1]]) --hclen;
@@ -440,24 +531,24 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     }
     T.scal[0] = (uint32_t)nr; T.scal[1] = (uint32_t)hlit; T.scal[2] = (uint32_t)hdist;
     T.scal[3] = (uint32_t)hclen; T.scal[4] = bits;
+  } else {
+    int mi = 0, mp = nm ? (int)(ml[0] >> 16) + p0 : p1;
+    for (int p = p0; p < p1;) {
+      if (p == mp) {
+        const uint32_t v = ml[mi];
+        const int len = (int)(v & 255) + 3, di = (int)(v >> 8) & 3;
+        int c, nb, ev;
+        len_sym(len, c, nb, ev);
+        mybits += T.llen[c] + nb + T.llen[286 + dcs[di]] + dns[di];
+        p += len;
+        ++mi;
+        mp = mi < nm ? (int)(ml[mi] >> 16) + p0 : p1;
+      } else {
+        mybits += T.llen[f[p]];
+        ++p;
+      }
+    }
   }
-  __syncthreads();
-
-  // ---- 7. token bits, offsets, dynamic vs stored
-  const int dcode[4] = {0, 2, 4, 0};
-  int dc3, dnb3, dev3;
-  dist_sym(RS, dc3, dnb3, dev3);
-  auto tok_bits = [&](uint16_t v) -> uint32_t {
-    if (!(v & 0x8000u)) return T.llen[v];
-    int c, nb, ev;
-    len_sym((v & 255) + 3, c, nb, ev);
-    const int di = (v >> 8) & 3;
-    const int dc = di == 3 ? dc3 : dcode[di], dnb = di == 3 ? dnb3 : (di == 2 ? 1 : 0);
-    return T.llen[c] + nb + T.llen[286 + dc] + dnb;
-  };
-  uint32_t mybits = 0;
-  const uint16_t* tk = tok + t * g.G;
-  for (int k = 0; k < nt; ++k) mybits += tok_bits(tk[k]);
   uint32_t tbits;
   const uint32_t myoff = block_scan_u32(mybits, T.red, &tbits);
   const uint32_t pre = first ? 16u : 0u;  // zlib header
@@ -467,8 +558,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   const bool dyn = dyn_bytes < sto_bytes;
   const uint32_t bytes = dyn ? dyn_bytes : sto_bytes;
   const int nw = (int)(bytes + 3) / 4 + 1;
-  __syncthreads();
-  for (int i = t; i < nw; i += kT) ow[i] = 0;
+  for (int i = t; i < nw; i += kT) ow[i] = 0;  // the Huffman work arrays are dead
   __syncthreads();
 
   // ---- 8. write
@@ -494,20 +584,24 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     }
     {
       BitW w(ow, pre + T.scal[4] + myoff);
-      for (int k = 0; k < nt; ++k) {
-        const uint16_t v = tk[k];
-        if (!(v & 0x8000u)) {
-          w.put(T.lcode[v], T.llen[v]);
-        } else {
+      int mi = 0, mp = nm ? (int)(ml[0] >> 16) + p0 : p1;
+      for (int p = p0; p < p1;) {
+        if (p == mp) {
+          const uint32_t v = ml[mi];
+          const int len = (int)(v & 255) + 3, di = (int)(v >> 8) & 3;
           int c, nb, ev;
-          len_sym((v & 255) + 3, c, nb, ev);
+          len_sym(len, c, nb, ev);
           w.put(T.lcode[c], T.llen[c]);
           if (nb) w.put((uint32_t)ev, nb);
-          const int di = (v >> 8) & 3;
-          const int d = di == 0 ? 1 : di == 1 ? 3 : di == 2 ? 6 : RS;
-          dist_sym(d, c, nb, ev);
-          w.put(T.lcode[286 + c], T.llen[286 + c]);
-          if (nb) w.put((uint32_t)ev, nb);
+          w.put(T.lcode[286 + dcs[di]], T.llen[286 + dcs[di]]);
+          if (dns[di]) w.put((uint32_t)dvs[di], dns[di]);
+          p += len;
+          ++mi;
+          mp = mi < nm ? (int)(ml[mi] >> 16) + p0 : p1;
+        } else {
+          const int x = f[p];
+          w.put(T.lcode[x], T.llen[x]);
+          ++p;
         }
       }
       w.flush();
@@ -596,12 +690,9 @@ __device__ __forceinline__ void put_be32(uint8_t* p, uint32_t v) {
 // --------------------------------------------------------------------------- K-b: per image
 __global__ void __launch_bounds__(kT) png_image_kernel(PngGeom g, uint8_t* __restrict__ scratch,
                                                        const StripMeta* __restrict__ meta, uint32_t* __restrict__ offs,
-                                                       uint8_t* __restrict__ out, long long stride,
                                                        uint32_t* __restrict__ sizes) {
-  __shared__ uint32_t tab[256];
   __shared__ uint32_t red[kT / 32];
   __shared__ unsigned long long ared[2][kT / 32];
-  crc_table(tab);
   const int img = blockIdx.x, t = threadIdx.x, ns = g.nstrips;
   const StripMeta* mi = meta + (size_t)img * ns;
   const unsigned long long N = (unsigned long long)g.H * g.RS;
@@ -630,33 +721,62 @@ __global__ void __launch_bounds__(kT) png_image_kernel(PngGeom g, uint8_t* __res
     offs[(size_t)img * ns + s] = off;
     off += 12u + mi[s].bytes;
   }
-  uint8_t* o = out + (size_t)img * stride;
   if (t == 0) {
     unsigned long long a = 1, b = N % kAdler;
     for (int w = 0; w < kT / 32; ++w) { a += ared[0][w]; b += ared[1][w]; }
     const uint32_t adler = (uint32_t)((b % kAdler) << 16 | (a % kAdler));
     put_be32(scratch + ((size_t)img * ns + ns - 1) * g.cap + mi[ns - 1].bytes - 4, adler);
+    sizes[img] = 33u + total + 12u;
+  }
+}
+
+// --------------------------------------------------------------------------- K-b2: image bases, frames
+// base[i] = i * stride, or (contiguous) the exclusive scan of the sizes; then the signature, IHDR
+// and IEND of every image
+__global__ void __launch_bounds__(kT) png_frame_kernel(PngGeom g, const uint32_t* __restrict__ sizes,
+                                                       unsigned long long* __restrict__ bases, uint8_t* __restrict__ out,
+                                                       long long stride, int contiguous) {
+  __shared__ uint32_t tab[256];
+  __shared__ unsigned long long part[kT];
+  crc_table(tab);
+  const int t = threadIdx.x, n = g.n;
+  const int per = (n + kT - 1) / kT, i0 = t * per;
+  unsigned long long sum = 0;
+  for (int i = i0; i < i0 + per && i < n; ++i) sum += sizes[i];
+  part[t] = sum;
+  __syncthreads();
+  if (t == 0) {  // n / kT partial sums: a serial scan is plenty
+    unsigned long long acc = 0;
+    for (int k = 0; k < kT; ++k) { const unsigned long long v = part[k]; part[k] = acc; acc += v; }
+  }
+  __syncthreads();
+  unsigned long long base = part[t];
+  for (int i = i0; i < i0 + per && i < n; ++i) {
+    const unsigned long long b = contiguous ? base : (unsigned long long)i * (unsigned long long)stride;
+    base += sizes[i];
+    bases[i] = b;
+    uint8_t* o = out + b;
     const uint8_t sig[8] = {0x89, 'P', 'N', 'G', 0x0D, 0x0A, 0x1A, 0x0A};
-    for (int i = 0; i < 8; ++i) o[i] = sig[i];
+    for (int k = 0; k < 8; ++k) o[k] = sig[k];
     uint8_t ih[17] = {'I', 'H', 'D', 'R'};
     put_be32(ih + 4, (uint32_t)g.W);
     put_be32(ih + 8, (uint32_t)g.H);
     ih[12] = 8; ih[13] = 2; ih[14] = 0; ih[15] = 0; ih[16] = 0;  // 8-bit RGB, deflate, adaptive, no interlace
     put_be32(o + 8, 13);
-    for (int i = 0; i < 17; ++i) o[12 + i] = ih[i];
+    for (int k = 0; k < 17; ++k) o[12 + k] = ih[k];
     put_be32(o + 29, ~crc_raw(tab, 0xFFFFFFFFu, ih, 17));
-    const uint32_t e = 33u + total;
     const uint8_t iend[12] = {0, 0, 0, 0, 'I', 'E', 'N', 'D', 0xAE, 0x42, 0x60, 0x82};
-    for (int i = 0; i < 12; ++i) o[e + i] = iend[i];
-    sizes[img] = e + 12u;
+    uint8_t* e = o + sizes[i] - 12;
+    for (int k = 0; k < 12; ++k) e[k] = iend[k];
   }
 }
 
 // --------------------------------------------------------------------------- K-c: per strip
 __global__ void __launch_bounds__(kT) png_chunk_kernel(PngGeom g, const uint8_t* __restrict__ scratch,
                                                        const StripMeta* __restrict__ meta,
-                                                       const uint32_t* __restrict__ offs, uint8_t* __restrict__ out,
-                                                       long long stride) {
+                                                       const uint32_t* __restrict__ offs,
+                                                       const unsigned long long* __restrict__ bases,
+                                                       uint8_t* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ uint32_t tab[256];
   __shared__ uint32_t xr[kT / 32];
@@ -678,7 +798,7 @@ __global__ void __launch_bounds__(kT) png_chunk_kernel(PngGeom g, const uint8_t*
   for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
   if ((t & 31) == 0) xr[t >> 5] = c;
   __syncthreads();
-  uint8_t* o = out + (size_t)img * stride + offs[blockIdx.x];
+  uint8_t* o = out + bases[img] + offs[blockIdx.x];
   for (uint32_t i = t; i < L; i += kT) o[4 + i] = c0[i];
   if (t == 0) {
     uint32_t x = 0;
@@ -692,18 +812,27 @@ PngGeom png_geom(int n, int H, int W) {
   PngGeom g{};
   g.n = n; g.H = H; g.W = W;
   g.RS = 3 * W + 1;
-  g.R = kMaxStripBytes / g.RS;
-  if (g.R > 8) g.R = 8;
-  if (g.R < 1) g.R = 1;
+  g.MC = 16;
+  // rows per strip: at most 8, at most 32 KB of filtered bytes, and shared memory for three CTAs
+  // per SM where the width allows
+  int R = kMaxStripBytes / g.RS;
+  if (R > 8) R = 8;
+  if (R < 1) R = 1;
+  for (;; --R) {
+    const int S = R * g.RS;
+    g.R = R;
+    g.G = (S + kT - 2) / (kT - 1);
+    const int raw = ((R + 2) * 3 * W + 15) & ~15, ow = ((S + 48) & ~15) + 16;
+    int r0 = raw > ow ? raw : ow;
+    if (r0 < (int)sizeof(HuffWork)) r0 = ((int)sizeof(HuffWork) + 15) & ~15;
+    g.off_filt = r0;
+    g.off_ml = g.off_filt + (((R + 1) * g.RS + 15) & ~15);
+    g.off_tab = g.off_ml + kT * g.MC * 4;
+    g.smem = g.off_tab + (int)((sizeof(StripTables) + 15) & ~size_t(15));
+    if (R == 1 || g.smem <= 74 * 1024) break;
+  }
   g.nstrips = (H + g.R - 1) / g.R;
-  const int S = g.R * g.RS;
-  g.cap = ((S + 16 + 15) & ~15) + 16;
-  g.G = (S + kT - 1) / kT;
-  const int raw = ((g.R + 2) * 3 * W + 15) & ~15, tok = (kT * g.G * 2 + 15) & ~15;
-  g.off_filt = raw > tok ? raw : tok;
-  g.off_ow = g.off_filt + (((g.R + 1) * g.RS + 15) & ~15);
-  g.off_tab = g.off_ow + ((S + 32) & ~15) + 16;
-  g.smem = g.off_tab + (int)((sizeof(StripTables) + 15) & ~size_t(15));
+  g.cap = ((g.R * g.RS + 16 + 15) & ~15) + 16;
   return g;
 }
 
@@ -718,12 +847,13 @@ size_t png_bound(int H, int W) {
 size_t png_workspace(int n, int H, int W) {
   const PngGeom g = png_geom(n, H, W);
   const size_t ns = (size_t)n * g.nstrips;
-  return ns * g.cap + ns * sizeof(StripMeta) + ns * 4 + 256;
+  return ns * g.cap + ns * sizeof(StripMeta) + ns * 4 + 8 * (size_t)n + 256;
 }
 
 cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* out, long long stride,
-                              uint32_t* sizes, uint8_t* work, cudaStream_t s) {
-  if (n <= 0 || H <= 0 || W <= 0 || W > 8192 || H > 65535 || (size_t)stride < png_bound(H, W)) return cudaErrorInvalidValue;
+                              uint32_t* sizes, uint8_t* work, cudaStream_t s, bool contiguous) {
+  if (n <= 0 || H <= 0 || W <= 0 || W > 8192 || H > 65535 || (!contiguous && (size_t)stride < png_bound(H, W)))
+    return cudaErrorInvalidValue;
   const PngGeom g = png_geom(n, H, W);
   static int attr_set = 0;
   if (attr_set < g.smem) {
@@ -737,9 +867,12 @@ cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* 
   uint8_t* scratch = work;
   StripMeta* meta = reinterpret_cast<StripMeta*>(work + ns * g.cap);
   uint32_t* offs = reinterpret_cast<uint32_t*>(meta + ns);
+  unsigned long long* bases =
+      reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(offs + ns) + 7) & ~uintptr_t(7));
   png_strip_kernel<<<(unsigned)ns, kT, g.smem, s>>>(rgb, g, scratch, meta);
-  png_image_kernel<<<n, kT, 0, s>>>(g, scratch, meta, offs, out, stride, sizes);
-  png_chunk_kernel<<<(unsigned)ns, kT, g.cap + 32, s>>>(g, scratch, meta, offs, out, stride);
+  png_image_kernel<<<n, kT, 0, s>>>(g, scratch, meta, offs, sizes);
+  png_frame_kernel<<<1, kT, 0, s>>>(g, sizes, bases, out, stride, contiguous ? 1 : 0);
+  png_chunk_kernel<<<(unsigned)ns, kT, g.cap + 32, s>>>(g, scratch, meta, offs, bases, out);
   return cudaGetLastError();
 }
 

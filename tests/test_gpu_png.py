@@ -90,3 +90,22 @@ def test_png_rejects_bad_args():
     with pytest.raises(lbx.LbxError):
         lbx.png_encode_device(0, 1, 4, 4, 0, 1024, 0)
     assert lbx.png_bound(0, 5) == 0 and lbx.png_bound(4, 9000) == 0
+
+
+def test_reconstruct_png_matches_reconstruct():
+    """lbx_reconstruct_png (blobs -> PNG bytes on the host) decodes to exactly lbx_reconstruct's RGB."""
+    dec = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=3)
+    rng = np.random.default_rng(5)
+    lats = rng.standard_normal((3, 4, 64, 64), dtype=np.float32).astype(np.float16)
+    blobs = [lbx.pack(lats[i], 1) for i in range(3)]
+    rgb = dec.reconstruct(blobs)
+    pngs = dec.reconstruct_png(blobs)
+    assert len(pngs) == 3
+    for i in range(3):
+        got, types, _ = P.decode_png(pngs[i])
+        assert np.array_equal(got, rgb[i])
+    # a too-small cap reports the need and fails cleanly; the decoder stays usable
+    with pytest.raises(lbx.LbxError):
+        dec.reconstruct_png(blobs, out=np.empty(1000, np.uint8))
+    again = dec.reconstruct_png(blobs[:1])
+    assert again[0] == pngs[0]
