@@ -386,12 +386,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 
 cudaError_t launch_attn_fa(const __half* qkv, __half* out, int n, int L, cudaStream_t s) {
   constexpr int smem = 1024 + kQBytes + (kKSt + kVSt) * kChunk + kPBytes + kXBytes + 256 * 4 + 128 * 4 + 256;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return cudaErrorNotSupported;
-    attr = true;
-  }
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(attn_fa_kernel), smem)) return cudaErrorNotSupported;
   if (n <= 0 || L % 128) return cudaErrorInvalidValue;
   CUtensorMap tmQK, tmV;
   const uint64_t dims[2] = {1536, (uint64_t)n * L};

@@ -281,15 +281,9 @@ __global__ void __launch_bounds__(kCoThreads, 1)
 
 cudaError_t launch_conv_out_tc(const __half* x, const float2* ss, const float* w, const float* b, uint8_t* rgb,
                                int n, int H, int W, bool h2, cudaStream_t s) {
-  static bool attr_ok = false;
-  if (!attr_ok) {
-    if (cudaFuncSetAttribute(conv_out_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCoSmem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(conv_out_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCoSmem) !=
-            cudaSuccess)
-      return cudaErrorNotSupported;
-    attr_ok = true;
-  }
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(conv_out_tc_kernel<true>), kCoSmem) ||
+      !ensure_smem_attr(reinterpret_cast<const void*>(conv_out_tc_kernel<false>), kCoSmem))
+    return cudaErrorNotSupported;
   if (n <= 0 || W % 128 || H < 1) return cudaErrorInvalidValue;
   CUtensorMap tm;
   const uint64_t dims[4] = {128, (uint64_t)W, (uint64_t)H, (uint64_t)n};

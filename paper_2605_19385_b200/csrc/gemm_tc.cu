@@ -22,7 +22,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "act.cuh"
 #include "gemm_tc.cuh"
@@ -934,21 +936,26 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
 
 template <int BN, int CG>
 static bool set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<BN, CG>::SMEM_MAX) == cudaSuccess &&
-         cudaFuncSetAttribute(gemm_tc_kernel<BN, CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Cfg<BN, CG>::SMEM_MAX) == cudaSuccess;
+  return ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, CG, false>), Cfg<BN, CG>::SMEM_MAX) &&
+         ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, CG, true>), Cfg<BN, CG>::SMEM_MAX);
 }
 
-bool gemm_tc_prepare() {
-  static int ok = -1;
+bool ensure_smem_attr(const void* func, int bytes) {
   static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
   std::lock_guard<std::mutex> g(mu);
-  if (ok < 0) {
-    ok = tma_available() && set_attr<256, 2>() && set_attr<128, 2>() && set_attr<256, 1>() && set_attr<128, 1>();
-    num_sms();
-  }
-  return ok == 1;
+  int& have = done[{dev, func}];
+  if (have >= bytes) return true;
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  have = bytes;
+  return true;
+}
+
+bool gemm_tc_prepare() {  // per device (a multi-GPU batcher drives several from one process)
+  num_sms();
+  return tma_available() && set_attr<256, 2>() && set_attr<128, 2>() && set_attr<256, 1>() && set_attr<128, 1>();
 }
 
 bool resid_fold_always() { return g_fold_always != 0; }

@@ -79,5 +79,8 @@ bool make_tensor_map_f16(CUtensorMap* m, const void* base, int rank, const uint6
 // Number of SMs (cached) and the driver entry point used to encode TMA descriptors.
 int num_sms();
 bool tma_available();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it for the current device the
+// first time a kernel is launched there (again if a larger size is needed).  Thread-safe.
+bool ensure_smem_attr(const void* func, int bytes);
 
 }  // namespace lbx

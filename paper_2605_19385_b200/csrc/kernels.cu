@@ -226,13 +226,7 @@ static bool gn_apply_bulk_launch(const __half* x, __half* y, const GnSrc& g, int
   // the register-staged kernel (scripts/op_bench.py gn)
   if (!g_apply_bulk || img_bytes % kApChunk) return false;
   constexpr int smem = kApStages * kApChunk + kApStages * 8;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gn_apply_bulk_kernel<SILU, CV, H2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess)
-      return false;
-    attr = true;
-  }
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(gn_apply_bulk_kernel<SILU, CV, H2>), smem)) return false;
   const long long chunks = (long long)n * img_bytes / kApChunk;
   const int grid = (int)(chunks < num_sms() ? chunks : num_sms());
   gn_apply_bulk_kernel<SILU, CV, H2><<<grid, 256, smem, s>>>(x, y, g, img_bytes, chunks);

@@ -22,6 +22,7 @@
 
 #include <cstdint>
 
+#include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace lbx {
@@ -855,14 +856,9 @@ cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* 
   if (n <= 0 || H <= 0 || W <= 0 || W > 8192 || H > 65535 || (!contiguous && (size_t)stride < png_bound(H, W)))
     return cudaErrorInvalidValue;
   const PngGeom g = png_geom(n, H, W);
-  static int attr_set = 0;
-  if (attr_set < g.smem) {
-    cudaError_t e = cudaFuncSetAttribute(png_strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(png_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, g.cap + 32);
-    if (e != cudaSuccess) return e;
-    attr_set = g.smem;
-  }
+  if (!ensure_smem_attr(reinterpret_cast<const void*>(png_strip_kernel), g.smem) ||
+      !ensure_smem_attr(reinterpret_cast<const void*>(png_chunk_kernel), g.cap + 32))
+    return cudaErrorNotSupported;
   const size_t ns = (size_t)n * g.nstrips;
   uint8_t* scratch = work;
   StripMeta* meta = reinterpret_cast<StripMeta*>(work + ns * g.cap);
