@@ -62,6 +62,7 @@ struct KParams {
   int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
   int rpf_pf;          // 1: L2-prefetch the next preload's rows before waiting for the accumulator
+  int sched;           // 1: each cluster takes a contiguous block of tiles (conv modes), 0: round-robin
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
@@ -186,6 +187,12 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
   const bool leader = rank == 0;
   const int cluster_id = blockIdx.x / CG;
   const int nclusters = gridDim.x / CG;
+  // tile sequence of this cluster: a contiguous block (conv modes: a CTA walks down its own rows,
+  // so the halo rows it shares with the row pair above were fetched by itself one tile-row earlier
+  // and hit L2), or round-robin (plain GEMMs: concurrent clusters share A / B tiles through L2)
+  const int t_first = p.sched ? (int)((long long)cluster_id * p.tiles / nclusters) : cluster_id;
+  const int t_end = p.sched ? (int)((long long)(cluster_id + 1) * p.tiles / nclusters) : p.tiles;
+  const int t_step = p.sched ? 1 : nclusters;
   // A stages per tile and taps (B stages) per A stage
   const int n_a = p.halo ? p.cblocks : p.num_kb;
   const int per_a = p.halo ? p.taps : 1;
@@ -218,7 +225,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     if (ptx::elect_one()) {
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cluster_id; t < p.tiles; t += nclusters) {
+      for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int rows_cta = 128 * p.msub;
@@ -292,7 +299,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     if (ptx::elect_one()) {
       int st = 0;
       uint32_t ph = 0;
-      for (int t = cluster_id; t < p.tiles; t += nclusters) {
+      for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int bimg = p.batch_m ? (m_tile * 128 * p.msub * CG) / p.batch_m : 0;  // batched: image of the tile
@@ -348,7 +355,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       const uint32_t a_stage16 = (uint32_t)p.a_stage_bytes >> 4, sub16 = (uint32_t)p.halo_sub_bytes >> 4;
       const int msub = p.msub;
       const bool conv = p.mode == GEMM_CONV3X3, halo = p.halo != 0, dbm = p.desc_base_mode != 0;
-      for (int t = cluster_id; t < p.tiles; t += nclusters) {
+      for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         // rpf: every use of a buffer (the first included) waits for the epilogue's residual preload
@@ -425,7 +432,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     const int rows = box_rows * 130;
     int st = 0;
     uint32_t ph = 0;
-    for (int t = cluster_id; t < p.tiles; t += nclusters) {
+    for (int t = t_first; t < t_end; t += t_step) {
       int m_tile, n_tile, phs;
       tile_coords(p, t, m_tile, n_tile, phs);
       const int m0 = tile_row0(p, m_tile, (int)rank, CG, 0);
@@ -525,7 +532,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     // buffer to the MMA issuer is the arrival after the preload.  It replaces the folded extra K
     // (4-8 short k-blocks of MMAs) and the epilogue's late residual reads.
     auto prefill = [&](int tn, int buf) {
-      if (tn < p.tiles) {
+      if (tn < t_end) {
         int mt, nt, phn;
         tile_coords(p, tn, mt, nt, phn);
         for (int sub = 0; sub < p.msub; ++sub) {
@@ -562,7 +569,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     };
     // L2 prefetch of the rows the next preload reads, issued before the wait for the accumulator
     auto prefetch_resid = [&](int tn) {
-      if (tn >= p.tiles || !g_rpf_l2pf_dev(p)) return;
+      if (tn >= t_end || !g_rpf_l2pf_dev(p)) return;
       int mt, nt, phn;
       tile_coords(p, tn, mt, nt, phn);
       for (int sub = 0; sub < p.msub; ++sub) {
@@ -573,13 +580,13 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       }
     };
     if (p.rpf) {
-      prefill(cluster_id, 0);
-      prefill(cluster_id + nclusters, 1);
+      prefill(t_first, 0);
+      prefill(t_first + t_step, 1);
     }
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t ochunk = 0;  // tstore: staged chunks so far (selects the staging buffer)
-    for (int t = cluster_id; t < p.tiles; t += nclusters) {
+    for (int t = t_first; t < t_end; t += t_step) {
       int m_tile, n_tile, ph;
       tile_coords(p, t, m_tile, n_tile, ph);
       const int n0 = n_tile * BN;
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         __syncwarp();
         bias_ntile = n_tile;
       }
-      if (p.rpf) prefetch_resid(t + 2 * nclusters);
+      if (p.rpf) prefetch_resid(t + 2 * t_step);
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       for (int sub = 0; sub < (p.epi_skip == 1 ? 0 : p.msub); ++sub) {
@@ -727,7 +734,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       }
       }  // sub-tiles
       if (p.rpf) {
-        prefill(t + 2 * nclusters, acc);  // this buffer's next tile: preload, then release
+        prefill(t + 2 * t_step, acc);  // this buffer's next tile: preload, then release
       } else {
         ptx::tc_fence_before();
         __syncwarp();
@@ -816,6 +823,9 @@ static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel inst
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
+static int g_sched_policy = 0;     // 1: contiguous tile blocks per cluster for conv modes (bit 22 sets;
+                                   // measured worse: c128 conv reads 25.5 vs 23.0 GB from DRAM, the
+                                   // vertical halo reuse distance outlives L2; decode time neutral)
 static int g_rpf_pf = 0;           // 1: L2 prefetch ahead of the residual preload (bit 21 sets;
                                    // measured neutral under the power cap)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
@@ -836,6 +846,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
   g_rpf_pf = (halo_policy >> 21) & 1;
+  g_sched_policy = (halo_policy >> 22) & 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -1017,6 +1028,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy &&
             (g_rpf_policy == 2 || a.N <= 128)) ? 1 : 0;
   kp.rpf_pf = g_rpf_pf;
+  kp.sched = (g_sched_policy && a.mode != GEMM_PLAIN) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
