@@ -50,7 +50,8 @@ def _check(imgs, pngs):
         assert np.array_equal(types, want), f"image {i}: filter types differ"
 
 
-@pytest.mark.parametrize("H,W", [(1, 1), (2, 3), (37, 45), (9, 1000), (17, 1024), (64, 64), (130, 77)])
+@pytest.mark.parametrize("H,W", [(1, 1), (2, 3), (37, 45), (9, 1000), (17, 1024), (64, 64), (130, 77), (3, 8192),
+                                 (5, 5000), (700, 4)])
 def test_png_shapes(H, W):
     imgs = _images(H, W, seed=H * 1000 + W)
     _check(imgs, gpu_png(imgs))
