@@ -20,7 +20,11 @@
 //                          (per-thread segments combined by multiplication by x^(8n) mod P).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
@@ -48,6 +52,7 @@ struct PngGeom {
   int cap;      // scratch bytes per strip
   int G;        // parse segment bytes per thread
   int MC;       // LZ77 matches kept per parse segment
+  unsigned long long* tl;  // diagnostics (LBX_PNG_TIMING): per-strip phase timestamps, or null
   // dynamic smem layout (bytes): raw rows, then Huffman work arrays, then the output words share
   // offset 0 (each dead before the next); filtered rows, match lists and tables follow
   int off_filt, off_ml, off_tab, smem;
@@ -97,11 +102,32 @@ struct Alpha {
 struct HuffWork {
   Alpha<286> lit;
   Alpha<30> dst;
+  uint32_t keys[512];       // bitonic sort keys: (freq << 9 | sym) literal/length, (1 << 31 | freq << 5 | sym) distance
+  uint32_t ccnt[10][32];    // canonical codes: per 32-symbol chunk, count per (alphabet, length)
 };
+
+// code-length run-length coding (RFC 1951 3.2.7) of one maximal run of `run` copies of `v`:
+// returns the token count; writes the tokens (sym | extra << 5) when out != null
+__device__ __forceinline__ int rle_run(int v, int run, uint16_t* out) {
+  int n = 0;
+  if (v == 0) {
+    int r = run;
+    while (r >= 11) { const int k = r < 138 ? r : 138; if (out) out[n] = (uint16_t)(18 | ((k - 11) << 5)); ++n; r -= k; }
+    if (r >= 3) { if (out) out[n] = (uint16_t)(17 | ((r - 3) << 5)); ++n; r = 0; }
+    for (; r > 0; --r) { if (out) out[n] = 0; ++n; }
+  } else {
+    if (out) out[n] = (uint16_t)v;
+    ++n;
+    int r = run - 1;
+    while (r >= 3) { const int k = r < 6 ? r : 6; if (out) out[n] = (uint16_t)(16 | ((k - 3) << 5)); ++n; r -= k; }
+    for (; r > 0; --r) { if (out) out[n] = (uint16_t)v; ++n; }
+  }
+  return n;
+}
 
 __device__ void huff_merge(const uint32_t* wl, uint32_t* wi, uint16_t* pl, uint16_t* pi, uint8_t* di, int m) {
   int li = 0, ii = 0, ni = 0;
-  uint32_t hl = wl[0], hi = 0;  // queue heads
+  uint32_t hl = wl[0], hl1 = m > 1 ? wl[1] : 0u, hi = 0;  // queue heads (next leaf prefetched)
   for (int k = 0; k < m - 1; ++k) {
     uint32_t w2 = 0;
 #pragma unroll
@@ -109,7 +135,8 @@ __device__ void huff_merge(const uint32_t* wl, uint32_t* wi, uint16_t* pl, uint1
       if (li < m && (ii >= ni || hl <= hi)) {
         w2 += hl;
         pl[li++] = (uint16_t)ni;
-        hl = li < m ? wl[li] : 0u;
+        hl = hl1;
+        hl1 = li + 1 < m ? wl[li + 1] : 0u;
       } else {
         w2 += hi;
         pi[ii++] = (uint16_t)ni;
@@ -256,6 +283,7 @@ struct StripTables {
   uint16_t lcode[286 + 30];
   uint16_t ccode[19];
   uint16_t rle[320];   // code-length RLE symbols (sym | extra << 5)
+  uint16_t rle_off[320];  // their bit offsets within the header's RLE part
   uint32_t red[kT / 32];
   uint32_t scal[8];    // 0 nrle, 1 hlit, 2 hdist, 3 hclen, 4 header bits, 5 m_lit, 6 m_dist
   uint8_t nmatch[kT];
@@ -265,6 +293,14 @@ struct StripTables {
 
 // short match distances (1, 3, 6 bytes back); the fourth candidate is the row above (RS)
 __device__ __forceinline__ int short_dist(int di) { return di == 0 ? 1 : di == 1 ? 3 : 6; }
+
+__device__ __forceinline__ void png_mark(const PngGeom& g, int i) {
+  if (g.tl && threadIdx.x == 0) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    g.tl[blockIdx.x * 16 + i] = ns;
+  }
+}
 
 __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict__ rgb, PngGeom g,
                                                        uint8_t* __restrict__ scratch, StripMeta* __restrict__ meta) {
@@ -281,6 +317,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   uint8_t* filt = sm + g.off_filt;          // row y0-1 then the strip's rows (RS bytes each)
   uint32_t* mlist = reinterpret_cast<uint32_t*>(sm + g.off_ml);  // per-thread LZ77 matches
   StripTables& T = *reinterpret_cast<StripTables*>(sm + g.off_tab);
+  png_mark(g, 0);
 
   // ---- 1. raw rows into smem (rows before the image are zero)
   const uint8_t* src = rgb + (size_t)img * g.H * rb;
@@ -305,6 +342,59 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   __syncthreads();
 
   // ---- 2. filter rows y0-1 (history, when it exists) .. y0+rows-1
+  png_mark(g, 1);
+  if ((rb & 3) == 0) {
+    // one warp per row, no block barriers: 32-bit shared loads, lane l takes words l, l+32, ...;
+    // the word before (for the left / up-left neighbours, 3 bytes back) comes from lane l-1
+    const int lane = t & 31, nwords = rb >> 2;
+    for (int fr = (y0 > 0 ? 0 : 1) + (t >> 5); fr <= rows; fr += kT / 32) {
+      const uint32_t* c32 = reinterpret_cast<const uint32_t*>(raw + (fr + 1) * rb);
+      const uint32_t* u32 = reinterpret_cast<const uint32_t*>(raw + fr * rb);
+      auto pass = [&](int mode, uint8_t* out) -> void {  // mode < 0: sums; else write filter `mode`
+        uint32_t cc = 0, uc = 0;  // lane 31's words of the previous round
+        uint32_t sum[5] = {0, 0, 0, 0, 0};
+        for (int base = 0; base < nwords; base += 32) {
+          const int w = base + lane;
+          const uint32_t cw = w < nwords ? c32[w] : 0u, uw = w < nwords ? u32[w] : 0u;
+          uint32_t cp = __shfl_up_sync(0xffffffffu, cw, 1), upw = __shfl_up_sync(0xffffffffu, uw, 1);
+          if (lane == 0) { cp = cc; upw = uc; }
+          cc = __shfl_sync(0xffffffffu, cw, 31);
+          uc = __shfl_sync(0xffffffffu, uw, 31);
+          if (w < nwords) {
+            const uint64_t cwin = (uint64_t)cw << 32 | cp, uwin = (uint64_t)uw << 32 | upw;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int x = (int)((cw >> (8 * j)) & 255u), a = (int)((cwin >> (8 * j + 8)) & 255u);
+              const int b = (int)((uw >> (8 * j)) & 255u), c = (int)((uwin >> (8 * j + 8)) & 255u);
+              if (mode < 0) {
+#pragma unroll
+                for (int k = 0; k < 5; ++k) sum[k] += (uint32_t)abs((int)(int8_t)filt_byte(k, x, a, b, c));
+              } else {
+                out[1 + 4 * w + j] = filt_byte(mode, x, a, b, c);
+              }
+            }
+          }
+        }
+        if (mode < 0) {
+          int best = 0;
+          uint32_t bsum = 0xffffffffu;
+#pragma unroll
+          for (int k = 0; k < 5; ++k) {
+            uint32_t v = sum[k];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (v < bsum) { bsum = v; best = k; }  // ties: the lower filter type
+          }
+          out[0] = (uint8_t)best;  // every lane holds the same choice
+        }
+      };
+      uint8_t* out = filt + fr * RS;
+      uint8_t choice[1];
+      pass(-1, choice);
+      if (lane == 0) out[0] = choice[0];
+      pass(choice[0], out);
+    }
+  } else
   for (int fr = (y0 > 0 ? 0 : 1); fr <= rows; ++fr) {
     const uint8_t* cur = raw + (fr + 1) * rb;  // image row y0-1+fr
     const uint8_t* up = raw + fr * rb;         // zeros above row 0
@@ -345,6 +435,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   const uint8_t* f = filt + RS;  // the strip's bytes; f[-RS..-1] is the previous row when y0 > 0
 
   // ---- 3. Adler-32 partials: a = sum x_j, b = sum (S - j) x_j
+  png_mark(g, 2);
   {
     unsigned long long a = 0, b = 0;
     for (int j = t; j < S; j += kT) {
@@ -377,8 +468,12 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     };
     int nm = 0;
     uint64_t back = window(p0);
+    // f[p] and f[p - RS] of the next position are loaded one step ahead (the common step is a
+    // literal), so the shared-memory latency overlaps the current step's work
+    auto up_at = [&](int p) -> int { return p - RS >= lo ? (int)f[p - RS] : -1; };
+    int x = p0 < p1 ? (int)f[p0] : 0, u = p0 < p1 ? up_at(p0) : -1;
     for (int p = p0; p < p1;) {
-      const int x = f[p];
+      const int xn = p + 1 < p1 ? (int)f[p + 1] : 0, un = p + 1 < p1 ? up_at(p + 1) : -1;
       const int maxl = min(258, p1 - p);
       int bl = 0, bd = 0;
       if (maxl >= 3 && nm < g.MC) {
@@ -386,7 +481,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
         for (int di = 0; di < 4; ++di) {
           const int d = di < 3 ? short_dist(di) : RS;
           if (p - d < lo) continue;
-          const int y = di < 3 ? (int)((back >> (8 * (d - 1))) & 255u) : f[p - d];
+          const int y = di < 3 ? (int)((back >> (8 * (d - 1))) & 255u) : u;
           if (y != x) continue;
           int l = 1;
           while (l < maxl && f[p + l] == f[p + l - d]) ++l;
@@ -402,10 +497,13 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
         atomicAdd(&T.lfreq[286 + c], 1u);
         p += bl;
         back = window(p);
+        if (p < p1) { x = f[p]; u = up_at(p); }
       } else {
         atomicAdd(&T.lfreq[x], 1u);
         back = ((back << 8) | (uint64_t)x) & 0xFFFFFFFFFFFFull;
         ++p;
+        x = xn;
+        u = un;
       }
     }
     T.nmatch[t] = (uint8_t)nm;
@@ -414,28 +512,47 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   if (t == 0) T.lfreq[256] = 1;  // end of block
   __syncthreads();
 
-  // ---- 5. rank sort of the used symbols by (freq, symbol); zero the lengths
+  // ---- 5. sort the used symbols by (freq, symbol): one bitonic sort of 512 keys, literal/length
+  // keys first, then distance keys, unused last
+  png_mark(g, 3);
   uint32_t ml_cnt = 0, md_cnt = 0;
-  for (int sym = t; sym < 286 + 30; sym += kT) {
-    T.llen[sym] = 0;
-    const uint32_t fs = T.lfreq[sym];
-    if (!fs) continue;
-    const int b0 = sym < 286 ? 0 : 286, b1 = sym < 286 ? 286 : 316;
-    int rank = 0;
-    for (int u = b0; u < b1; ++u) {
-      const uint32_t fu = T.lfreq[u];
-      rank += fu && (fu < fs || (fu == fs && u < sym));
+  for (int i = t; i < 512; i += kT) {
+    uint32_t key = 0xFFFFFFFFu;
+    if (i < 316) {
+      T.llen[i] = 0;
+      const uint32_t fs = T.lfreq[i];
+      if (fs) {
+        key = i < 286 ? (fs << 9 | (uint32_t)i) : (1u << 31 | fs << 5 | (uint32_t)(i - 286));
+        if (i < 286) ++ml_cnt; else ++md_cnt;
+      }
     }
-    T.order[b0 + rank] = (uint16_t)(sym - b0);
-    if (sym < 286) ++ml_cnt; else ++md_cnt;
+    hw.keys[i] = key;
   }
+  if (t < 2) { T.scal[1 + t] = t ? 1u : 257u; }  // hlit / hdist minima (raised by atomicMax below)
   const int m_l = (int)block_sum_u32(ml_cnt, T.red);
   const int m_d = (int)block_sum_u32(md_cnt, T.red);
-  for (int r = t; r < m_l; r += kT) hw.lit.wl[r] = T.lfreq[T.order[r]];
-  if (t < m_d) hw.dst.wl[t] = T.lfreq[286 + T.order[286 + t]];
+  for (int k = 2; k <= 512; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1)), ixj = i | j;
+      const uint32_t x = hw.keys[i], y = hw.keys[ixj];
+      if ((x > y) == ((i & k) == 0)) { hw.keys[i] = y; hw.keys[ixj] = x; }
+      __syncthreads();
+    }
+  }
+  for (int r = t; r < m_l + m_d; r += kT) {
+    const uint32_t key = hw.keys[r];
+    if (r < m_l) {
+      T.order[r] = (uint16_t)(key & 511u);
+      hw.lit.wl[r] = key >> 9;
+    } else {
+      T.order[286 + r - m_l] = (uint16_t)(key & 31u);
+      hw.dst.wl[r - m_l] = (key >> 5) & 0x3FFFFFFu;
+    }
+  }
   __syncthreads();
 
   // ---- 6. code lengths and codes
+  png_mark(g, 4);
   if (t == 0 && m_l >= 2) huff_merge(hw.lit.wl, hw.lit.wi, hw.lit.pl, hw.lit.pi, hw.lit.di, m_l);
   if (t == 32 && m_d >= 2) huff_merge(hw.dst.wl, hw.dst.wi, hw.dst.pl, hw.dst.pi, hw.dst.di, m_d);
   __syncthreads();
@@ -447,6 +564,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     const int d = hw.dst.di[hw.dst.pl[t]] + 1;
     atomicAdd(&T.cnt[1][d > 15 ? 15 : d], 1u);
   }
+  for (int i = t; i < 320; i += kT) hw.ccnt[i >> 5][i & 31] = 0;
   __syncthreads();
   if (t == 0 || t == 32) {
     const int k = t ? 1 : 0, m = k ? m_d : m_l;
@@ -470,69 +588,48 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     }
   }
   __syncthreads();
-  // canonical codes: next[len] + the number of lower symbols with the same length
+  // canonical codes: next[len] + the number of lower symbols of the same alphabet and length,
+  // counted per 32-symbol chunk (shared counters, then a prefix over chunks) and within the chunk
+  // by a warp match
   for (int i = t; i < 316; i += kT) {
-    const int k = i < 286 ? 0 : 1, b0 = 286 * k;
     const int len = T.llen[i];
-    uint16_t code = 0;
-    if (len) {
-      uint32_t c = T.next[k][len];
-      for (int u = b0; u < i; ++u) c += T.llen[u] == len;
-      code = (uint16_t)rev_bits(c, len);
-    }
-    T.lcode[i] = code;
+    if (len) atomicAdd(&hw.ccnt[i >> 5][(i >= 286) * 16 + len], 1u);
   }
   __syncthreads();
-  // ---- 7. block header (thread 0) || token bits (the rest); offsets; dynamic vs stored
+  if (t < 32) {
+    uint32_t acc = 0;
+    for (int c = 0; c < 10; ++c) { const uint32_t v = hw.ccnt[c][t]; hw.ccnt[c][t] = acc; acc += v; }
+  }
+  // hlit / hdist: one past the last used symbol of each alphabet
+  for (int i = t; i < 316; i += kT)
+    if (T.llen[i]) atomicMax(&T.scal[i < 286 ? 1 : 2], (uint32_t)(i < 286 ? i + 1 : i - 285));
+  __syncthreads();
+  {
+    const int lane = t & 31;
+    for (int i0 = t & ~31; i0 < 316; i0 += kT) {  // warp-uniform
+      const int i = i0 + lane;
+      const int len = i < 316 ? T.llen[i] : 0, k = i >= 286;
+      const int key = len ? k * 16 + len : 255;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      if (i < 316) {
+        uint16_t code = 0;
+        if (len)
+          code = (uint16_t)rev_bits(T.next[k][len] + hw.ccnt[i >> 5][key] + __popc(grp & ((1u << lane) - 1u)), len);
+        T.lcode[i] = code;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 7. token bits; the block header: parallel run-length coding of the code lengths, their
+  // code (thread 0), bit offsets by block scans; dynamic vs stored
   int dcs[4], dns[4], dvs[4];
 #pragma unroll
   for (int di = 0; di < 4; ++di) dist_sym(di < 3 ? short_dist(di) : RS, dcs[di], dns[di], dvs[di]);
   const int nm = T.nmatch[t];
   uint32_t mybits = 0;
-  if (t == 0) {  // header: run-length coded code lengths (RFC 1951 3.2.7) and their own code
-    int hlit = 286, hdist = 30;
-    while (hlit > 257 && !T.llen[hlit - 1]) --hlit;
-    while (hdist > 1 && !T.llen[286 + hdist - 1]) --hdist;
-    const int nl = hlit + hdist;
-    auto seq = [&](int i) -> int { return i < hlit ? T.llen[i] : T.llen[286 + i - hlit]; };
-    int nr = 0;
-    for (int i = 0; i < nl;) {
-      const int v = seq(i);
-      int run = 1;
-      while (i + run < nl && seq(i + run) == v) ++run;
-      if (v == 0) {
-        int r = run;
-        while (r >= 11) { const int k = r < 138 ? r : 138; T.rle[nr++] = (uint16_t)(18 | ((k - 11) << 5)); r -= k; }
-        if (r >= 3) { T.rle[nr++] = (uint16_t)(17 | ((r - 3) << 5)); r = 0; }
-        while (r-- > 0) T.rle[nr++] = 0;
-      } else {
-        T.rle[nr++] = (uint16_t)v;
-        int r = run - 1;
-        while (r >= 3) { const int k = r < 6 ? r : 6; T.rle[nr++] = (uint16_t)(16 | ((k - 3) << 5)); r -= k; }
-        while (r-- > 0) T.rle[nr++] = (uint16_t)v;
-      }
-      i += run;
-    }
-    for (int i = 0; i < nr; ++i) ++T.cfreq[T.rle[i] & 31];
-    int mc = 0;
-    for (int sym = 0; sym < 19; ++sym)  // insertion sort of the used code-length symbols
-      if (T.cfreq[sym]) {
-        int j = mc++;
-        while (j > 0 && (T.cfreq[T.corder[j - 1]] > T.cfreq[sym])) { T.corder[j] = T.corder[j - 1]; --j; }
-        T.corder[j] = (uint16_t)sym;
-      }
-    huff_small(T.cfreq, 19, T.corder, mc, 7, T.clen, T.ccode);
-    const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
-    int hclen = 19;
-    while (hclen > 4 && !T.clen[kOrd[hclen - 1]]) --hclen;
-    uint32_t bits = 3 + 5 + 5 + 4 + 3 * hclen;
-    for (int i = 0; i < nr; ++i) {
-      const int sym = T.rle[i] & 31;
-      bits += T.clen[sym] + (sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0);
-    }
-    T.scal[0] = (uint32_t)nr; T.scal[1] = (uint32_t)hlit; T.scal[2] = (uint32_t)hdist;
-    T.scal[3] = (uint32_t)hclen; T.scal[4] = bits;
-  } else {
+  png_mark(g, 5);
+  {
     int mi = 0, mp = nm ? (int)(ml[0] >> 16) + p0 : p1;
     for (int p = p0; p < p1;) {
       if (p == mp) {
@@ -550,10 +647,67 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
       }
     }
   }
+  const int hlit = (int)T.scal[1], hdist = (int)T.scal[2], nl = hlit + hdist;
+  auto seq = [&](int i) -> int { return i < hlit ? T.llen[i] : T.llen[286 + i - hlit]; };
+  int rv[2] = {0, 0}, rn[2] = {0, 0}, rc[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {  // runs starting at 2t, 2t+1 (index order, for the scan)
+    const int i = 2 * t + q;
+    if (i < nl) {
+      const int v = seq(i);
+      if (i == 0 || seq(i - 1) != v) {
+        int run = 1;
+        while (i + run < nl && seq(i + run) == v) ++run;
+        rv[q] = v; rn[q] = run; rc[q] = rle_run(v, run, nullptr);
+      }
+    }
+  }
+  uint32_t nr_tot;
+  const uint32_t roff = block_scan_u32((uint32_t)(rc[0] + rc[1]), T.red, &nr_tot);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (rc[q]) {
+      uint16_t* o = T.rle + roff + (q ? rc[0] : 0);
+      rle_run(rv[q], rn[q], o);
+      for (int k = 0; k < rc[q]; ++k) atomicAdd(&T.cfreq[o[k] & 31], 1u);
+    }
+  __syncthreads();
+  if (t == 0) {  // the code-length code: 19 symbols, one thread
+    int mc = 0;
+    for (int sym = 0; sym < 19; ++sym)  // insertion sort of the used code-length symbols
+      if (T.cfreq[sym]) {
+        int j = mc++;
+        while (j > 0 && (T.cfreq[T.corder[j - 1]] > T.cfreq[sym])) { T.corder[j] = T.corder[j - 1]; --j; }
+        T.corder[j] = (uint16_t)sym;
+      }
+    huff_small(T.cfreq, 19, T.corder, mc, 7, T.clen, T.ccode);
+    const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
+    int hclen = 19;
+    while (hclen > 4 && !T.clen[kOrd[hclen - 1]]) --hclen;
+    T.scal[3] = (uint32_t)hclen;
+    T.scal[0] = nr_tot;
+  }
+  __syncthreads();
+  uint32_t rb2[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int i = 2 * t + q;
+    if (i < (int)nr_tot) {
+      const int sym = T.rle[i] & 31;
+      rb2[q] = T.clen[sym] + (sym == 16 ? 2 : sym == 17 ? 3 : sym == 18 ? 7 : 0);
+    }
+  }
+  uint32_t rle_bits;
+  const uint32_t rboff = block_scan_u32(rb2[0] + rb2[1], T.red, &rle_bits);
+  if (2 * t < (int)nr_tot) T.rle_off[2 * t] = (uint16_t)rboff;
+  if (2 * t + 1 < (int)nr_tot) T.rle_off[2 * t + 1] = (uint16_t)(rboff + rb2[0]);
+  const uint32_t hfix = 3 + 5 + 5 + 4 + 3 * T.scal[3];  // BFINAL, BTYPE, HLIT, HDIST, HCLEN, lengths
   uint32_t tbits;
   const uint32_t myoff = block_scan_u32(mybits, T.red, &tbits);
+  png_mark(g, 6);
   const uint32_t pre = first ? 16u : 0u;  // zlib header
-  const uint32_t dyn_end = pre + T.scal[4] + tbits + T.llen[256];  // bit after the end-of-block code
+  const uint32_t hdr_bits = hfix + rle_bits;
+  const uint32_t dyn_end = pre + hdr_bits + tbits + T.llen[256];  // bit after the end-of-block code
   const uint32_t dyn_bytes = (last ? (dyn_end + 7) / 8 : (dyn_end + 3 + 7) / 8 + 4) + (last ? 4 : 0);
   const uint32_t sto_bytes = pre / 8 + 5 + (uint32_t)S + (last ? 4 : 0);
   const bool dyn = dyn_bytes < sto_bytes;
@@ -564,27 +718,29 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
 
   // ---- 8. write
   if (dyn) {
-    if (t == 0) {
+    if (t == 0) {  // fixed part of the header
       BitW w(ow, 0);
       if (first) { w.put(0x78, 8); w.put(0x5E, 8); }
       w.put(last ? 1u : 0u, 1);
       w.put(2, 2);
-      w.put(T.scal[1] - 257, 5);
-      w.put(T.scal[2] - 1, 5);
+      w.put((uint32_t)hlit - 257, 5);
+      w.put((uint32_t)hdist - 1, 5);
       w.put(T.scal[3] - 4, 4);
       const uint8_t kOrd[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
       for (int i = 0; i < (int)T.scal[3]; ++i) w.put(T.clen[kOrd[i]], 3);
-      for (int i = 0; i < (int)T.scal[0]; ++i) {
-        const int sym = T.rle[i] & 31, ex = T.rle[i] >> 5;
-        w.put(T.ccode[sym], T.clen[sym]);
-        if (sym == 16) w.put(ex, 2);
-        else if (sym == 17) w.put(ex, 3);
-        else if (sym == 18) w.put(ex, 7);
-      }
+      w.flush();
+    }
+    for (int i = t; i < (int)nr_tot; i += kT) {  // run-length coded code lengths, one token each
+      BitW w(ow, pre + hfix + T.rle_off[i]);
+      const int sym = T.rle[i] & 31, ex = T.rle[i] >> 5;
+      w.put(T.ccode[sym], T.clen[sym]);
+      if (sym == 16) w.put(ex, 2);
+      else if (sym == 17) w.put(ex, 3);
+      else if (sym == 18) w.put(ex, 7);
       w.flush();
     }
     {
-      BitW w(ow, pre + T.scal[4] + myoff);
+      BitW w(ow, pre + hdr_bits + myoff);
       int mi = 0, mp = nm ? (int)(ml[0] >> 16) + p0 : p1;
       for (int p = p0; p < p1;) {
         if (p == mp) {
@@ -634,6 +790,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
   __syncthreads();
 
   // ---- 9. out to the strip's scratch slot; meta
+  png_mark(g, 7);
   uint8_t* dst = scratch + (size_t)blockIdx.x * g.cap;
   const int nvec = ((int)bytes + 15) / 16;
   for (int i = t; i < nvec; i += kT) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(ow)[i];
@@ -647,6 +804,7 @@ __global__ void __launch_bounds__(kT) png_strip_kernel(const uint8_t* __restrict
     m.rsv = dyn ? 1u : 0u;
     meta[blockIdx.x] = m;
   }
+  png_mark(g, 8);
 }
 
 // --------------------------------------------------------------------------- CRC-32
@@ -865,7 +1023,27 @@ cudaError_t launch_png_encode(const uint8_t* rgb, int n, int H, int W, uint8_t* 
   uint32_t* offs = reinterpret_cast<uint32_t*>(meta + ns);
   unsigned long long* bases =
       reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(offs + ns) + 7) & ~uintptr_t(7));
-  png_strip_kernel<<<(unsigned)ns, kT, g.smem, s>>>(rgb, g, scratch, meta);
+  static const bool timing = getenv("LBX_PNG_TIMING") != nullptr;
+  PngGeom gt = g;
+  if (timing) cudaMallocAsync(reinterpret_cast<void**>(&gt.tl), ns * 16 * 8, s);
+  png_strip_kernel<<<(unsigned)ns, kT, g.smem, s>>>(rgb, gt, scratch, meta);
+  if (timing) {  // per-phase mean durations over the strips, and the kernel's span
+    std::vector<unsigned long long> h(ns * 16);
+    cudaMemcpyAsync(h.data(), gt.tl, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(gt.tl, s);
+    double ph[8] = {0};
+    unsigned long long lo = ~0ull, hi = 0;
+    for (size_t b = 0; b < ns; ++b) {
+      for (int i = 0; i < 8; ++i) ph[i] += (double)(h[b * 16 + i + 1] - h[b * 16 + i]);
+      lo = std::min(lo, h[b * 16]);
+      hi = std::max(hi, h[b * 16 + 8]);
+    }
+    const char* names[8] = {"load", "filter", "adler+parse", "rank sort", "huffman", "header||bits+scan", "write", "copy out"};
+    fprintf(stderr, "png_strip timing: %zu strips, span %.3f ms; mean per strip (us):", ns, (hi - lo) * 1e-6);
+    for (int i = 0; i < 8; ++i) fprintf(stderr, " %s %.1f", names[i], ph[i] / ns * 1e-3);
+    fprintf(stderr, "\n");
+  }
   png_image_kernel<<<n, kT, 0, s>>>(g, scratch, meta, offs, sizes);
   png_frame_kernel<<<1, kT, 0, s>>>(g, sizes, bases, out, stride, contiguous ? 1 : 0);
   png_chunk_kernel<<<(unsigned)ns, kT, g.cap + 32, s>>>(g, scratch, meta, offs, bases, out);
