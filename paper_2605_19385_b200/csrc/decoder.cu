@@ -9,8 +9,8 @@
 // activations / shortcut / upsample output), H (conv1 output, normalised in place; attention QKV):
 //   prep(latents) -> A ; conv_in(A) -> X
 //   Res: A = SiLU(GN1(X)); H = conv1(A); H = SiLU(GN2(H)); [A = shortcut(X)]; X = conv2(H) + X|A
-//   Attn: A = GN(X); H = A Wqkv^T; per image: S = QK^T/sqrt(d); P = exp(S - max); O = P V / sum
-//         -> A; X = A Wo^T + bo + X
+//   Attn: A = GN(X); H = A Wqkv^T; per group of up to 8 images (one launch each): S = QK^T/sqrt(d);
+//         P = exp(S - max); O = P V / sum (V read in place, MN-major) -> A; X = A Wo^T + bo + X
 //   Up:   A = subpixel_conv(X) (nearest-2x + conv3x3 in 4 phases); swap(X, A)
 //   tail: rgb = u8(conv_out(SiLU(GN(X))))
 // Every conv epilogue accumulates the GroupNorm-32 statistics its consumer needs.
