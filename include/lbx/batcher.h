@@ -37,6 +37,9 @@ typedef struct {
   uint32_t max_batch;          /* per-launch batch cap (also the decoders' arena size) */
   uint32_t max_wait_us;        /* close a partial batch once its oldest request waited this long */
   uint64_t weight_seed;        /* decoder weights (deterministic generator) */
+  uint32_t policy;             /* 0 (default): close batches of up to max_batch (greedy); 1: each worker
+                                  measures its device's service curve at creation and closes the batch
+                                  size lbx_batch_pick chooses (no batching when it does not pay) */
 } lbx_batcher_desc;
 
 typedef struct {
@@ -63,6 +66,14 @@ int lbx_batcher_poll(lbx_batcher* b, lbx_completion* out, int cap, uint32_t wait
 
 /* Requests submitted but not yet returned by poll. */
 uint64_t lbx_batcher_pending(lbx_batcher* b);
+
+/* Batch size to close from `queued` waiting requests, 1 <= result <= min(queued, max_batch) (0 if
+ * queued == 0), given a service curve cost_ms[b-1] = GPU time of a batch of b, b = 1..n_cost
+ * (extended linearly past n_cost): the size with the lowest GPU time per request, where a larger
+ * batch must beat the best smaller one by 2%.  cost_ms == NULL: min(queued, max_batch) (greedy).
+ * On B200 the decode's time per image is flat in the batch size, so this returns 1 and batching
+ * adds only latency; on engines with a fixed per-launch cost it batches. */
+uint32_t lbx_batch_pick(const double* cost_ms, uint32_t n_cost, uint32_t queued, uint32_t max_batch);
 
 /* Steady-clock microseconds, the time base of lbx_completion. */
 uint64_t lbx_now_us(void);

@@ -323,7 +323,7 @@ class Shape(ctypes.Structure):
 class BatcherDesc(ctypes.Structure):
     _fields_ = [("devices", ctypes.POINTER(ctypes.c_int)), ("n_devices", ctypes.c_int),
                 ("shapes", ctypes.POINTER(Shape)), ("n_shapes", ctypes.c_int), ("max_batch", ctypes.c_uint32),
-                ("max_wait_us", ctypes.c_uint32), ("weight_seed", ctypes.c_uint64)]
+                ("max_wait_us", ctypes.c_uint32), ("weight_seed", ctypes.c_uint64), ("policy", ctypes.c_uint32)]
 
 
 class Completion(ctypes.Structure):
@@ -347,6 +347,9 @@ def _batcher_lib():
         L.lbx_batcher_pending.argtypes = [vp]
         L.lbx_batcher_pending.restype = ctypes.c_uint64
         L.lbx_now_us.restype = ctypes.c_uint64
+        L.lbx_batch_pick.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_uint32, ctypes.c_uint32,
+                                     ctypes.c_uint32]
+        L.lbx_batch_pick.restype = ctypes.c_uint32
         L._batcher_ready = True
     return L
 
@@ -354,11 +357,14 @@ def _batcher_lib():
 class Batcher:
     """Multi-GPU request batcher: one worker + decoder per (device, shape class)."""
 
-    def __init__(self, devices, shapes, max_batch=32, max_wait_us=5000, seed=0):
+    def __init__(self, devices, shapes, max_batch=32, max_wait_us=5000, seed=0, policy="greedy"):
+        """policy "greedy": batches of up to max_batch; "cost": the size lbx_batch_pick chooses from
+        each device's measured service curve."""
         L = _batcher_lib()
         self._devs = (ctypes.c_int * len(devices))(*devices)
         self._shapes = (Shape * len(shapes))(*[Shape(FAMILY[f], h, w) for f, h, w in shapes])
-        d = BatcherDesc(self._devs, len(devices), self._shapes, len(shapes), max_batch, max_wait_us, seed)
+        d = BatcherDesc(self._devs, len(devices), self._shapes, len(shapes), max_batch, max_wait_us, seed,
+                        {"greedy": 0, "cost": 1}[policy])
         h = ctypes.c_void_p()
         check(L.lbx_batcher_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
@@ -394,6 +400,15 @@ class Batcher:
             self.close()
         except Exception:
             pass
+
+
+def batch_pick(cost_ms, queued: int, max_batch: int) -> int:
+    """lbx_batch_pick: batch size to close from `queued` requests given cost_ms[b-1] (None: greedy)."""
+    L = _batcher_lib()
+    if cost_ms is None:
+        return int(L.lbx_batch_pick(None, 0, queued, max_batch))
+    arr = (ctypes.c_double * len(cost_ms))(*cost_ms)
+    return int(L.lbx_batch_pick(arr, len(cost_ms), queued, max_batch))
 
 
 def now_us() -> int:

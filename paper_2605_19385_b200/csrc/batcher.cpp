@@ -5,7 +5,11 @@
 // whose head request is oldest.  It does so once that queue holds max_batch requests, once the head
 // has waited max_wait_us, or when draining at shutdown.  Then it runs one lbx_reconstruct_v.  Pulling
 // work only when idle is what makes the placement least-loaded-first (proj/src/sim.cpp:238-243);
-// the FIFO order per shape mirrors the simulator's FIFO GPU (sim.cpp:413).
+// the FIFO order per shape mirrors the simulator's FIFO GPU (sim.cpp:413).  With policy 1 the batch
+// size comes from lbx_batch_pick over the worker's own measured service curve.
+#include <cuda_runtime.h>
+
+#include <algorithm>
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
@@ -16,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "lbx/batch_pick.h"
 #include "lbx/batcher.h"
 
 namespace lbx {
@@ -57,9 +62,50 @@ struct lbx_batcher {
   void worker(int dev_index);
 };
 
+namespace {
+
+// GPU time of one decode of b latents, b = 1..max_b (measured at 1, 2, 4, ... and max_b, linear in
+// between): device-resident latents, so the curve is the decode alone
+std::vector<double> measure_curve(lbx_decoder* dec, int fam_channels, uint32_t lh, uint32_t lw, uint32_t max_b) {
+  std::vector<double> pts_b, pts_ms;
+  void* lat = nullptr;
+  uint8_t* rgb = nullptr;
+  const size_t lat_bytes = (size_t)max_b * fam_channels * lh * lw * 2, rgb_bytes = (size_t)max_b * 64 * lh * lw * 3;
+  if (cudaMalloc(&lat, lat_bytes) != cudaSuccess || cudaMalloc(reinterpret_cast<void**>(&rgb), rgb_bytes) != cudaSuccess) {
+    if (lat) cudaFree(lat);
+    return {};
+  }
+  cudaMemset(lat, 0, lat_bytes);
+  for (uint32_t b = 1;; b = std::min(2 * b, max_b)) {
+    lbx_decode(dec, lat, b, rgb, nullptr);  // graph already captured by lbx_decoder_prepare
+    cudaDeviceSynchronize();
+    const int reps = b <= 4 ? 4 : 2;
+    const uint64_t t0 = now_us();
+    for (int r = 0; r < reps; ++r) lbx_decode(dec, lat, b, rgb, nullptr);
+    cudaDeviceSynchronize();
+    pts_b.push_back(b);
+    pts_ms.push_back((now_us() - t0) / 1000.0 / reps);
+    if (b == max_b) break;
+  }
+  cudaFree(lat);
+  cudaFree(rgb);
+  std::vector<double> c(max_b);
+  for (uint32_t b = 1; b <= max_b; ++b) {
+    size_t k = 0;
+    while (k + 1 < pts_b.size() && pts_b[k + 1] < b) ++k;
+    if (k + 1 >= pts_b.size() || pts_b[k] == b) { c[b - 1] = pts_ms[k]; continue; }
+    const double f = (b - pts_b[k]) / (pts_b[k + 1] - pts_b[k]);
+    c[b - 1] = pts_ms[k] + f * (pts_ms[k + 1] - pts_ms[k]);
+  }
+  return c;
+}
+
+}  // namespace
+
 void lbx_batcher::worker(int di) {
   const int device = devices[di];
   std::vector<lbx_decoder*> decs(shapes.size(), nullptr);
+  std::vector<std::vector<double>> curves(shapes.size());  // policy 1: this device's service curves
   lbx_status st = LBX_OK;
   for (size_t s = 0; s < shapes.size() && st == LBX_OK; ++s) {
     lbx_decoder_desc d{};
@@ -71,6 +117,11 @@ void lbx_batcher::worker(int di) {
     d.max_batch = desc.max_batch;
     st = lbx_decoder_create(&d, &decs[s]);
     if (st == LBX_OK) st = lbx_decoder_prepare(decs[s], desc.max_batch);  // no capture on the request path
+    if (st == LBX_OK && desc.policy == 1) {
+      const int ch = shapes[s].family == LBX_FAMILY_SD15 ? 4 : 16;
+      curves[s] = measure_curve(decs[s], ch, shapes[s].latent_h, shapes[s].latent_w, desc.max_batch);
+      if (curves[s].empty()) st = LBX_E_CUDA;
+    }
   }
   {
     std::lock_guard<std::mutex> g(mu);
@@ -111,7 +162,9 @@ void lbx_batcher::worker(int di) {
       }
       if (shape < 0) break;  // stopping and drained
       auto& q = queues[shape];
-      const size_t take = q.size() < desc.max_batch ? q.size() : desc.max_batch;
+      const auto& cv = curves[shape];
+      const size_t take = lbx_batch_pick(cv.empty() ? nullptr : cv.data(), (uint32_t)cv.size(), (uint32_t)q.size(),
+                                         desc.max_batch);
       batch.clear();
       for (size_t i = 0; i < take; ++i) {
         batch.push_back(std::move(q.front()));
@@ -147,6 +200,10 @@ void lbx_batcher::worker(int di) {
 extern "C" {
 
 uint64_t lbx_now_us(void) { return now_us(); }
+
+uint32_t lbx_batch_pick(const double* cost_ms, uint32_t n_cost, uint32_t queued, uint32_t max_batch) {
+  return lbx_batch_pick_rule(cost_ms, n_cost, queued, max_batch);
+}
 
 lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out) {
   if (!desc || !out || desc->n_devices <= 0 || !desc->devices || desc->n_shapes <= 0 || !desc->shapes ||

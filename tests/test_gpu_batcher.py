@@ -53,3 +53,25 @@ def test_batcher_two_shape_classes(lbx):
     for i in range(3):
         assert np.array_equal(outs[i], ra[i]) and np.array_equal(outs[10 + i], rb[i])
     b.close()
+
+
+def test_batcher_cost_policy(lbx):
+    """policy "cost": each worker measures its service curve at creation and closes the batch size
+    lbx_batch_pick chooses; on B200 (time per image flat in the batch size) that is 1."""
+    z = weights_ref.make_latents("sd3", 6, 64, 64, seed=34)
+    blobs = [lbx.pack(z[i], 1) for i in range(6)]
+    ref = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=6).reconstruct(blobs)
+    b = lbx.Batcher([0], [("sd3", 64, 64)], max_batch=8, max_wait_us=0, policy="cost")
+    outs = [np.zeros((512, 512, 3), dtype=np.uint8) for _ in range(6)]
+    for i in range(6):
+        b.submit(i, 0, blobs[i], outs[i])
+    done = []
+    for _ in range(400):
+        done += b.poll(wait_us=50000)
+        if len(done) == 6:
+            break
+    assert sorted(c["id"] for c in done) == list(range(6))
+    assert all(c["status"] == 0 and 1 <= c["batch"] <= 8 for c in done)
+    for i in range(6):
+        assert np.array_equal(outs[i], ref[i]), i
+    b.close()

@@ -32,6 +32,7 @@ struct Opts {
   double window_start = 0.6;   // live: window start as a fraction of the trace duration
   int n_devices = 1;
   std::string service;         // "ms1,ms2,ms4,ms8,ms16,ms32" (sim mode); empty = defaults
+  std::string policy = "cost"; // batch sizing: "cost" (lbx_batch_pick over the curve) or "greedy"
   std::string json;
   std::string dump;            // live: per-job "submit_ms start_ms end_ms batch" lines (diagnostics)
 };
@@ -76,6 +77,7 @@ bool parse(int argc, char** argv, Opts& o) {
     else if (k == "--window-s") o.window_s = std::stod(v);
     else if (k == "--window-start") o.window_start = std::stod(v);
     else if (k == "--service") o.service = v;
+    else if (k == "--policy") o.policy = v;
     else if (k == "--json") o.json = v;
     else if (k == "--dump") o.dump = v;
     else {
@@ -158,7 +160,8 @@ int main(int argc, char** argv) {
     std::fprintf(stderr,
                  "usage: c5_replay sim|live [--scale S] [--gpus G] [--devices D] [--max-batch B] [--max-wait-ms W]\n"
                  "       [--days N] [--rpd R] [--objects N] [--seed S] [--cache-frac F] [--window-s S]\n"
-                 "       [--window-start F] [--service m1,m2,m4,m8,m16,m32] [--json out.json]\n");
+                 "       [--window-start F] [--service m1,m2,m4,m8,m16,m32] [--policy cost|greedy]\n"
+                 "       [--json out.json]\n");
     return 2;
   }
   double pts[6];
@@ -178,6 +181,7 @@ int main(int argc, char** argv) {
     }
   }
   o.rp.service_ms = curve_from(pts, o.rp.max_batch);
+  o.rp.cost_policy = o.policy == "cost";
 
   const double t0 = now_ms();
   const lbsim::Workload w = lbsim::synth(o.synth);
@@ -192,12 +196,13 @@ int main(int argc, char** argv) {
   int len = std::snprintf(
       buf, sizeof buf,
       "{\"config\": \"c5\", \"mode\": \"%s\", \"requests\": %.0f, \"objects\": %llu, \"time_scale\": %g, \"gpus\": %d, "
-      "\"max_batch\": %d, \"max_wait_ms\": %g, \"cache_frac\": %g, \"mix\": {\"image_hit\": %.4f, "
+      "\"max_batch\": %d, \"policy\": \"%s\", \"max_wait_ms\": %g, \"cache_frac\": %g, \"mix\": {\"image_hit\": %.4f, "
       "\"latent_hit\": %.4f, \"full_miss\": %.4f, \"coalesced\": %.4f}, \"final_alpha\": %.4f, \"windows\": %llu, "
       "\"service_ms\": [%.2f, %.2f, %.2f, %.2f, %.2f, %.2f], \"sim\": {\"decode_p50_ms\": %.2f, \"decode_p99_ms\": "
       "%.2f, \"decode_mean_ms\": %.2f, \"e2e_p50_ms\": %.2f, \"e2e_p99_ms\": %.2f, \"e2e_mean_ms\": %.2f, "
       "\"decodes\": %llu, \"mean_batch\": %.2f}",
       o.mode.c_str(), n, (unsigned long long)w.objects_total, o.rp.time_scale, o.rp.gpus, o.rp.max_batch,
+      o.rp.cost_policy ? "cost" : "greedy",
       o.rp.max_wait_ms, o.rp.cache_frac, r.image_hits / n, r.latent_hits / n, r.full_misses / n, r.coalesced / n,
       r.final_alpha, (unsigned long long)r.windows, pts[0], pts[1], pts[2], pts[3], pts[4], pts[5], rep.decode_p50,
       rep.decode_p99, rep.decode_mean, rep.e2e_p50, rep.e2e_p99, rep.e2e_mean, (unsigned long long)rep.n_decodes,
@@ -216,18 +221,20 @@ int main(int argc, char** argv) {
     for (int i = 0; i < o.n_devices; ++i) devs[i] = i;
     lbx_shape shape{LBX_FAMILY_SD3, 128, 128};
     lbx_batcher_desc bd{devs.data(), o.n_devices, &shape, 1, (uint32_t)o.rp.max_batch,
-                        (uint32_t)(o.rp.max_wait_ms * 1000.0), 0};
+                        (uint32_t)(o.rp.max_wait_ms * 1000.0), 0, o.rp.cost_policy ? 1u : 0u};
     lbx_batcher* b = nullptr;
     if (lbx_batcher_create(&bd, &b) != LBX_OK) {
       std::fprintf(stderr, "batcher: %s\n", lbx_last_error());
       return 1;
     }
     const size_t img = 1024ull * 1024 * 3;
-    const int nbuf = 4 * o.rp.max_batch * o.n_devices;
+    // output buffers in flight: enough that small batch caps never stall submission
+    const int nbuf = std::max(64, 4 * o.rp.max_batch) * o.n_devices;
     std::vector<uint8_t> pool((size_t)nbuf * img);
     std::vector<int> free_bufs;
     for (int i = nbuf - 1; i >= 0; --i) free_bufs.push_back(i);
     std::vector<int> buf_of(jobs.size(), -1);
+    std::vector<double> lag(jobs.size(), 0.0);  // submit - due (ms): a stalled submission still counts
     std::vector<double> live_dec, sim_dec;
     std::vector<lbx_completion> all_comp;
     std::vector<lbx_completion> comp(512);
@@ -236,7 +243,7 @@ int main(int argc, char** argv) {
       const int k = lbx_batcher_poll(b, comp.data(), (int)comp.size(), wait_us);
       for (int i = 0; i < k; ++i) {
         const size_t q = comp[i].request_id;
-        live_dec.push_back((comp[i].t_end_us - comp[i].t_submit_us) / 1000.0);
+        live_dec.push_back((comp[i].t_end_us - comp[i].t_submit_us) / 1000.0 + lag[q]);
         if (!o.dump.empty()) all_comp.push_back(comp[i]);
         free_bufs.push_back(buf_of[q]);
       }
@@ -254,6 +261,7 @@ int main(int argc, char** argv) {
       }
       buf_of[q] = free_bufs.back();
       free_bufs.pop_back();
+      lag[q] = std::max(0.0, now_ms() - due);
       const auto& blob = blobs[J.object_id % blobs.size()];
       lbx_batcher_submit(b, q, 0, blob.data(), blob.size(), pool.data() + (size_t)buf_of[q] * img);
       sim_dec.push_back(J.t_end - J.t_ready);

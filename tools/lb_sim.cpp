@@ -1,5 +1,6 @@
 // Config-5 harness: restated workload / cache / tuner / coalescing and the virtual-time batched
 // decode service model.  See lb_sim.hpp for the reference mapping (file:line).
+#include "../include/lbx/batch_pick.h"  // the live batcher's rule
 #include "lb_sim.hpp"
 
 #include <algorithm>
@@ -334,9 +335,14 @@ ReplayOut replay(const Workload& w, const ReplayCfg& cfg) {
         fetch_q.pop();
         continue;
       }
-      uint32_t b = 0;
+      uint32_t b = 0, lim = (uint32_t)cfg.max_batch;
+      if (cfg.cost_policy && !cfg.service_ms.empty()) {  // the live batcher's rule (lbx_batch_pick)
+        uint32_t q = 0;
+        while (q < ready.size() && (int)q < cfg.max_batch && out.jobs[ready[q]].t_ready <= t_batch) ++q;
+        lim = lbx_batch_pick_rule(cfg.service_ms.data(), (uint32_t)cfg.service_ms.size(), q, (uint32_t)cfg.max_batch);
+      }
       std::vector<int> batch;
-      while (!ready.empty() && (int)b < cfg.max_batch && out.jobs[ready.front()].t_ready <= t_batch) {
+      while (!ready.empty() && b < lim && out.jobs[ready.front()].t_ready <= t_batch) {
         batch.push_back(ready.front());
         ready.pop_front();
         ++b;

@@ -123,6 +123,7 @@ struct ReplayCfg {
   int max_batch = 32;
   double max_wait_ms = 0.0;        // 0 = work-conserving: an idle GPU takes whatever is queued
   std::vector<double> service_ms;   // service_ms[b-1] = GPU time of a batch of b (measured)
+  bool cost_policy = false;         // batch size by lbx_batch_pick over service_ms (else greedy)
 };
 
 // A decode job: the leader request of an in-flight object (LatentHit or FullMiss).
