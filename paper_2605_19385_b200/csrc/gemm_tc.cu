@@ -63,6 +63,7 @@ struct KParams {
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
   int rpf_pf;          // 1: L2-prefetch the next preload's rows before waiting for the accumulator
   int sched;           // 1: each cluster takes a contiguous block of tiles (conv modes), 0: round-robin
+  int pdl;             // 1: launched as a programmatic dependent (wait before any global access)
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
@@ -218,6 +219,9 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
+  // programmatic dependent launch: the prologue above overlapped the previous kernel's tail; from
+  // here on global memory is touched, so wait for that kernel to complete and flush
+  if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -749,6 +753,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     if (p.tstore && lane == 0) ptx::bulk_wait_all();
   }
 
+  if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // this CTA's work is done
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
   if (warp == 1) {
@@ -823,6 +828,7 @@ static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel inst
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
+static int g_pdl_policy = 0;       // 1: programmatic dependent launch of the GEMM kernels (bit 23)
 static int g_sched_policy = 0;     // 1: contiguous tile blocks per cluster for conv modes (bit 22 sets;
                                    // measured worse: c128 conv reads 25.5 vs 23.0 GB from DRAM, the
                                    // vertical halo reuse distance outlives L2; decode time neutral)
@@ -847,6 +853,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
   g_rpf_pf = (halo_policy >> 21) & 1;
   g_sched_policy = (halo_policy >> 22) & 1;
+  g_pdl_policy = (halo_policy >> 23) & 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -935,13 +942,18 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   cfg.blockDim = dim3(XF ? Cf::THREADS_XF : Cf::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (kp.pdl) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, tmA2, tmO, kp);
 }
 
@@ -972,6 +984,7 @@ bool gemm_tc_prepare() {  // per device (a multi-GPU batcher drives several from
 bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
 bool resid_preload() { return g_rpf_policy != 0; }
+bool pdl_enabled() { return g_pdl_policy != 0; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments); four extra warps transform each landed halo
@@ -1029,6 +1042,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
             (g_rpf_policy == 2 || a.N <= 128)) ? 1 : 0;
   kp.rpf_pf = g_rpf_pf;
   kp.sched = (g_sched_policy && a.mode != GEMM_PLAIN) ? 1 : 0;
+  kp.pdl = g_pdl_policy;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||

@@ -70,6 +70,9 @@ bool resid_preload();
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();
+// programmatic dependent launch of the decode's kernels (debug bit 23); kernels that support it wait
+// (griddepcontrol.wait) before their first global access and trigger their dependents when done
+bool pdl_enabled();
 
 // fp16 tiled TMA descriptor with 128-byte swizzle (dims innermost first; strides in bytes for
 // dims 1..rank-1).  Out-of-bounds boxes are zero-filled.

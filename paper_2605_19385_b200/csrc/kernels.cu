@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
     ptx::fence_mbar_init();
   }
   __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // no-op unless launched as a PDL dependent
   const uint8_t* src = reinterpret_cast<const uint8_t*>(x);
   uint8_t* dst = reinterpret_cast<uint8_t*>(y);
   const long long first = blockIdx.x, step = gridDim.x;
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
     }
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 static bool g_apply_bulk = true;  // bulk-copy apply (debug bit 8 selects the register-staged one)
@@ -229,7 +231,17 @@ static bool gn_apply_bulk_launch(const __half* x, __half* y, const GnSrc& g, int
   if (!ensure_smem_attr(reinterpret_cast<const void*>(gn_apply_bulk_kernel<SILU, CV, H2>), smem)) return false;
   const long long chunks = (long long)n * img_bytes / kApChunk;
   const int grid = (int)(chunks < num_sms() ? chunks : num_sms());
-  gn_apply_bulk_kernel<SILU, CV, H2><<<grid, 256, smem, s>>>(x, y, g, img_bytes, chunks);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, gn_apply_bulk_kernel<SILU, CV, H2>, x, y, g, img_bytes, chunks);
   return true;
 }
 
