@@ -127,6 +127,14 @@ lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, co
 lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
                                  size_t stride, uint32_t* sizes_dev, lbx_stream stream);
 
+/* Unpack of LBLP blobs already in device memory (e.g. an HBM-resident latent tier): blob i at
+ * blobs_dev + offs_dev[i] (8-byte aligned), sizes_dev[i] bytes; out_dev = n fp16 NCHW latents of
+ * c x h x w.  A malformed blob sets *err_dev (device int, zero it first) to a nonzero code and leaves
+ * that latent unspecified.  Bit-exact with lbx_unpack.  Asynchronous on `stream`. */
+lbx_status lbx_op_unpack(const uint8_t* blobs_dev, const unsigned long long* offs_dev, const uint32_t* sizes_dev,
+                         uint32_t n, uint32_t c, uint32_t h, uint32_t w, void* out_dev, int* err_dev,
+                         lbx_stream stream);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* lbx_last_error(void);
 

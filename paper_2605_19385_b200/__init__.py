@@ -29,7 +29,7 @@ SYMBOLS = [
     "lbx_reconstruct", "lbx_reconstruct_latents", "lbx_pack", "lbx_last_error", "lbx_op_gemm",
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
     "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
-    "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png",
+    "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png", "lbx_op_unpack",
 ]
 
 
@@ -114,6 +114,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_png_bound.restype = ctypes.c_size_t
     L.lbx_png_encode_device.argtypes = [vp, u32, u32, u32, vp, ctypes.c_size_t, vp, vp]
     L.lbx_reconstruct_png.argtypes = [vp, vp, vp, u32, vp, ctypes.c_size_t, vp, vp]
+    L.lbx_op_unpack.argtypes = [vp, vp, vp, u32, u32, u32, u32, vp, vp, vp]
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error", "lbx_pack_bound", "lbx_png_bound"):
             getattr(L, name).restype = ctypes.c_int
@@ -299,6 +300,11 @@ def pack_bound(c: int, h: int, w: int) -> int:
 def pack_device(latents_ptr, n, c, h, w, out_ptr, stride, sizes_ptr, stream=0):
     """Device-side LBLP mode-1 pack (lbx_pack_device): blob i at out + i*stride, size in sizes[i]."""
     check(lib().lbx_pack_device(latents_ptr, n, c, h, w, out_ptr, stride, sizes_ptr, stream or None))
+
+
+def op_unpack(blobs_ptr, offs_ptr, sizes_ptr, n, c, h, w, out_ptr, err_ptr, stream=0):
+    """Device-resident LBLP blobs -> fp16 latents (lbx_op_unpack)."""
+    check(lib().lbx_op_unpack(blobs_ptr, offs_ptr, sizes_ptr, n, c, h, w, out_ptr, err_ptr, stream or None))
 
 
 def png_bound(h: int, w: int) -> int:

@@ -1048,6 +1048,22 @@ lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h,
   return LBX_OK;
 }
 
+lbx_status lbx_op_unpack(const uint8_t* blobs_dev, const unsigned long long* offs_dev, const uint32_t* sizes_dev,
+                         uint32_t n, uint32_t c, uint32_t h, uint32_t w, void* out_dev, int* err_dev,
+                         lbx_stream stream) {
+  if (n == 0) return LBX_OK;
+  if (!blobs_dev || !offs_dev || !sizes_dev || !out_dev || !err_dev)
+    return set_err(LBX_E_CONFIG, "lbx_op_unpack: null pointer");
+  if (c == 0 || h == 0 || w == 0 || w % 32 || c > 65535 || h > 65535 || w > 65535)
+    return set_err(LBX_E_CONFIG, "lbx_op_unpack: shape must be nonzero, <= 65535, w % 32 == 0");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  lbx::launch_lblp_unpack(blobs_dev, offs_dev, reinterpret_cast<const unsigned int*>(sizes_dev), (int)n, (int)c,
+                          (int)h, (int)w, reinterpret_cast<__half*>(out_dev), err_dev, s);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("lbx_op_unpack: ") + cudaGetErrorString(e));
+  return LBX_OK;
+}
+
 lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
                            int H, int W, int impl, lbx_stream stream) {
   if (!x || !ss || !w || !b || !rgb || n <= 0 || H <= 0 || W <= 0)
@@ -1072,6 +1088,7 @@ lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
   lbx::gemm_tc_set_debug(halo_policy, desc_base_mode);
   lbx::kernels_set_conv_out_legacy((halo_policy >> 4) & 1);
   lbx::kernels_set_apply_bulk(!((halo_policy >> 8) & 1));
+  lbx::kernels_set_unpack_rows((halo_policy >> 24) & 1);
   return LBX_OK;
 }
 

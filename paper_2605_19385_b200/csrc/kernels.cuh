@@ -58,6 +58,7 @@ void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaS
 // LBLP v1 device unpack (include/lbx/lblp.h).  `blobs` is one device buffer holding n blobs at
 // byte offsets `offs[i]` (device array); output fp16 NCHW [n][C][H][W].  Any malformed blob sets
 // *err (device int) to a nonzero code; the output of that latent is then unspecified (zeros).
+void kernels_set_unpack_rows(bool on);  // debug bit 24: the row-per-warp unpack kernel
 void launch_lblp_unpack(const uint8_t* blobs, const unsigned long long* offs, const unsigned int* sizes, int n,
                         int C, int H, int W, __half* out, int* err, cudaStream_t s);
 

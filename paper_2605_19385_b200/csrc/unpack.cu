@@ -8,8 +8,12 @@
 
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace lbx {
+
+static bool g_unpack_rows = false;  // row kernel instead of the plane kernel (diagnostics)
+void kernels_set_unpack_rows(bool on) { g_unpack_rows = on; }
 
 __device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) { return *reinterpret_cast<const uint32_t*>(p); }
 __device__ __forceinline__ uint16_t ld_u16(const uint8_t* p) { return *reinterpret_cast<const uint16_t*>(p); }
@@ -109,8 +113,355 @@ __global__ void __launch_bounds__(256) lblp_unpack_kernel(const uint8_t* __restr
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Plane kernel (the default for planes of <= kPlaneMaxVals values): one CTA per (latent, channel)
+// plane.  Thread 0 validates the 32-byte header once for the plane; mode-1 rows are staged into
+// shared memory with independent 32-bit loads (the whole plane's compressed bytes in flight at
+// once instead of a dependent chain per row), decoded there one warp per row, and the plane is
+// written back with 16-byte stores.  Modes 0 / 2 stream straight through with vector loads.  A row
+// whose table offset lies outside the staged range (a valid but non-canonical layout) is decoded
+// from global memory.  Bit-exact with the row kernel above; same error codes.
+constexpr int kPlaneMaxVals = 16384;           // 128 x 128
+constexpr int kPlaneInBytes = 34 * 1024 + 64;  // mode-1 plane at 128 x 128: <= 128 x 264 B
+constexpr int kPlaneThreads = 256;  // decode threads (W/32 per mode-1 row) + one producer warp
+
+// decode one mode-1 row (W values) on ONE lane: the prefix sum runs sequentially in registers over
+// a 64-bit bit reader (no warp shuffles); 8 values per 16-byte store to `dst` (global, 16-byte
+// aligned).  Bounds as in the row kernel; on an error the caller zeroes the row.
+__device__ __forceinline__ int decode_row_lane(const uint8_t* row, uint32_t avail, int W, uint16_t* dst) {
+  const uint32_t head = (2u + (uint32_t)(W / 32) + 3u) & ~3u;
+  if (avail < head) return 4;
+  uint32_t prev = omap(*reinterpret_cast<const uint16_t*>(row));
+  uint32_t wpos = head;
+  uint4* d16 = reinterpret_cast<uint4*>(dst);
+  for (int j = 0; j < W / 32; ++j) {
+    const uint32_t bw = row[2 + j];
+    if (bw > 16 || wpos + 4ull * bw > avail) return 4;
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(row + wpos);
+    const uint32_t mask = (1u << bw) - 1u;
+    uint64_t buf = 0;
+    uint32_t nb = 0, wi = 0;
+    uint32_t pk[16];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (nb < bw) {
+        buf |= (uint64_t)wp[wi++] << nb;
+        nb += 32;
+      }
+      const uint32_t z = (uint32_t)buf & mask;
+      buf >>= bw;
+      nb -= bw;
+      const uint32_t d = (j == 0 && k == 0) ? 0u : (uint32_t)(uint16_t)((z >> 1) ^ (uint32_t)(-(int)(z & 1)));
+      prev = (prev + d) & 0xFFFFu;
+      const uint32_t h = omap_inv((uint16_t)prev);
+      if (k & 1) pk[k >> 1] |= h << 16; else pk[k >> 1] = h;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d16[4 * j + q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    wpos += 4u * bw;
+  }
+  return 0;
+}
+
+// decode one mode-1 row on L = W/32 lanes (a power of two <= 32): lane j of the row's segment
+// takes mini-block j -- widths prefix, bit extraction and a register prefix sum of its 32 deltas --
+// then a segmented shuffle scan across the L lanes supplies each block's carry-in.  Every lane of
+// the warp must call it (inactive rows pass active = false).  Returns the row's error code
+// (uniform over the segment); on an error nothing is stored.
+__device__ __forceinline__ int decode_row_split(const uint8_t* row, uint32_t avail, int L, int lane, bool active,
+                                                uint16_t* dst) {
+  const int j = lane & (L - 1);
+  const uint32_t head = (2u + (uint32_t)L + 3u) & ~3u;
+  const bool hok = active && avail >= head;
+  const uint32_t bits0 = hok ? *reinterpret_cast<const uint16_t*>(row) : 0u;
+  const uint32_t bw = hok ? row[2 + j] : 0u;
+  uint32_t incl = bw;
+  for (int o = 1; o < L; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, incl, o, L);
+    if (j >= o) incl += u;
+  }
+  const uint32_t wpos = head + 4u * (incl - bw);
+  const bool bad = active && (!hok || bw > 16 || wpos + 4ull * bw > avail);
+  const uint32_t seg = (uint32_t)(lane & ~(L - 1));
+  const uint32_t gmask = (L == 32 ? 0xffffffffu : ((1u << L) - 1u)) << seg;
+  const bool seg_bad = (__ballot_sync(0xffffffffu, bad) & gmask) != 0;
+  uint32_t sv[16];  // running sums mod 2^16, two per register
+  uint32_t acc = 0;
+  if (active && !seg_bad) {
+    const uint32_t* wp = reinterpret_cast<const uint32_t*>(row + wpos);
+    const uint32_t mask = (1u << bw) - 1u;
+    uint64_t buf = 0;
+    uint32_t nb = 0, wi = 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (nb < bw) {
+        buf |= (uint64_t)wp[wi++] << nb;
+        nb += 32;
+      }
+      const uint32_t z = (uint32_t)buf & mask;
+      buf >>= bw;
+      nb -= bw;
+      const uint32_t d = (j == 0 && k == 0) ? 0u : ((z >> 1) ^ (uint32_t)(-(int)(z & 1)));
+      acc += d;
+      if (k & 1) sv[k >> 1] |= (acc & 0xFFFFu) << 16; else sv[k >> 1] = acc & 0xFFFFu;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sv[k] = 0;
+  }
+  // carry-in of block j: omap(bits0) + the totals of blocks 0..j-1 (mod 2^16)
+  uint32_t tin = acc;
+  for (int o = 1; o < L; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, tin, o, L);
+    if (j >= o) tin += u;
+  }
+  if (!active || seg_bad) return seg_bad ? 4 : 0;
+  const uint32_t off = (uint32_t)omap((uint16_t)bits0) + tin - acc;
+  uint32_t pk[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t a = omap_inv((uint16_t)(off + (sv[k] & 0xFFFFu))), b = omap_inv((uint16_t)(off + (sv[k] >> 16)));
+    pk[k] = a | b << 16;
+  }
+  uint4* d16 = reinterpret_cast<uint4*>(dst + 32 * j);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) d16[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  return 0;
+}
+
+__device__ __forceinline__ void ubulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   ptx::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(ptx::smem_u32(bar))
+               : "memory");
+}
+
+struct PlaneInfo {
+  int code, mode;
+  uint32_t start, bytes;  // mode 1: the plane's canonical byte range (bytes = 0: rows from global)
+  uint32_t payload, nbytes;
+  uint32_t lo;            // staged copy of [lo, start + bytes) at the buffer's base (lo = start & ~15)
+  int use_bar;            // the bulk part of the copy completes on the buffer's mbarrier
+};
+
+// thread 0: validate the plane's header, and for mode 1 start staging its rows into `buf`
+__device__ void plane_prep(const uint8_t* base, uint32_t nbytes, bool aligned16, int c, int C, int H, int W,
+                           PlaneInfo& pi, uint8_t* buf, uint64_t* bar) {
+  int code = 0, mode = -1;
+  uint32_t start = 0, bytes = 0, table = 0, payload = 0;
+  if (nbytes < 32 || base[0] != 'L' || base[1] != 'B' || base[2] != 'L' || base[3] != 'P' || base[4] != 1 ||
+      base[5] != 1)
+    code = 2;
+  else if (ld_u16(base + 8) != C || ld_u16(base + 10) != H || ld_u16(base + 12) != W)
+    code = 3;
+  else if (ld_u32(base + 16) != nbytes)
+    code = 4;
+  if (!code) {
+    mode = base[6];
+    table = ld_u32(base + 20);
+    payload = ld_u32(base + 24);
+    const long long rows_per = (long long)C * H;
+    if (mode == 0) {
+      if (payload != 32 || 32ull + 2ull * rows_per * W > nbytes) code = 4;
+    } else if (mode == 2) {
+      if (table != 32 || payload != 32u + 8u * (uint32_t)C || (unsigned long long)payload + rows_per * W > nbytes)
+        code = 4;
+    } else if (mode == 1) {
+      if ((W & 31) || table != 32 || payload != 32u + 4u * (uint32_t)rows_per || payload > nbytes) {
+        code = 4;
+      } else {  // canonical layout: this plane's rows are contiguous from row c*H's offset
+        const uint32_t r0 = ld_u32(base + 32 + 4 * (c * H));
+        const uint32_t r1 = c + 1 < C ? ld_u32(base + 32 + 4 * ((c + 1) * H)) : nbytes - payload;
+        start = payload + r0;
+        bytes = (aligned16 && r1 > r0 && (r0 & 3) == 0 && (r1 & 3) == 0 && r1 - r0 <= (uint32_t)kPlaneInBytes &&
+                 (unsigned long long)payload + r1 <= nbytes) ? r1 - r0 : 0u;
+      }
+    } else {
+      code = 5;
+    }
+  }
+  pi.code = code; pi.mode = mode; pi.start = start; pi.bytes = bytes; pi.payload = payload; pi.nbytes = nbytes;
+  pi.use_bar = 0;
+  pi.lo = start & ~15u;
+  if (!code && mode == 1 && bytes) {
+    const uint32_t end = start + bytes, hi = end & ~15u;  // [lo, hi) by TMA (the caller), [hi, end) here
+    for (uint32_t o = hi > pi.lo ? hi : pi.lo; o < end; o += 4)
+      *reinterpret_cast<uint32_t*>(buf + (o - pi.lo)) = ld_u32(base + o);
+  }
+}
+
+__global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kernel(
+    const uint8_t* __restrict__ blobs, const unsigned long long* __restrict__ offs,
+    const unsigned int* __restrict__ sizes, int n, int C, int H, int W, __half* __restrict__ out, int* err) {
+  // warps 0..kPlaneThreads/32-1 decode; the last warp is the producer: it validates each plane's
+  // header and stages its rows (TMA) into a 2-slot ring, full / empty mbarriers, no block barrier
+  extern __shared__ __align__(16) uint8_t s_dyn[];
+  constexpr int kBuf = kPlaneInBytes + 32, kDecWarps = kPlaneThreads / 32;
+  uint8_t* s_in[2] = {s_dyn, s_dyn + kBuf};
+  __shared__ PlaneInfo s_pi[2];
+  __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const long long planes = (long long)n * C;
+  const int vals = H * W;
+  if (t == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_empty[i], kDecWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp == kDecWarps) {  // producer
+    if (lane == 0) {
+      int k = 0;
+      for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x, ++k) {
+        const int b = k & 1;
+        ptx::mbar_wait(&s_empty[b], (uint32_t)(((k >> 1) & 1) ^ 1));  // slot free (first use: passes)
+        const int bi = (int)(pl / C), c = (int)(pl - (long long)bi * C);
+        const uint8_t* base = blobs + offs[bi];
+        PlaneInfo& pi = s_pi[b];
+        plane_prep(base, sizes[bi], (offs[bi] & 15) == 0, c, C, H, W, pi, s_in[b], nullptr);
+        // plane_prep issued nothing (null barrier): issue the staging copy here with its bytes
+        uint32_t tx = 0;
+        if (!pi.code && pi.mode == 1 && pi.bytes) {
+          const uint32_t end = pi.start + pi.bytes, hi = end & ~15u;
+          if (hi > pi.lo) tx = hi - pi.lo;
+        }
+        pi.use_bar = tx ? 1 : 0;
+        if (tx) {
+          ptx::mbar_arrive_expect_tx(&s_full[b], tx);
+          ubulk_load(s_in[b], base + pi.lo, tx, &s_full[b]);
+        } else {
+          ptx::mbar_arrive(&s_full[b]);
+        }
+      }
+    }
+    return;
+  }
+  int k = 0;
+  for (long long pl = blockIdx.x; pl < planes; pl += gridDim.x, ++k) {
+    const int b = k & 1;
+    ptx::mbar_wait(&s_full[b], (uint32_t)((k >> 1) & 1));
+    const PlaneInfo pi = s_pi[b];
+    const int bi = (int)(pl / C), c = (int)(pl - (long long)bi * C);
+    const uint8_t* base = blobs + offs[bi];
+    uint16_t* dst = reinterpret_cast<uint16_t*>(out) + (size_t)pl * vals;
+    if (pi.code) {
+      for (int i = t; i < vals; i += kPlaneThreads) dst[i] = 0;
+      if (t == 0) atomicExch(err, pi.code);
+    } else if (pi.mode == 0) {  // raw fp16: 16-byte vectors when aligned
+      const uint8_t* src = base + pi.payload + 2ull * c * H * W;
+      if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const uint4* s16 = reinterpret_cast<const uint4*>(src);
+        uint4* d16 = reinterpret_cast<uint4*>(dst);
+        for (int i = t; i < vals / 8; i += kPlaneThreads) d16[i] = __ldg(s16 + i);
+      } else {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dst);
+        for (int i = t; i < vals / 2; i += kPlaneThreads) d32[i] = __ldg(s32 + i);
+      }
+    } else if (pi.mode == 2) {  // q8: 16 values per 16-byte load (4 per 32-bit load if unaligned)
+      const float scale = __uint_as_float(ld_u32(base + 32 + 4 * c));
+      const int zp = (int)ld_u32(base + 32 + 4 * C + 4 * c);
+      const uint8_t* qb = base + pi.payload + (size_t)c * H * W;
+      auto deq4 = [&](uint32_t w4, uint32_t& lo, uint32_t& hi) {
+        uint16_t h[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float f = __fmul_rn((float)((int)(int8_t)(w4 >> (8 * e)) - zp), scale);
+          h[e] = __half_as_ushort(__float2half_rn(f));
+        }
+        lo = h[0] | (uint32_t)h[1] << 16;
+        hi = h[2] | (uint32_t)h[3] << 16;
+      };
+      if ((reinterpret_cast<uintptr_t>(qb) & 15) == 0) {
+        const uint4* q = reinterpret_cast<const uint4*>(qb);
+        uint4* d16 = reinterpret_cast<uint4*>(dst);
+        for (int i = t; i < vals / 16; i += kPlaneThreads) {
+          const uint4 w = __ldg(q + i);
+          uint4 o0, o1;
+          deq4(w.x, o0.x, o0.y);
+          deq4(w.y, o0.z, o0.w);
+          deq4(w.z, o1.x, o1.y);
+          deq4(w.w, o1.z, o1.w);
+          d16[2 * i] = o0;
+          d16[2 * i + 1] = o1;
+        }
+      } else {
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(qb);
+        uint2* d64 = reinterpret_cast<uint2*>(dst);
+        for (int i = t; i < vals / 4; i += kPlaneThreads) {
+          uint2 o;
+          deq4(__ldg(q + i), o.x, o.y);
+          d64[i] = o;
+        }
+      }
+    } else {  // mode 1 from the staged copy
+      const uint8_t* sb = s_in[b] + (pi.start - pi.lo);  // the plane's first byte
+      int code = 0;
+      const int L = W / 32;
+      if ((L & (L - 1)) == 0 && L <= 32) {  // L lanes per row
+        const int rows_per_pass = kPlaneThreads / L;
+        for (int y0 = 0; y0 < H; y0 += rows_per_pass) {
+          const int y = y0 + t / L;
+          const bool active = y < H;
+          const uint32_t roff = active ? ld_u32(base + 32 + 4 * (c * H + y)) : 0u, at = pi.payload + roff;
+          uint16_t* drow = dst + (size_t)(active ? y : 0) * W;
+          const bool fmt = active && ((roff & 3) || (unsigned long long)at > pi.nbytes);
+          const bool staged = pi.bytes && at >= pi.start && at < pi.start + pi.bytes;
+          const uint8_t* src = staged ? sb + (at - pi.start) : base + at;
+          const uint32_t avail = fmt ? 0u : (staged ? pi.start + pi.bytes - at : pi.nbytes - at);
+          int rc = decode_row_split(src, avail, L, lane, active && !fmt, drow);
+          const bool retry = rc != 0 && staged;  // the row runs past the staged range: from global
+          if (__any_sync(0xffffffffu, retry)) {
+            const int rc2 = decode_row_split(base + at, pi.nbytes - at, L, lane, active && !fmt && retry, drow);
+            if (retry) rc = rc2;
+          }
+          if (fmt) rc = 4;
+          if (rc && active) {
+            for (int e = 32 * (t & (L - 1)); e < 32 * (t & (L - 1)) + 32; e += 8)
+              *reinterpret_cast<uint4*>(drow + e) = make_uint4(0, 0, 0, 0);
+            code = rc;
+          }
+        }
+      } else {
+        for (int y = t; y < H; y += kPlaneThreads) {
+          const uint32_t roff = ld_u32(base + 32 + 4 * (c * H + y)), at = pi.payload + roff;
+          uint16_t* drow = dst + (size_t)y * W;
+          int rc;
+          if ((roff & 3) || (unsigned long long)at > pi.nbytes) {
+            rc = 4;
+          } else if (pi.bytes && at >= pi.start && at < pi.start + pi.bytes) {
+            rc = decode_row_lane(sb + (at - pi.start), pi.start + pi.bytes - at, W, drow);
+            if (rc) rc = decode_row_lane(base + at, pi.nbytes - at, W, drow);  // runs past the staged range
+          } else {
+            rc = decode_row_lane(base + at, pi.nbytes - at, W, drow);
+          }
+          if (rc) {
+            for (int e = 0; e < W; e += 8) *reinterpret_cast<uint4*>(drow + e) = make_uint4(0, 0, 0, 0);
+            code = rc;
+          }
+        }
+      }
+      if (code) atomicExch(err, code);
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&s_empty[b]);  // this warp is done with slot b
+  }
+}
+
 void launch_lblp_unpack(const uint8_t* blobs, const unsigned long long* offs, const unsigned int* sizes, int n,
                         int C, int H, int W, __half* out, int* err, cudaStream_t s) {
+  if ((long long)H * W <= kPlaneMaxVals && W % 32 == 0 && !g_unpack_rows) {
+    const long long planes = (long long)n * C;
+    const long long cap = (long long)num_sms() * 3;  // three 70 KB CTAs per SM
+    constexpr int smem = 2 * (kPlaneInBytes + 32);
+    if (ensure_smem_attr(reinterpret_cast<const void*>(lblp_unpack_plane_kernel), smem)) {
+      lblp_unpack_plane_kernel<<<(int)(planes < cap ? planes : cap), kPlaneThreads + 32, smem, s>>>(blobs, offs, sizes,
+                                                                                                     n, C, H, W, out, err);
+      return;
+    }
+  }
   const long long rows = (long long)n * C * H;
   long long blocks = (rows + 7) / 8;
   const long long cap = (long long)num_sms() * 8;
