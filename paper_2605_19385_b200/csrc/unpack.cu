@@ -190,17 +190,18 @@ __device__ __forceinline__ int decode_row_split(const uint8_t* row, uint32_t ava
   if (active && !seg_bad) {
     const uint32_t* wp = reinterpret_cast<const uint32_t*>(row + wpos);
     const uint32_t mask = (1u << bw) - 1u;
-    uint64_t buf = 0;
-    uint32_t nb = 0, wi = 0;
+    // two-word window (nxt:cur) and a bit position < 32: one funnel shift per value
+    uint32_t cur = bw ? wp[0] : 0u, nxt = bw > 1 ? wp[1] : 0u, pos = 0, wi = 2;
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      if (nb < bw) {
-        buf |= (uint64_t)wp[wi++] << nb;
-        nb += 32;
+      const uint32_t z = __funnelshift_r(cur, nxt, pos) & mask;
+      pos += bw;
+      if (pos >= 32) {
+        pos -= 32;
+        cur = nxt;
+        nxt = wi < bw ? wp[wi] : 0u;
+        ++wi;
       }
-      const uint32_t z = (uint32_t)buf & mask;
-      buf >>= bw;
-      nb -= bw;
       const uint32_t d = (j == 0 && k == 0) ? 0u : ((z >> 1) ^ (uint32_t)(-(int)(z & 1)));
       acc += d;
       if (k & 1) sv[k >> 1] |= (acc & 0xFFFFu) << 16; else sv[k >> 1] = acc & 0xFFFFu;
