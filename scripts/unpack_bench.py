@@ -79,6 +79,14 @@ def main():
         blob = torch.empty(n * stride, dtype=torch.uint8, device=dev)
         sizes = torch.empty(n, dtype=torch.int32, device=dev)
         lbx.pack_device(z.data_ptr(), n, 16, 128, 128, blob.data_ptr(), stride, sizes.data_ptr(), s.cuda_stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(3):
+            lbx.pack_device(z.data_ptr(), n, 16, 128, 128, blob.data_ptr(), stride, sizes.data_ptr(), s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        pack_ms = e0.elapsed_time(e1) / 3
         offs = torch.arange(n, dtype=torch.int64, device=dev) * stride
         ms = time_unpack(blob, offs, sizes, n, out, err, a.reps, s)
         assert int(err.item()) == 0
@@ -87,7 +95,8 @@ def main():
         algo = blob_bytes + 2 * vals * n
         res[f"mode1_{kind}"] = {"ms": round(ms, 3), "ratio": round(blob_bytes / (2 * vals * n), 3),
                                 "algo_bytes": algo, "GBps": round(algo / ms / 1e6, 1),
-                                "frac_of_hbm": round(algo / ms / 1e6 / res["peak_hbm_gbps"], 3)}
+                                "frac_of_hbm": round(algo / ms / 1e6 / res["peak_hbm_gbps"], 3),
+                                "pack_ms": round(pack_ms, 3), "pack_GBps": round(algo / pack_ms / 1e6, 1)}
         del blob
     # mode 2 (q8 + per-channel affine): host packer, one blob per 64 latents replicated
     zq = latents("smooth", 64, dev, gen).cpu().numpy()
