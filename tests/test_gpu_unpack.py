@@ -112,3 +112,64 @@ def test_device_pack_equals_host_packer(lbx, shape, smooth):
         dec = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=n)
         blobs = [o[i * stride:i * stride + int(sizes[i].item())].tobytes() for i in range(n)]
         assert np.array_equal(_gpu_unpack(lbx, dec, blobs), np.ascontiguousarray(z).view(np.uint16))
+
+
+@pytest.mark.parametrize("n,c,h,w", [(3, 4, 256, 256), (2, 3, 40, 96), (2, 2, 7, 32), (2, 1, 3, 1024), (5, 16, 64, 64)])
+def test_device_pack_unpack_round_trip_shapes(lbx, n, c, h, w):
+    """lbx_pack_device -> lbx_op_unpack on device-resident blobs is the identity for shapes that take
+    every kernel path: planes over 16 K values (row kernel), W/32 = 3 (lane-per-row decode), W/32 = 1
+    and 32 (segment widths at both ends), plus the decoder's 64x64; the bytes equal the host packer's."""
+    import torch
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(n * 1000 + c * 100 + w)
+    z = (torch.randn((n, c, h, w), generator=g, device=dev) * 3).half()
+    z[0, 0, 0, :8] = torch.tensor([0.0, -0.0, 65504.0, -65504.0, 1e-7, -1e-7, float("inf"), float("-inf")],
+                                  dtype=torch.float16)
+    stride = (lbx.pack_bound(c, h, w) + 15) // 16 * 16
+    blob = torch.zeros(n * stride, dtype=torch.uint8, device=dev)
+    sizes = torch.zeros(n, dtype=torch.int32, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    lbx.pack_device(z.data_ptr(), n, c, h, w, blob.data_ptr(), stride, sizes.data_ptr(), s)
+    offs = torch.arange(n, dtype=torch.int64, device=dev) * stride
+    out = torch.empty_like(z)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    lbx.op_unpack(blob.data_ptr(), offs.data_ptr(), sizes.data_ptr(), n, c, h, w, out.data_ptr(), err.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert torch.equal(out.view(torch.int16), z.view(torch.int16))
+    zh = z.cpu().numpy()
+    bh, sz = blob.cpu().numpy(), sizes.cpu().numpy()
+    for i in range(n):
+        assert bh[i * stride:i * stride + sz[i]].tobytes() == lbx.pack(zh[i], 1)
+
+
+def test_noncanonical_row_order_decodes(lbx):
+    """A valid blob whose rows are stored in reverse order (row table rewritten) decodes to the same
+    latent: the plane kernel stages only the canonical contiguous layout and must fall back to
+    reading such rows from global memory."""
+    import struct
+    import torch
+    rng = np.random.default_rng(9)
+    c, h, w = 4, 64, 64
+    z = rng.standard_normal((c, h, w)).astype(np.float16)
+    blob = bytearray(lbx.pack(z, 1))
+    rows = c * h
+    table_off, payload = struct.unpack_from("<II", blob, 20)
+    offs = list(struct.unpack_from(f"<{rows}I", blob, table_off))
+    ends = offs[1:] + [len(blob) - payload]
+    pieces = [bytes(blob[payload + offs[r]:payload + ends[r]]) for r in range(rows)]
+    new_payload, new_offs, pos = b"", [0] * rows, 0
+    for r in reversed(range(rows)):
+        new_offs[r] = pos
+        new_payload += pieces[r]
+        pos += len(pieces[r])
+    rev = bytes(blob[:table_off]) + struct.pack(f"<{rows}I", *new_offs) + new_payload
+    assert len(rev) == len(blob)
+    dec = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=2)
+    dev = torch.device("cuda")
+    lat = torch.empty((2, c, h, w), dtype=torch.float16, device=dev)
+    dec.unpack_ptr([bytes(blob), rev], lat.data_ptr())
+    torch.cuda.synchronize()
+    got = lat.cpu().numpy()
+    assert np.array_equal(got[0].view(np.int16), z.view(np.int16))
+    assert np.array_equal(got[1].view(np.int16), z.view(np.int16))
