@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--config", type=int, choices=[2, 3, 4], default=2)
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the codec / PNG kernel rates")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the per-launch profile here")
     return ap.parse_args()
@@ -141,6 +142,57 @@ def cpu_decode_sample(fam, c, threads, images=1, seed=123):
     t = time.perf_counter()
     vae_ref.decode(z, W, fam, threads=threads)
     return (time.perf_counter() - t) / images
+
+
+def codec_rates(lbx, torch, dev, stream, hbm_peak):
+    """HBM-roofline lines for the codec (K1 unpack, the device packer) at 4096 latents of 16x128x128
+     and the GPU PNG encode of 32 RGB images: CUDA events on `stream`, inputs resident.
+    Unpack output is checked bit-exact against the packed latents."""
+    n, c, h, w = 4096, 16, 128, 128
+    vals = c * h * w
+    g = torch.Generator(device=dev).manual_seed(5)
+    z = torch.randn((n, c, h, w), generator=g, device=dev).half()
+    stride = (lbx.pack_bound(c, h, w) + 15) // 16 * 16
+    blob = torch.empty(n * stride, dtype=torch.uint8, device=dev)
+    sizes = torch.empty(n, dtype=torch.int32, device=dev)
+    offs = torch.arange(n, dtype=torch.int64, device=dev) * stride
+    out = torch.empty_like(z)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    sp = stream.cuda_stream
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1) / reps
+
+    pack_ms = timed(lambda: lbx.pack_device(z.data_ptr(), n, c, h, w, blob.data_ptr(), stride, sizes.data_ptr(), sp))
+    unpack_ms = timed(lambda: lbx.op_unpack(blob.data_ptr(), offs.data_ptr(), sizes.data_ptr(), n, c, h, w,
+                                            out.data_ptr(), err.data_ptr(), sp))
+    exact = int(err.item()) == 0 and torch.equal(out.view(torch.int16), z.view(torch.int16))
+    algo = int(sizes.sum().item()) + 2 * vals * n
+    del out, blob
+    rgb = torch.randint(0, 256, (32, 1024, 1024, 3), dtype=torch.uint8, generator=g, device=dev)
+    pstride = (lbx.png_bound(1024, 1024) + 15) // 16 * 16
+    pout = torch.empty(32 * pstride, dtype=torch.uint8, device=dev)
+    psz = torch.empty(32, dtype=torch.int32, device=dev)
+    png_ms = timed(lambda: lbx.png_encode_device(rgb.data_ptr(), 32, 1024, 1024, pout.data_ptr(), pstride,
+                                                 psz.data_ptr(), sp))
+
+    def line(ms, nbytes):
+        gbs = nbytes / ms / 1e6
+        return {"ms": round(ms, 3), "GBps": round(gbs, 1), "frac_of_hbm": round(gbs / hbm_peak, 3)}
+
+    return {"workload": "4096 x 16x128x128 fp16 latents (N(0,1)), LBLP mode 1 (lossless); 32 RGB 1024^2 images",
+            "unpack": dict(line(unpack_ms, algo), bit_exact=exact), "pack": line(pack_ms, algo),
+            "png_encode": {"ms": round(png_ms, 3), "img_s": round(32 / png_ms * 1e3, 1),
+                           "note": "uniform-noise RGB (stored blocks); decoded images: scripts/png_bench.py"},
+            "bytes": "algorithmic: packed blob bytes + 2 B per latent value; peak = MEASURED_PEAKS hbm"}
 
 
 def run_reference(args):
@@ -317,6 +369,11 @@ def main():
         cpu = {"value": 1.0 / sec, "unit": "img/s", "cores": threads, "kind": "port",
                "sample": f"one 1024^2 image ({fam}), oracle/vae_ref.py torch fp32 on {threads} threads"}
 
+    # ---------------------------------------------------------------- codec / return-path kernels (rank 0, N=1)
+    kernels = None
+    if rank == 0 and world == 1 and not args.no_kernels:
+        kernels = codec_rates(lbx, torch, dev, stream, hbm)
+
     if rank == 0:
         line = {
             "metric": "1024^2 images/sec decoded", "value": value, "unit": "img/s", "n_gpus": world,
@@ -329,6 +386,7 @@ def main():
                        "parallelism": f"dp{world} (whole-request sharding, no collective)"},
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,
+            "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
