@@ -112,7 +112,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
@@ -123,11 +123,15 @@ class ClockSampler:
                 mx = float(f[2])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for i, nm in enumerate(names):
                 if f[4 + i].lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": round(statistics.median(pw), 1) if pw else None}
 
 
 def cpu_decode_sample(fam, c, threads, images=1, seed=123):
@@ -285,6 +289,8 @@ def main():
     barrier()
     clocks = clk.stop()
     ms = e0.elapsed_time(e1)
+    if clocks.get("power_w"):  # energy per image at the median board power of the timed region
+        clocks["joules_per_img"] = round(clocks["power_w"] * (ms / 1e3) / (batch * args.steps), 3)
     ms_max = reduce_max(ms, dev)
     value = world * batch * args.steps / (ms_max / 1e3)
     launches = dec.launch_count(batch)
