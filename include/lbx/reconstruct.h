@@ -202,7 +202,8 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * residuals in the epilogue instead of preloading them into the TMEM accumulator (default: preload for
  * 128-wide outputs, epilogue add for wider ones; bit 20 preloads at every width; bit 21 L2-prefetches
  * the next preload's rows; bit 22 gives each conv cluster a contiguous block of tiles instead of
- * round-robin; bit 23 launches the GEMM and GroupNorm-apply kernels as programmatic dependents);
+ * round-robin; bit 23 launches the GEMM and GroupNorm-apply kernels as programmatic dependents; bit 25 routes
+ * the residual preload through per-warp shared-memory staging with line-covering loads);
  * 12-15 are
  * epilogue ablations (wrong results: skip all work / keep only TMEM loads / no stores / no
  * statistics); bits 16-17 = 1 + epilogue store mode (0 STG.128, 1 STG.256 = default, 2 streaming); 18

@@ -64,6 +64,7 @@ struct KParams {
   int rpf_pf;          // 1: L2-prefetch the next preload's rows before waiting for the accumulator
   int sched;           // 1: each cluster takes a contiguous block of tiles (conv modes), 0: round-robin
   int pdl;             // 1: launched as a programmatic dependent (wait before any global access)
+  int rres;            // 1: residual preload through per-warp smem staging (line-covering loads)
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
@@ -536,7 +537,48 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     // buffer to the MMA issuer is the arrival after the preload.  It replaces the folded extra K
     // (4-8 short k-blocks of MMAs) and the epilogue's late residual reads.
     auto prefill = [&](int tn, int buf) {
-      if (tn < t_end) {
+      if (tn < t_end && p.rres) {
+        // line-covering loads: instruction k reads pixels 8k..8k+7 of the warp's 32 rows, 64 B each
+        // (lane l: pixel 8k + l/4, quarter l%4), transposed through the warp's 2 KB swizzled stage
+        int mt, nt, phn;
+        tile_coords(p, tn, mt, nt, phn);
+        const uint32_t stage = ptx::smem_u32(sOut + (warp - 2) * 2 * 2048);
+        for (int sub = 0; sub < p.msub; ++sub) {
+          const long long prow0 = tile_row0(p, mt, (int)rank, CG, sub) + q * 32;  // the warp's first pixel row
+          const uint32_t tb = tmem_base + ((q * 32u) << 16) + buf * (p.msub * BN) + sub * BN;
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            const __half* rb0 = p.resid + prow0 * p.ldr + nt * BN + (cbase + cstep * j) * 32;
+            uint4 u[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int px = 8 * k + (int)(lane >> 2);
+              u[k] = __ldg(reinterpret_cast<const uint4*>(rb0 + (long long)px * p.ldr) + (lane & 3));
+            }
+            __syncwarp();  // the stage's previous contents are consumed
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int px = 8 * k + (int)(lane >> 2);
+              ptx::sts128(stage + px * 64 + ((((int)lane & 3) ^ ((px >> 1) & 3)) << 4), u[k]);
+            }
+            __syncwarp();
+            uint32_t r[32];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const uint4 v = ptx::lds128(stage + lane * 64 + ((i ^ ((lane >> 1) & 3)) << 4));
+              const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
+                r[i * 8 + 2 * k] = __float_as_uint(f.x);
+                r[i * 8 + 2 * k + 1] = __float_as_uint(f.y);
+              }
+            }
+            ptx::tmem_st32(tb + (cbase + cstep * j) * 32, r);
+          }
+        }
+        ptx::tmem_st_wait();
+      } else if (tn < t_end) {
         int mt, nt, phn;
         tile_coords(p, tn, mt, nt, phn);
         for (int sub = 0; sub < p.msub; ++sub) {
@@ -828,6 +870,8 @@ static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel inst
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
+static int g_rres_policy = 0;      // 1: residual preload via per-warp smem staging (bit 25; half the
+                                   // LSU wavefronts, measured neutral: same ms and J/TFLOP sustained)
 static int g_pdl_policy = 0;       // 1: programmatic dependent launch of the GEMM kernels (bit 23)
 static int g_sched_policy = 0;     // 1: contiguous tile blocks per cluster for conv modes (bit 22 sets;
                                    // measured worse: c128 conv reads 25.5 vs 23.0 GB from DRAM, the
@@ -854,6 +898,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_rpf_pf = (halo_policy >> 21) & 1;
   g_sched_policy = (halo_policy >> 22) & 1;
   g_pdl_policy = (halo_policy >> 23) & 1;
+  g_rres_policy = (halo_policy >> 25) & 1;
   g_tstore_policy = (halo_policy >> 18) & 1;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -865,7 +910,7 @@ template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
   // ---- operand staging plan (tstore: 32 KB of the budget go to the output staging tiles)
-  const int budget = kSmemBudget - (kp.tstore ? 33 * 1024 : 0);
+  const int budget = kSmemBudget - ((kp.tstore || kp.rres) ? 33 * 1024 : 0);
   if (kp.halo) {
     if (kp.vsub) {  // one box of halo_rows + msub - 1 rows; sub-tile s starts 130 s rows in
       kp.halo_sub_bytes = 130 * 128;
@@ -878,7 +923,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     }
     // policy 1: a halo stage feeds >= 36 MMAs, so two are enough and the rest of the budget goes to
     // B; policy 0 (default): three A stages when the B tile is small and there is one sub-tile
-    if (g_stage_policy || (kp.tstore && Cf::B_BYTES >= 16384)) kp.a_stages = 2;
+    if (g_stage_policy || ((kp.tstore || kp.rres) && Cf::B_BYTES >= 16384)) kp.a_stages = 2;
     else kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
     kp.b_stages = (budget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
   } else {
@@ -889,7 +934,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
   if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
   const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16 +
-                   16 + 8 * (BN / 2) * 4 + (kp.tstore ? 1024 + 8 * 2 * 2048 : 0);
+                   16 + 8 * (BN / 2) * 4 + ((kp.tstore || kp.rres) ? 1024 + 8 * 2 * 2048 : 0);
   if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
 
   CUtensorMap tmA, tmB;
@@ -1043,6 +1088,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.rpf_pf = g_rpf_pf;
   kp.sched = (g_sched_policy && a.mode != GEMM_PLAIN) ? 1 : 0;
   kp.pdl = g_pdl_policy;
+  kp.rres = (kp.rpf && g_rres_policy && !kp.tstore && a.ldr % 8 == 0) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
