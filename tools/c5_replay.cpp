@@ -38,8 +38,9 @@ struct Opts {
 };
 
 // Batch service curve measured on one B200 for 16x128x128 -> 1024^2 (lbx_reconstruct, host blobs,
-// round-1 build, gpurun_out/c5_live_10x.err); sizes 1,2,4,8,16,32.  Used by sim mode unless --service or live measurement overrides.
-const double kDefaultService[6] = {9.40, 19.33, 40.27, 80.49, 165.76, 334.71};
+// power-capped steady state, profiles/r1f_c5_live_1gpu_25x_cost_sustained_curve.json); sizes
+// 1,2,4,8,16,32.  Used by sim mode unless --service or live measurement overrides.
+const double kDefaultService[6] = {9.06, 17.85, 35.64, 73.03, 149.75, 293.35};
 const int kSizes[6] = {1, 2, 4, 8, 16, 32};
 
 std::vector<double> curve_from(const double* pts, int maxb) {
