@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernels", action="store_true", help="skip the codec / PNG kernel rates")
+    ap.add_argument("--no-latency", action="store_true", help="skip the config-5 live replay (p50/p99)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default="", help="write the per-launch profile here")
     return ap.parse_args()
@@ -197,6 +198,32 @@ def codec_rates(lbx, torch, dev, stream, hbm_peak):
             "png_encode": {"ms": round(png_ms, 3), "img_s": round(32 / png_ms * 1e3, 1),
                            "note": "uniform-noise RGB (stored blocks); decoded images: scripts/png_bench.py"},
             "bytes": "algorithmic: packed blob bytes + 2 B per latent value; peak = MEASURED_PEAKS hbm"}
+
+
+def c5_latency(device, scale=25):
+    """BASELINE's p50/p99 miss-decode latency: a 20 s wall-clock window of the config-5 trace's decode
+    jobs replayed through lbx_batcher on this GPU (tools/c5_replay live)."""
+    exe = os.path.join(ROOT, "tools", "c5_replay")
+    if not os.path.exists(exe):
+        return {"unavailable": "tools/c5_replay not built"}
+    out = os.path.join("/tmp", f"lbx_c5_{os.getpid()}.json")
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(device)))
+    try:
+        subprocess.run([exe, "live", "--scale", str(scale), "--devices", "1", "--gpus", "1", "--json", out],
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=240, check=True, env=env)
+        with open(out) as f:
+            d = json.load(f)
+        os.remove(out)
+    except Exception as e:  # report, do not fail the bench line
+        return {"unavailable": f"c5_replay: {type(e).__name__}"}
+    live = d.get("live", {})
+    return {"workload": f"config 5 trace (Zipf x decay, 10 M requests), {scale}x replay, 20 s window, 1 GPU, "
+                        f"sd3 16x128x128 -> 1024^2, batch rule '{d.get('policy')}'",
+            "decode_p50_ms": live.get("decode_p50_ms"), "decode_p99_ms": live.get("decode_p99_ms"),
+            "decodes_per_s": live.get("throughput_img_s"), "jobs": live.get("jobs"),
+            "service_ms_b1": d.get("service_ms", [None])[0],
+            "sim_whole_trace": {k: d.get("sim", {}).get(k) for k in ("decode_p50_ms", "decode_p99_ms", "e2e_p50_ms", "e2e_p99_ms")},
+            "unit": "ms, decode stage = queue + batch wait + GPU (submit -> RGB in host memory)"}
 
 
 def run_reference(args):
@@ -380,6 +407,13 @@ def main():
     if rank == 0 and world == 1 and not args.no_kernels:
         kernels = codec_rates(lbx, torch, dev, stream, hbm)
 
+    # ---------------------------------------------------------------- miss-decode latency (rank 0, N=1)
+    latency = None
+    if rank == 0 and world == 1 and not args.no_latency:
+        dec.close()  # the replay builds its own decoder (batcher)
+        torch.cuda.empty_cache()
+        latency = c5_latency(local)
+
     if rank == 0:
         line = {
             "metric": "1024^2 images/sec decoded", "value": value, "unit": "img/s", "n_gpus": world,
@@ -393,6 +427,7 @@ def main():
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,
             "kernels": kernels,
+            "latency": latency,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
