@@ -32,10 +32,13 @@ def test_batcher_matches_direct_decode(lbx):
     b.close()
 
 
-def test_batcher_two_shape_classes(lbx):
+@pytest.mark.parametrize("policy", ["greedy", "cost"])
+def test_batcher_two_shape_classes(lbx, policy):
+    """Two shape classes (SD1.5 4-channel and SD3 16-channel) through one worker; with the cost
+    policy each class has its own measured service curve."""
     za = weights_ref.make_latents("sd15", 3, 64, 64, seed=32)
     zb = weights_ref.make_latents("sd3", 3, 64, 64, seed=33)
-    b = lbx.Batcher([0], [("sd15", 64, 64), ("sd3", 64, 64)], max_batch=8, max_wait_us=1000)
+    b = lbx.Batcher([0], [("sd15", 64, 64), ("sd3", 64, 64)], max_batch=8, max_wait_us=1000, policy=policy)
     outs = {}
     for i in range(3):
         for s, z in ((0, za), (1, zb)):
