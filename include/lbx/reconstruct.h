@@ -207,7 +207,8 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * 12-15 are
  * epilogue ablations (wrong results: skip all work / keep only TMEM loads / no stores / no
  * statistics); bits 16-17 = 1 + epilogue store mode (0 STG.128, 1 STG.256 = default, 2 streaming); 18
- * stages epilogue chunks in smem and TMA-stores them (measured equal to STG.256).
+ * stages every eligible GEMM's epilogue chunks in smem and TMA-stores them (default: plain GEMMs
+ * only, i.e. the attention projections and scores), 26 disables the TMA-store epilogue.
  * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
 /* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],
