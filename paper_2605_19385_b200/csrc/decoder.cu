@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -336,7 +337,10 @@ lbx_status Decoder::alloc_arena() {
   const size_t nb = (size_t)max_batch;
   const size_t x_el = nb * hw * 64 * 256;  // max residual-stream tensor: 8h x 8w x 256
   const size_t h_el = nb * hw * 64 * 128;  // max conv1 output: 8h x 8w x 128 (>= QKV hw x 1536)
-  s_imgs = std::max(1, std::min(max_batch, 8));  // attention scores of up to 8 images at once
+  // attention scores of up to 8 images at once (LBX_ATTN_GROUP overrides, diagnostics)
+  int group = 8;
+  if (const char* e = std::getenv("LBX_ATTN_GROUP")) group = std::max(1, std::atoi(e));
+  s_imgs = std::max(1, std::min(max_batch, group));
   const size_t s_el = hw * hw * (size_t)s_imgs;
   const size_t vt_el = 512 * hw;
   size_t off = 0;
