@@ -211,6 +211,9 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * only, i.e. the attention projections and scores), 26 disables the TMA-store epilogue.
  * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
 lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
+/* Diagnostics: GEMM grids use at most gemm_sms SMs and bulk GroupNorm applies at most apply_sms
+ * (0 = all), so that two kernels can share the GPU on different streams. */
+lbx_status lbx_op_set_grid_limits(int gemm_sms, int apply_sms);
 /* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],
  * ss float pairs [n][128], w fp32 [3][3][3][128] ([out][ky][kx][in]), rgb [n][H][W][3].  impl 0 =
  * tensor cores (fp32 SiLU), 2 = tensor cores with packed-half SiLU, 1 = CUDA cores (fp32). */

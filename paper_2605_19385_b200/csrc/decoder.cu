@@ -1096,6 +1096,12 @@ lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
   return LBX_OK;
 }
 
+lbx_status lbx_op_set_grid_limits(int gemm_sms, int apply_sms) {
+  lbx::gemm_tc_set_max_sms(gemm_sms);
+  lbx::kernels_set_apply_max_sms(apply_sms);
+  return LBX_OK;
+}
+
 lbx_status lbx_subpixel_weights(const float* w3, int N, int C, uint16_t* out) {
   if (!w3 || !out || N <= 0 || C <= 0) return set_err(LBX_E_CONFIG, "lbx_subpixel_weights: bad argument");
   static const int kset[2][2][2] = {{{0, -1}, {1, 2}}, {{0, 1}, {2, -1}}};

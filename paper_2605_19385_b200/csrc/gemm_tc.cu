@@ -870,6 +870,7 @@ static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel inst
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
+static int g_gemm_max_sms = 0;     // diagnostics: cap on the SMs a GEMM grid uses (0 = all)
 static int g_rres_policy = 0;      // 1: residual preload via per-warp smem staging (bit 25; half the
                                    // LSU wavefronts, measured neutral: same ms and J/TFLOP sustained)
 static int g_pdl_policy = 0;       // 1: programmatic dependent launch of the GEMM kernels (bit 23)
@@ -982,7 +983,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   }
   auto kern = gemm_tc_kernel<BN, CG, XF>;
   const int sms = num_sms();
-  int clusters = sms / CG;
+  int clusters = (g_gemm_max_sms > 0 && g_gemm_max_sms < sms ? g_gemm_max_sms : sms) / CG;
   if (clusters > kp.tiles) clusters = kp.tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG);
@@ -1032,6 +1033,7 @@ bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
 bool resid_preload() { return g_rpf_policy != 0; }
 bool pdl_enabled() { return g_pdl_policy != 0; }
+void gemm_tc_set_max_sms(int n) { g_gemm_max_sms = n; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments); four extra warps transform each landed halo

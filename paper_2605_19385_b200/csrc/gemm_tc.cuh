@@ -73,6 +73,7 @@ bool gemm_tc_prepare();
 // programmatic dependent launch of the decode's kernels (debug bit 23); kernels that support it wait
 // (griddepcontrol.wait) before their first global access and trigger their dependents when done
 bool pdl_enabled();
+void gemm_tc_set_max_sms(int n);  // diagnostics: GEMM grids use at most n SMs (0 = all)
 
 // fp16 tiled TMA descriptor with 128-byte swizzle (dims innermost first; strides in bytes for
 // dims 1..rank-1).  Out-of-bounds boxes are zero-filled.

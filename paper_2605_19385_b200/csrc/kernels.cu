@@ -218,6 +218,8 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+static int g_apply_max_sms = 0;  // diagnostics: cap on the SMs a bulk GroupNorm apply uses
+void kernels_set_apply_max_sms(int n) { g_apply_max_sms = n; }
 static bool g_apply_bulk = true;  // bulk-copy apply (debug bit 8 selects the register-staged one)
 void kernels_set_apply_bulk(bool on) { g_apply_bulk = on; }
 
@@ -230,7 +232,8 @@ static bool gn_apply_bulk_launch(const __half* x, __half* y, const GnSrc& g, int
   constexpr int smem = kApStages * kApChunk + kApStages * 8;
   if (!ensure_smem_attr(reinterpret_cast<const void*>(gn_apply_bulk_kernel<SILU, CV, H2>), smem)) return false;
   const long long chunks = (long long)n * img_bytes / kApChunk;
-  const int grid = (int)(chunks < num_sms() ? chunks : num_sms());
+  const int sms = g_apply_max_sms > 0 && g_apply_max_sms < num_sms() ? g_apply_max_sms : num_sms();
+  const int grid = (int)(chunks < sms ? chunks : sms);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(256);

@@ -49,6 +49,7 @@ cudaError_t launch_conv_out_tc(const __half* x, const float2* ss, const float* w
                                int n, int H, int W, bool h2, cudaStream_t s);
 void kernels_set_conv_out_legacy(bool on);
 void kernels_set_apply_bulk(bool on);
+void kernels_set_apply_max_sms(int n);
 bool kernels_conv_out_legacy();
 
 // GroupNorm-32 statistics (sum, sumsq per image and group) of x [n][hw][C] fp16 into stats
