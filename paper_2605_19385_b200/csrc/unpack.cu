@@ -1,8 +1,14 @@
-// K1: LBLP v1 latent unpack on the GPU (format: include/lbx/lblp.h).  One warp per latent row
-// (c, y): lane k owns value k of every 32-value mini-block, extracts its zigzag delta from the
-// bit-packed words, and a warp-wide inclusive scan (mod 2^16) rebuilds the order-mapped values.
-// Stores are 64 contiguous bytes per warp per mini-block.  Bit-exact by construction; checked
-// against the C oracle (oracle/lblp_ref.c) in tests/test_gpu_unpack.py.
+// K1: LBLP v1 latent unpack on the GPU (format: include/lbx/lblp.h).  Two kernels:
+//   lblp_unpack_plane_kernel (default; planes of <= 16 K values, W % 32 == 0): one CTA per
+//     (latent, channel) plane.  A producer warp validates each plane's header once and stages its
+//     rows into a 2-slot shared-memory ring with a 1-D TMA copy (full / empty mbarriers); the
+//     decode warps give each row W/32 lanes, one 32-value mini-block per lane (funnel-shift bit
+//     reader, register prefix sum, one segmented shuffle scan for the carries), and write 16-byte
+//     vectors.  q8 / raw planes stream through with 16-byte vectors.
+//   lblp_unpack_kernel (fallback for larger planes; debug bit 24): one warp per latent row, lane k
+//     owns value k of every mini-block, warp-wide scans rebuild the values.
+// Bit-exact by construction; checked against the C oracle (oracle/lblp_ref.c) in
+// tests/test_gpu_unpack.py.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -114,20 +120,17 @@ __global__ void __launch_bounds__(256) lblp_unpack_kernel(const uint8_t* __restr
 }
 
 // ---------------------------------------------------------------------------------------------
-// Plane kernel (the default for planes of <= kPlaneMaxVals values): one CTA per (latent, channel)
-// plane.  Thread 0 validates the 32-byte header once for the plane; mode-1 rows are staged into
-// shared memory with independent 32-bit loads (the whole plane's compressed bytes in flight at
-// once instead of a dependent chain per row), decoded there one warp per row, and the plane is
-// written back with 16-byte stores.  Modes 0 / 2 stream straight through with vector loads.  A row
-// whose table offset lies outside the staged range (a valid but non-canonical layout) is decoded
-// from global memory.  Bit-exact with the row kernel above; same error codes.
+// Plane kernel (the default for planes of <= kPlaneMaxVals values): see the file comment.  A row
+// whose table offset lies outside the staged canonical range (a valid but non-canonical layout)
+// is decoded from global memory.  Bit-exact with the row kernel above; same error codes.
 constexpr int kPlaneMaxVals = 16384;           // 128 x 128
 constexpr int kPlaneInBytes = 34 * 1024 + 64;  // mode-1 plane at 128 x 128: <= 128 x 264 B
 constexpr int kPlaneThreads = 256;  // decode threads (W/32 per mode-1 row) + one producer warp
 
-// decode one mode-1 row (W values) on ONE lane: the prefix sum runs sequentially in registers over
-// a 64-bit bit reader (no warp shuffles); 8 values per 16-byte store to `dst` (global, 16-byte
-// aligned).  Bounds as in the row kernel; on an error the caller zeroes the row.
+// decode one mode-1 row (W values) on ONE lane (used when W/32 is not a power of two): the prefix
+// sum runs sequentially in registers over a 64-bit bit reader (no warp shuffles); 8 values per
+// 16-byte store to `dst` (global, 16-byte aligned).  Bounds as in the row kernel; on an error the
+// caller zeroes the row.
 __device__ __forceinline__ int decode_row_lane(const uint8_t* row, uint32_t avail, int W, uint16_t* dst) {
   const uint32_t head = (2u + (uint32_t)(W / 32) + 3u) & ~3u;
   if (avail < head) return 4;
@@ -217,12 +220,14 @@ __device__ __forceinline__ int decode_row_split(const uint8_t* row, uint32_t ava
     if (j >= o) tin += u;
   }
   if (!active || seg_bad) return seg_bad ? 4 : 0;
-  const uint32_t off = (uint32_t)omap((uint16_t)bits0) + tin - acc;
+  const uint32_t off = ((uint32_t)omap((uint16_t)bits0) + tin - acc) & 0xFFFFu;
+  const uint32_t off2 = off | off << 16, off2lo = off2 & 0x7FFF7FFFu;
   uint32_t pk[16];
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const uint32_t a = omap_inv((uint16_t)(off + (sv[k] & 0xFFFFu))), b = omap_inv((uint16_t)(off + (sv[k] >> 16)));
-    pk[k] = a | b << 16;
+  for (int k = 0; k < 16; ++k) {  // both halves at once: add mod 2^16 per half, then the inverse order map
+    const uint32_t v = ((sv[k] & 0x7FFF7FFFu) + off2lo) ^ ((sv[k] ^ off2) & 0x80008000u);
+    const uint32_t neg = ((v & 0x80008000u) >> 15) * 0x7FFFu;  // 0x7FFF in each half whose bit 15 is set
+    pk[k] = ~(v ^ neg);  // bit 15 set: v ^ 0x8000 (= v & 0x7FFF); clear: ~v
   }
   uint4* d16 = reinterpret_cast<uint4*>(dst + 32 * j);
 #pragma unroll
