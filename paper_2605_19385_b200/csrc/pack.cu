@@ -2,14 +2,16 @@
 // that are already on the device (e.g. straight out of a VAE encoder).  Byte-identical to the host
 // packer (csrc/codec.cpp lblp_pack) and to the C oracle; format in include/lbx/lblp.h.
 //
-//   K-a  lblp_rows_kernel   one warp per latent row (c, y): order-map, delta, zigzag, and per
-//                           32-value mini-block the bit width (warp max -> 32 - clz); writes the
-//                           widths and the row's byte size (head + 4 * sum of widths).
-//   K-b  lblp_scan_kernel   one block per latent: exclusive scan of the row sizes -> row table,
-//                           header, total size.
-//   K-c  lblp_write_kernel  one warp per row again: bits0, widths, padding, and the bit-packed
-//                           words -- value k of a mini-block of width w sits at bit k*w; word i is
-//                           the warp-wide OR (__reduce_or_sync) of each lane's share of it.
+//   K-a  lblp_rows_lane_kernel  W/32 lanes per latent row (c, y), one 32-value mini-block per
+//                               lane: order-map, delta against the value before, zigzag, width =
+//                               bit length of the OR; the row's byte size (head + 4 * sum widths).
+//   K-b  lblp_scan_kernel       one block per latent: exclusive scan of the row sizes -> row
+//                               table, header, total size.
+//   K-c  lblp_write_lane_kernel lanes as in K-a pack their words from a 64-bit accumulator into
+//                               the warp's rows in shared memory (bits0, widths, padding, words);
+//                               each row is then copied out with 4-byte stores across the warp.
+// The warp-per-row forms (lblp_rows_kernel / lblp_write_kernel: warp OR-reductions per word) are
+// kept for widths whose W/32 is not a power of two.
 // Blob i is written at out + i * stride (stride >= lbx_pack_bound); its size goes to sizes[i].
 #include <cuda_runtime.h>
 

@@ -9,11 +9,14 @@
 // byte boundary, and its matches may reach back into the previous strip's last row (the inflater
 // keeps a 32 KB window across blocks).
 //
-//   K-a png_strip_kernel   one CTA per strip: per-row filter choice (the minimum sum of |signed
-//                          residual| over the five PNG filters, the libpng heuristic), LZ77 parse
-//                          (256 independent segments, greedy, distances {1, 3, 6, row}), Huffman
-//                          code construction (length-limited 15 / 7), bit packing through
-//                          per-thread offsets from a block scan; Adler-32 partials of the strip.
+//   K-a png_strip_kernel   one CTA per strip: per-row filter choice, one warp per row (the minimum
+//                          sum of |signed residual| over the five PNG filters, the libpng
+//                          heuristic); LZ77 parse in 255 independent segments (greedy, distances
+//                          {1, 3, 6, row}); Huffman codes length-limited to 15 / 7, built in
+//                          phases (bitonic symbol sort, one-thread merge per alphabet, parallel
+//                          depths / lengths / canonical codes); the block header as a parallel
+//                          run-length coding; bit packing through per-thread offsets from block
+//                          scans; Adler-32 partials of the strip.
 //   K-b png_image_kernel   one CTA per image: Adler-32 combine, chunk offsets (scan), total size.
 //   K-b2 png_frame_kernel  image bases (strided, or packed back to back), signature, IHDR, IEND.
 //   K-c png_chunk_kernel   one CTA per strip: copy the strip's data to its chunk and CRC-32 it
