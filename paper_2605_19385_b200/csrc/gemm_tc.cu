@@ -11,9 +11,10 @@
 //   warp 1      TMEM allocator; in the leader CTA ONE thread issues every tcgen05.mma
 //               (M = 128*CG, N = BN, K = 16) into a double-buffered TMEM accumulator.
 //   warps 2..9  epilogue, two warps per TMEM lane quarter: tcgen05.ld -> (scale) + bias (+ residual)
-//               in fp32 -> fp16 STG.256, GroupNorm-32 partial sums of the fp32 values (per lane,
-//               reduced at image changes, fp64 atomics), and the residual preload of the tile that
-//               will reuse the buffer (tcgen05.st).
+//               in fp32 -> fp16, stored with STG.256 (convs) or staged in smem and TMA-stored (plain
+//               GEMMs); GroupNorm-32 partial sums of the fp32 values (per lane, reduced at image
+//               changes, fp64 atomics); at 128 output channels the residual of the tile that will
+//               reuse the accumulator is preloaded into it (tcgen05.st) -- wider outputs add it here.
 //   warps 11..14  (XF kernels only) GroupNorm + SiLU transform of each landed A halo.
 // CG = 2 runs the tile on a CTA pair (cta_group::2): each CTA stages its 128 A rows and half of B
 // (BN/2 rows); the leader's MMA reads both halves.
