@@ -39,6 +39,28 @@ def test_header_compiles_as_c(tmp_path):
     assert r == 0
 
 
+def test_headers_compile_and_link_as_cpp20(tmp_path):
+    """The reference is C++20: the public headers compile warning-free there, every entry point the
+    integration uses links against liblbx.so, and the host-only ones run without a GPU."""
+    src = tmp_path / "t.cpp"
+    src.write_text(
+        '#include "lbx/reconstruct.h"\n#include "lbx/batcher.h"\n#include "lbx/batch_pick.h"\n'
+        '#include "lbx/lblp.h"\n#include <cstdio>\n'
+        "int main() {\n"
+        "  const double c[3] = {8.0, 16.0, 24.0};\n"
+        "  if (lbx_batch_pick(c, 3, 5, 32) != lbx_batch_pick_rule(c, 3, 5, 32)) return 1;\n"
+        "  if (lbx_png_bound(1024, 1024) == 0 || lbx_pack_bound(16, 128, 128) == 0) return 2;\n"
+        "  auto a = &lbx_reconstruct; auto b = &lbx_reconstruct_png; auto d = &lbx_op_unpack;\n"
+        "  auto e = &lbx_batcher_create; auto f = &lbx_pack_device; (void)a; (void)b; (void)d; (void)e; (void)f;\n"
+        "  return 0;\n}\n")
+    lib_dir = os.path.join(ROOT, "paper_2605_19385_b200")
+    exe = tmp_path / "t"
+    r = os.system(f"g++ -std=c++20 -Wall -Wextra -Werror -I {ROOT}/include {src} -L {lib_dir} -llbx "
+                  f"-Wl,-rpath,{lib_dir} -o {exe}")
+    assert r == 0
+    assert os.system(str(exe)) == 0
+
+
 def test_no_device_fails_loudly(lbx):
     import torch
     if torch.cuda.is_available():
