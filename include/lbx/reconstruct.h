@@ -135,6 +135,11 @@ lbx_status lbx_op_unpack(const uint8_t* blobs_dev, const unsigned long long* off
                          uint32_t n, uint32_t c, uint32_t h, uint32_t w, void* out_dev, int* err_dev,
                          lbx_stream stream);
 
+/* Page-locked host memory for blobs and outputs (cudaMallocHost): copies to and from it run at full
+ * PCIe rate, where pageable memory goes through a staging copy.  NULL on failure. */
+void* lbx_host_alloc(size_t bytes);
+void lbx_host_free(void* p);
+
 /* Thread-local description of the last error on this thread ("" if none). */
 const char* lbx_last_error(void);
 

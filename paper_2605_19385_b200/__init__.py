@@ -30,6 +30,7 @@ SYMBOLS = [
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
     "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
     "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png", "lbx_op_unpack", "lbx_op_set_grid_limits",
+    "lbx_host_alloc", "lbx_host_free",
 ]
 
 
@@ -116,8 +117,13 @@ def lib() -> ctypes.CDLL:
     L.lbx_reconstruct_png.argtypes = [vp, vp, vp, u32, vp, ctypes.c_size_t, vp, vp]
     L.lbx_op_unpack.argtypes = [vp, vp, vp, u32, u32, u32, u32, vp, vp, vp]
     L.lbx_op_set_grid_limits.argtypes = [i32, i32]
+    L.lbx_host_alloc.argtypes = [ctypes.c_size_t]
+    L.lbx_host_alloc.restype = vp
+    L.lbx_host_free.argtypes = [vp]
+    L.lbx_host_free.restype = None
     for name in SYMBOLS:
-        if name not in ("lbx_param_count", "lbx_last_error", "lbx_pack_bound", "lbx_png_bound"):
+        if name not in ("lbx_param_count", "lbx_last_error", "lbx_pack_bound", "lbx_png_bound", "lbx_host_alloc",
+                        "lbx_host_free"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

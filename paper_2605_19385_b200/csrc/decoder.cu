@@ -1096,6 +1096,15 @@ lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode) {
   return LBX_OK;
 }
 
+void* lbx_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  return cudaMallocHost(&p, bytes) == cudaSuccess ? p : nullptr;
+}
+
+void lbx_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
 lbx_status lbx_op_set_grid_limits(int gemm_sms, int apply_sms) {
   lbx::gemm_tc_set_max_sms(gemm_sms);
   lbx::kernels_set_apply_max_sms(apply_sms);

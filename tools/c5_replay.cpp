@@ -129,7 +129,13 @@ bool measure_curve(int device, int maxb, const std::vector<std::vector<uint8_t>>
     std::fprintf(stderr, "decoder: %s\n", lbx_last_error());
     return false;
   }
-  std::vector<uint8_t> rgb((size_t)maxb * 1024 * 1024 * 3);
+  uint8_t* rgb_mem = static_cast<uint8_t*>(lbx_host_alloc((size_t)maxb * 1024 * 1024 * 3));  // pinned, as live
+  if (!rgb_mem) {
+    std::fprintf(stderr, "pinned host allocation failed\n");
+    lbx_decoder_destroy(dec);
+    return false;
+  }
+  struct View { uint8_t* p; uint8_t* data() { return p; } } rgb{rgb_mem};
   std::vector<const uint8_t*> ptrs;
   std::vector<size_t> sizes;
   for (int i = 0; i < maxb; ++i) {
@@ -158,6 +164,7 @@ bool measure_curve(int device, int maxb, const std::vector<std::vector<uint8_t>>
     std::fprintf(stderr, "service b=%d: %.2f ms (%.1f img/s, %d reps)\n", b, pts[k], b * 1000.0 / pts[k], reps);
   }
   lbx_decoder_destroy(dec);
+  lbx_host_free(rgb_mem);
   return true;
 }
 
@@ -239,7 +246,14 @@ int main(int argc, char** argv) {
     const size_t img = 1024ull * 1024 * 3;
     // output buffers in flight: enough that small batch caps never stall submission
     const int nbuf = std::max(64, 4 * o.rp.max_batch) * o.n_devices;
-    std::vector<uint8_t> pool((size_t)nbuf * img);
+    // page-locked output buffers, as an integration would use (pageable memory adds a staging copy)
+    uint8_t* pool_mem = static_cast<uint8_t*>(lbx_host_alloc((size_t)nbuf * img));
+    std::vector<uint8_t> pool_fallback;
+    if (!pool_mem) {
+      pool_fallback.resize((size_t)nbuf * img);
+      pool_mem = pool_fallback.data();
+    }
+    struct PoolView { uint8_t* p; uint8_t* data() { return p; } } pool{pool_mem};
     std::vector<int> free_bufs;
     for (int i = nbuf - 1; i >= 0; --i) free_bufs.push_back(i);
     std::vector<int> buf_of(jobs.size(), -1);
@@ -278,6 +292,7 @@ int main(int argc, char** argv) {
     while (lbx_batcher_pending(b)) drain(10000);
     const double wall = (now_ms() - wall0) / 1000.0;
     lbx_batcher_destroy(b);
+    if (pool_fallback.empty()) lbx_host_free(pool_mem);
     if (!o.dump.empty() && !all_comp.empty()) {
       FILE* f = std::fopen(o.dump.c_str(), "w");
       const uint64_t base = all_comp.front().t_submit_us;
