@@ -49,7 +49,8 @@ typedef enum { LBX_FAMILY_SD15 = 0, LBX_FAMILY_SD3 = 1, LBX_FAMILY_FLUX = 2 } lb
 /* Decoder descriptor.  Latent shapes: 4x64x64 (-> 512^2), 4x128x128 / 16x128x128 (-> 1024^2). */
 typedef struct {
   int family;                 /* lbx_family: sets latent channels, scaling/shift, post_quant_conv */
-  uint32_t latent_h, latent_w; /* latent spatial size; output is 8x larger */
+  uint32_t latent_h, latent_w; /* latent spatial size, output 8x larger: latent_w 64 or a multiple of
+                                  128, latent_h even, both in [8, 512] (LBX_E_CONFIG otherwise) */
   uint64_t weight_seed;       /* used when weights == NULL (deterministic generator) */
   const float* weights;       /* optional: all parameters, fp32, canonical order (lbx_param_count) */
   size_t weights_count;       /* number of floats in `weights` */
