@@ -1,7 +1,9 @@
 /*
  * lbx/batch_pick.h -- the batch-size rule behind lbx_batch_pick (include/lbx/batcher.h), header-only
  * so the config-5 simulator (tools/lb_sim.cpp, built standalone against the reference) applies the
- * same rule as the live batcher.
+ * same rule as the live batcher.  It is the batching decision the reference's FIFO service never
+ * makes: Engine::on_job_ready (proj/src/sim.cpp:409-429) serves one job per GPU at a constant
+ * decode_ms (proj/include/latentbox/sim.hpp:19).
  */
 #ifndef LBX_BATCH_PICK_H
 #define LBX_BATCH_PICK_H
