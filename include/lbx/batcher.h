@@ -4,13 +4,16 @@
  * Replaces the simulator's GPU placement and FIFO service (proj/src/sim.cpp:238-243, 409-442) with
  * real per-GPU queues.  One worker thread per device owns one lbx_decoder per latent shape class
  * ("groups cache-miss decodes by latent shape").  An idle worker pulls the next batch, so a request
- * goes to the least-loaded GPU, as least_loaded_gpu() picks the GPU with the smallest depth.  A batch
- * closes when it reaches max_batch requests or its oldest request has waited max_wait_us.  Whole
- * requests are never split across GPUs and there is no collective: one process drives all GPUs of a
- * box, and requests are independent.
+ * goes to the least-loaded GPU, as least_loaded_gpu() picks the GPU with the smallest depth; a worker
+ * that already has a batch in flight pre-stages a second one (lbx_reconstruct_submit) only while no
+ * worker is idle.  A batch closes when its queue holds max_batch requests, its oldest request has
+ * waited max_wait_us, or (policy 1) more requests would not change the size lbx_batch_pick chooses;
+ * any ready queue is served oldest-head first.  Whole requests are never split across GPUs and there
+ * is no collective: one process drives all GPUs of a box, and requests are independent.
  *
  * Each completion carries the timestamps that Engine::on_job_done feeds to observe_latency:
- * queue + batch wait = t_start - t_submit, and GPU = t_end - t_start (sim.cpp:438-440).
+ * queue + batch wait = t_start - t_submit, and service = t_end - t_start (sim.cpp:438-440); with a
+ * pre-staged batch the service includes the wait behind the batch ahead of it on the same GPU.
  */
 #ifndef LBX_BATCHER_H
 #define LBX_BATCHER_H
@@ -57,7 +60,8 @@ lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out);
 lbx_status lbx_batcher_destroy(lbx_batcher* b);
 
 /* Enqueue one request.  The blob is copied.  rgb_out (8h x 8w x 3 bytes, host memory; pinned is
- * fastest) must stay valid until the request's completion is returned by lbx_batcher_poll. */
+ * fastest) must stay valid until the request's completion is returned by lbx_batcher_poll.  A
+ * request_id still in flight (submitted, completion not yet polled) is rejected with LBX_E_CONFIG. */
 lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob, size_t nbytes,
                               uint8_t* rgb_out);
 

@@ -72,8 +72,9 @@ lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t cou
 
 lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out);
 lbx_status lbx_decoder_destroy(lbx_decoder* dec);
-/* Capture (without running) the CUDA graphs of the host-buffer reconstruct path for every batch
- * size 1..n_max, so the first request of each size does not pay graph capture (~tens of ms). */
+/* Capture (without running) the CUDA graphs for every batch size 1..n_max, so the first request of
+ * each size does not pay graph capture (~tens of ms).  Graphs run on the decoder's own latent / RGB
+ * buffers; every entry point (including lbx_decode on caller device buffers) reuses them. */
 lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max);
 
 /* Packed LBLP blobs (HOST memory) -> fp16 NCHW latents on the device, bit-exact.  Blob shapes must
@@ -94,6 +95,22 @@ lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const 
 /* Vectored form: image i lands in rgb_hosts[i] (8h x 8w x 3 bytes each).  Synchronous. */
 lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                              uint8_t* const* rgb_hosts, lbx_stream stream);
+
+/* Asynchronous, pipelined form of lbx_reconstruct_v (what lbx_batcher's workers use).  Stages the
+ * batch and enqueues H2D + unpack, the decode graph and the D2H on three streams of the decoder,
+ * then returns a ticket without waiting.  Up to two batches may be in flight: batch k+1's host
+ * staging, H2D and unpack and batch k-1's D2H overlap batch k's decode (PAPER.md:667-670 runs
+ * decompression and encoding in pools around GPU inference).  A third submit before the oldest
+ * ticket is waited for returns LBX_E_RUNTIME.  Blob headers are validated before anything is
+ * enqueued (LBX_E_FORMAT, no ticket).  rgb_hosts[i] must stay valid until the wait returns. */
+lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                                  uint8_t* const* rgb_hosts, uint64_t* ticket);
+/* Block until the batch of `ticket` is in rgb_hosts; its status (LBX_E_FORMAT if the device unpack
+ * found a malformed blob).  Each ticket is waited for exactly once. */
+lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket);
+
+/* CUDA graphs this decoder has captured (one per batch size; caller buffers never cause one). */
+uint64_t lbx_graph_captures(lbx_decoder* dec);
 
 /* Same path from fp16 NCHW latents in HOST memory (no codec): H2D -> decode -> D2H.  Synchronous. */
 lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
@@ -168,11 +185,12 @@ int lbx_launch_count(lbx_decoder* dec, uint32_t n);
 /* tcgen05 GEMM / conv: out[m, n] = alpha*rs[m]*sum_k A[m,k]*B[n,k] + bias[n] + resid[m,n].
  * mode 0 plain (A [M][K], row stride lda); mode 1 conv3x3 pad 1 (A NHWC [b][h][w][c], K = 9c);
  * mode 2 nearest-2x upsample + conv3x3 as 4 sub-pixel 2x2 convs (B = [4][N][4c], out 2h x 2w).
- * gn_stats (optional, double [b][32][2], accumulated) gets GroupNorm-32 partial sums of out.
+ * gn_stats (optional, uint64 [b][32][2][2], accumulated) gets GroupNorm-32 partial sums of out as
+ * exact fixed-point pairs: value = (int64)hi * 4 + lo * 2^-30 (order-independent, see gnfix.cuh).
  * cta_group/bn: 0 = auto, else force 1|2 and 128|256. */
 lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
                        const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
-                       const float* row_scale, float alpha, double* gn_stats, int cta_group, int bn,
+                       const float* row_scale, float alpha, uint64_t* gn_stats, int cta_group, int bn,
                        lbx_stream stream);
 /* Same op with an optional extra K segment from a second plain operand A2 [M][K2] (row stride lda2):
  * out += A2 . B[:, K:K+K2]^T inside the tensor-core accumulation (B then has K + K2 columns).  The
@@ -192,7 +210,7 @@ typedef struct {
   int ldr;
   const float* row_scale;
   float alpha;
-  double* gn_stats;
+  uint64_t* gn_stats;
   int cta_group, bn;
   const float* gn_ss; /* optional: fused A' = SiLU(A * ss[img][c].x + ss[img][c].y) (conv3x3), float pairs */
   int b_mn_major;     /* plain GEMM: B is [K][N] with N contiguous (row stride ldb) instead of [N][K] */
@@ -231,10 +249,11 @@ lbx_status lbx_op_attention(const void* qkv, void* out, int n, int L, lbx_stream
 /* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
 lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
 /* GroupNorm finalize + apply; silu 0 = identity, 1 = fp32 SiLU, 2 = packed-half SiLU; y may alias x. */
-lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta,
+lbx_status lbx_op_groupnorm(const void* x, void* y, const uint64_t* stats, const float* gamma, const float* beta,
                             int b, int hw, int c, int silu, float eps, lbx_stream stream);
-/* GroupNorm-32 statistics of x ([b][hw][c] fp16) into stats (double [b][32][2], zeroed here). */
-lbx_status lbx_op_gn_stats(const void* x, double* stats, int b, int hw, int c, lbx_stream stream);
+/* GroupNorm-32 statistics of x ([b][hw][c] fp16) into stats (uint64 [b][32][2][2] fixed point, zeroed
+ * here). */
+lbx_status lbx_op_gn_stats(const void* x, uint64_t* stats, int b, int hw, int c, lbx_stream stream);
 
 #ifdef __cplusplus
 }

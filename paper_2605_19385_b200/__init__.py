@@ -30,7 +30,8 @@ SYMBOLS = [
     "lbx_subpixel_weights", "lbx_op_groupnorm", "lbx_op_gn_stats", "lbx_profile", "lbx_launch_count", "lbx_op_set_debug", "lbx_op_gemm_desc", "lbx_decoder_prepare",
     "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
     "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png", "lbx_op_unpack", "lbx_op_set_grid_limits",
-    "lbx_host_alloc", "lbx_host_free",
+    "lbx_host_alloc", "lbx_host_free", "lbx_reconstruct_v", "lbx_reconstruct_submit", "lbx_reconstruct_wait",
+    "lbx_graph_captures",
 ]
 
 
@@ -121,9 +122,14 @@ def lib() -> ctypes.CDLL:
     L.lbx_host_alloc.restype = vp
     L.lbx_host_free.argtypes = [vp]
     L.lbx_host_free.restype = None
+    L.lbx_reconstruct_v.argtypes = [vp, vp, vp, u32, vp, vp]
+    L.lbx_reconstruct_submit.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_uint64)]
+    L.lbx_reconstruct_wait.argtypes = [vp, ctypes.c_uint64]
+    L.lbx_graph_captures.argtypes = [vp]
+    L.lbx_graph_captures.restype = ctypes.c_uint64
     for name in SYMBOLS:
         if name not in ("lbx_param_count", "lbx_last_error", "lbx_pack_bound", "lbx_png_bound", "lbx_host_alloc",
-                        "lbx_host_free"):
+                        "lbx_host_free", "lbx_graph_captures"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L
@@ -197,6 +203,11 @@ class Decoder:
     def out_hw(self):
         return 8 * self.h, 8 * self.w
 
+    @property
+    def rgb_bytes(self):
+        """Bytes of one decoded image (8h x 8w x 3 uint8)."""
+        return 64 * self.h * self.w * 3
+
     # -- device-pointer entry points (pointers are ints, e.g. torch.Tensor.data_ptr()) --------
     def decode_ptr(self, latents_dev: int, n: int, rgb_dev: int, stream: int = 0) -> None:
         check(lib().lbx_decode(self._h, latents_dev, n, rgb_dev, stream or None))
@@ -217,12 +228,43 @@ class Decoder:
     def launch_count(self, n: int) -> int:
         return int(lib().lbx_launch_count(self._h, n))
 
+    def graph_captures(self) -> int:
+        """CUDA graphs captured so far (one per batch size)."""
+        return int(lib().lbx_graph_captures(self._h))
+
+    def prepare(self, n_max: int) -> None:
+        check(lib().lbx_decoder_prepare(self._h, n_max))
+
+    # -- asynchronous pipeline (lbx_reconstruct_submit / lbx_reconstruct_wait) ------------------
+    def submit(self, blobs, outs) -> int:
+        """Enqueue a batch (blobs -> outs[i], each a uint8 array of one image); returns a ticket.
+        At most two batches in flight; the buffers are kept alive until wait(ticket)."""
+        if len(outs) != len(blobs):
+            raise LbxError(E_CONFIG, "outs: one output buffer per blob")
+        for o in outs:
+            _check_out(o, self.rgb_bytes, "outs[i]")
+        arr, sizes, keep = _blob_arrays(blobs)
+        optr = (ctypes.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+        t = ctypes.c_uint64(0)
+        check(lib().lbx_reconstruct_submit(self._h, arr, sizes, len(blobs), optr, ctypes.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (keep, outs, optr)
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        try:
+            check(lib().lbx_reconstruct_wait(self._h, ticket))
+        finally:
+            getattr(self, "_inflight", {}).pop(ticket, None)
+
     # -- host entry points ---------------------------------------------------------------------
     def reconstruct(self, blobs, out: np.ndarray | None = None, stream: int = 0) -> np.ndarray:
         """Packed LBLP blobs (host) -> uint8 RGB (n, 8h, 8w, 3).  Synchronous."""
         n = len(blobs)
         if out is None:
             out = np.empty((n, 8 * self.h, 8 * self.w, 3), dtype=np.uint8)
+        _check_out(out, n * self.rgb_bytes, "out")
         arr, sizes, keep = _blob_arrays(blobs)
         check(lib().lbx_reconstruct(self._h, arr, sizes, n, out.ctypes.data, stream or None))
         return out
@@ -234,6 +276,7 @@ class Decoder:
         h, w = self.out_hw
         if out is None:
             out = np.empty(n * png_bound(h, w), np.uint8)
+        _check_out(out, 1, "out")
         arr, sizes, keep = _blob_arrays(blobs)
         psz = (ctypes.c_size_t * max(n, 1))()
         check(lib().lbx_reconstruct_png(self._h, arr, sizes, n, out.ctypes.data, out.nbytes, psz, stream or None))
@@ -247,11 +290,23 @@ class Decoder:
     def reconstruct_latents(self, latents: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """fp16 NCHW latents (host) -> uint8 RGB (n, 8h, 8w, 3)."""
         lat = np.ascontiguousarray(latents.astype(np.float16))
+        if lat.ndim != 4 or lat.shape[1:] != (self.c, self.h, self.w):
+            raise LbxError(E_CONFIG, f"latents: shape {lat.shape} != (n, {self.c}, {self.h}, {self.w})")
         n = lat.shape[0]
         if out is None:
             out = np.empty((n, 8 * self.h, 8 * self.w, 3), dtype=np.uint8)
+        _check_out(out, n * self.rgb_bytes, "out")
         check(lib().lbx_reconstruct_latents(self._h, lat.ctypes.data, n, out.ctypes.data, None))
         return out
+
+
+def _check_out(out, min_bytes, name):
+    """A host output buffer handed to the C ABI must be uint8, C-contiguous and large enough: the
+    library writes min_bytes through its raw pointer (a short or strided buffer would be overrun)."""
+    if not isinstance(out, np.ndarray) or out.dtype != np.uint8 or not out.flags.c_contiguous or not out.flags.writeable:
+        raise LbxError(E_CONFIG, f"{name}: must be a writeable C-contiguous uint8 numpy array")
+    if out.nbytes < min_bytes:
+        raise LbxError(E_CONFIG, f"{name}: {out.nbytes} bytes < the {min_bytes} the call writes")
 
 
 def _blob_arrays(blobs):
@@ -328,6 +383,21 @@ def op_gn_stats(x, stats, b, hw, c, stream=0):
     check(lib().lbx_op_gn_stats(x, stats, b, hw, c, stream or None))
 
 
+def gn_stats_buffer(b, device="cuda"):
+    """A zeroed GroupNorm statistics buffer for b images: int64 [b][32][2 (sum, sumsq)][2 (hi, lo)],
+    the exact fixed-point layout the kernels accumulate into (csrc/gnfix.cuh)."""
+    import torch
+    return torch.zeros(b, 32, 2, 2, dtype=torch.int64, device=device)
+
+
+def gn_stats_values(stats):
+    """float64 [b][32][2] (sum, sumsq) from a gn_stats_buffer: hi * 4 + lo * 2^-30."""
+    hi = stats[..., 0].double()
+    lo = stats[..., 1].view(-1).cpu().numpy().view("uint64").astype("float64")
+    import torch
+    return hi * 4.0 + torch.from_numpy(lo).reshape(hi.shape).to(hi.device) * 2.0 ** -30
+
+
 # ---------------------------------------------------------------------------- batcher (batcher.h)
 class Shape(ctypes.Structure):
     _fields_ = [("family", ctypes.c_int), ("latent_h", ctypes.c_uint32), ("latent_w", ctypes.c_uint32)]
@@ -381,13 +451,19 @@ class Batcher:
         h = ctypes.c_void_p()
         check(L.lbx_batcher_create(ctypes.byref(d), ctypes.byref(h)))
         self._h = h
+        self._rgb_bytes = [64 * sh * sw * 3 for _, sh, sw in shapes]
         self._keep = {}
 
     def submit(self, request_id: int, shape: int, blob: bytes, out: np.ndarray):
+        """Enqueue one request; `out` (uint8, one image) is written by a worker and kept alive here
+        until its completion is polled.  A request_id already in flight is rejected (LBX_E_CONFIG)."""
+        if not 0 <= shape < len(self._rgb_bytes):
+            raise LbxError(E_CONFIG, f"shape: no shape class {shape}")
+        _check_out(out, self._rgb_bytes[shape], "out")
         buf = np.frombuffer(blob, dtype=np.uint8)
-        self._keep[request_id] = out
         check(_batcher_lib().lbx_batcher_submit(self._h, request_id, shape, buf.ctypes.data, buf.size,
                                                 out.ctypes.data))
+        self._keep[request_id] = out  # after the C side accepted it: a rejected duplicate keeps the original
 
     def poll(self, cap=256, wait_us=1000):
         arr = (Completion * cap)()

@@ -1,12 +1,17 @@
 // Multi-GPU decode-on-miss request batcher (include/lbx/batcher.h).
 //
 // One worker thread per device owns one lbx_decoder per shape class (created on that thread's
-// device).  Requests wait in per-shape FIFO queues.  An idle worker closes a batch on the shape
-// whose head request is oldest.  It does so once that queue holds max_batch requests, once the head
-// has waited max_wait_us, or when draining at shutdown.  Then it runs one lbx_reconstruct_v.  Pulling
-// work only when idle is what makes the placement least-loaded-first (proj/src/sim.cpp:238-243);
-// the FIFO order per shape mirrors the simulator's FIFO GPU (sim.cpp:413).  With policy 1 the batch
-// size comes from lbx_batch_pick over the worker's own measured service curve.
+// device).  Requests wait in per-shape FIFO queues.  A worker closes a batch on a ready queue: one
+// holding max_batch requests, one whose head has waited max_wait_us, (policy 1) one where more
+// requests would not change the size lbx_batch_pick chooses, or any queue when draining at shutdown;
+// among ready queues the oldest head goes first.  Batches run through the decoder's asynchronous
+// pipeline (lbx_reconstruct_submit / _wait): a worker keeps up to two batches in flight, so batch
+// k+1's host staging, H2D and unpack and batch k-1's D2H overlap batch k's decode -- the paper's
+// fetch / decompress / encode pools around GPU inference.  A worker with work in
+// flight takes another batch only when no worker is idle, so placement stays least-loaded-first
+// (proj/src/sim.cpp:238-243); the FIFO order per shape mirrors the simulator's FIFO GPU
+// (sim.cpp:413).  With policy 1 the batch size comes from lbx_batch_pick over the worker's own
+// measured service curve.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +23,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <unordered_set>
 #include <vector>
 
 #include "lbx/batch_pick.h"
@@ -58,8 +64,14 @@ struct lbx_batcher {
   std::string init_error;
   int init_status = LBX_OK;
   int workers_ready = 0;
+  int idle = 0;                            // workers with nothing in flight, waiting for work
+  std::unordered_set<uint64_t> live_ids;   // submitted, not yet returned by poll
+  std::vector<std::vector<std::vector<double>>> curves;  // [worker][shape] (policy 1)
 
   void worker(int dev_index);
+  // Index of a ready shape queue (see the header comment), or -1; *next_deadline = the earliest
+  // time a non-ready queue becomes ready by age.  Called with mu held.
+  int ready_shape(int di, uint64_t now, uint64_t* next_deadline) const;
 };
 
 namespace {
@@ -102,10 +114,37 @@ std::vector<double> measure_curve(lbx_decoder* dec, int fam_channels, uint32_t l
 
 }  // namespace
 
+int lbx_batcher::ready_shape(int di, uint64_t now, uint64_t* next_deadline) const {
+  int best = -1;
+  uint64_t best_t = UINT64_MAX;
+  *next_deadline = UINT64_MAX;
+  for (size_t s = 0; s < queues.size(); ++s) {
+    const auto& q = queues[s];
+    if (q.empty()) continue;
+    const uint64_t head = q.front().t_submit;
+    bool ready = stopping || q.size() >= desc.max_batch || now - head >= desc.max_wait_us;
+    if (!ready && desc.policy == 1) {
+      // the size the rule closes now equals the size it would close from a full queue: waiting
+      // for more requests cannot change the batch, only delay it
+      const auto& cv = curves[di][s];
+      const uint32_t now_pick = lbx_batch_pick_rule(cv.empty() ? nullptr : cv.data(), (uint32_t)cv.size(),
+                                                    (uint32_t)q.size(), desc.max_batch);
+      const uint32_t full_pick = lbx_batch_pick_rule(cv.empty() ? nullptr : cv.data(), (uint32_t)cv.size(),
+                                                     desc.max_batch, desc.max_batch);
+      ready = now_pick == full_pick;
+    }
+    if (ready && head < best_t) {
+      best_t = head;
+      best = (int)s;
+    }
+    if (!ready) *next_deadline = std::min(*next_deadline, head + desc.max_wait_us);
+  }
+  return best;
+}
+
 void lbx_batcher::worker(int di) {
   const int device = devices[di];
   std::vector<lbx_decoder*> decs(shapes.size(), nullptr);
-  std::vector<std::vector<double>> curves(shapes.size());  // policy 1: this device's service curves
   lbx_status st = LBX_OK;
   for (size_t s = 0; s < shapes.size() && st == LBX_OK; ++s) {
     lbx_decoder_desc d{};
@@ -119,8 +158,10 @@ void lbx_batcher::worker(int di) {
     if (st == LBX_OK) st = lbx_decoder_prepare(decs[s], desc.max_batch);  // no capture on the request path
     if (st == LBX_OK && desc.policy == 1) {
       const int ch = shapes[s].family == LBX_FAMILY_SD15 ? 4 : 16;
-      curves[s] = measure_curve(decs[s], ch, shapes[s].latent_h, shapes[s].latent_w, desc.max_batch);
-      if (curves[s].empty()) st = LBX_E_CUDA;
+      auto c = measure_curve(decs[s], ch, shapes[s].latent_h, shapes[s].latent_w, desc.max_batch);
+      if (c.empty()) st = LBX_E_CUDA;
+      std::lock_guard<std::mutex> g(mu);
+      curves[di][s] = std::move(c);
     }
   }
   {
@@ -133,65 +174,87 @@ void lbx_batcher::worker(int di) {
   }
   cv_done.notify_all();
 
-  std::vector<Request> batch;
+  struct InFlight {
+    uint64_t ticket;
+    int shape;
+    std::vector<Request> reqs;
+    uint64_t t_start;
+  };
+  std::deque<InFlight> inflight;  // <= 2 (the decoder pipeline's depth)
   std::vector<const uint8_t*> blobs;
   std::vector<size_t> sizes;
   std::vector<uint8_t*> outs;
-  for (;;) {
-    int shape = -1;
-    {
-      std::unique_lock<std::mutex> lk(mu);
-      for (;;) {
-        // oldest head across shapes
-        uint64_t oldest = UINT64_MAX;
-        shape = -1;
-        for (size_t s = 0; s < queues.size(); ++s)
-          if (!queues[s].empty() && queues[s].front().t_submit < oldest) {
-            oldest = queues[s].front().t_submit;
-            shape = (int)s;
-          }
-        if (shape >= 0) {
-          const bool full = queues[shape].size() >= desc.max_batch;
-          const uint64_t waited = now_us() - oldest;
-          if (full || waited >= desc.max_wait_us || stopping || st != LBX_OK) break;
-          cv_work.wait_for(lk, std::chrono::microseconds(desc.max_wait_us - waited));
-          continue;
-        }
-        if (stopping) break;
-        cv_work.wait(lk);
-      }
-      if (shape < 0) break;  // stopping and drained
-      auto& q = queues[shape];
-      const auto& cv = curves[shape];
-      const size_t take = lbx_batch_pick(cv.empty() ? nullptr : cv.data(), (uint32_t)cv.size(), (uint32_t)q.size(),
-                                         desc.max_batch);
-      batch.clear();
-      for (size_t i = 0; i < take; ++i) {
-        batch.push_back(std::move(q.front()));
-        q.pop_front();
-      }
-    }
-    cv_work.notify_all();  // another idle worker may take the remainder
-    const uint64_t t_start = now_us();
-    lbx_status rs = st;
-    if (rs == LBX_OK) {
-      blobs.clear();
-      sizes.clear();
-      outs.clear();
-      for (auto& r : batch) {
-        blobs.push_back(r.blob.data());
-        sizes.push_back(r.blob.size());
-        outs.push_back(r.rgb);
-      }
-      rs = lbx_reconstruct_v(decs[shape], blobs.data(), sizes.data(), (uint32_t)batch.size(), outs.data(), nullptr);
-    }
+  auto complete = [&](std::vector<Request>& reqs, lbx_status rs, uint64_t t_start) {
     const uint64_t t_end = now_us();
     {
       std::lock_guard<std::mutex> g(mu);
-      for (auto& r : batch)
-        done.push_back(lbx_completion{r.id, (int)rs, device, (uint32_t)batch.size(), r.t_submit, t_start, t_end});
+      for (auto& r : reqs)
+        done.push_back(lbx_completion{r.id, (int)rs, device, (uint32_t)reqs.size(), r.t_submit, t_start, t_end});
     }
     cv_done.notify_all();
+  };
+  for (;;) {
+    int shape = -1;
+    std::vector<Request> batch;
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      if (inflight.empty()) {
+        ++idle;
+        for (;;) {
+          uint64_t deadline = UINT64_MAX;
+          const uint64_t now = now_us();
+          shape = ready_shape(di, now, &deadline);
+          if (shape >= 0 || (stopping && deadline == UINT64_MAX)) break;
+          if (st != LBX_OK && deadline != UINT64_MAX) {  // failed worker: drain with errors
+            for (size_t s = 0; s < queues.size() && shape < 0; ++s)
+              if (!queues[s].empty()) shape = (int)s;
+            break;
+          }
+          if (deadline == UINT64_MAX) cv_work.wait(lk);
+          else cv_work.wait_for(lk, std::chrono::microseconds(deadline - now));
+        }
+        --idle;
+      } else if (inflight.size() < 2 && idle == 0) {
+        uint64_t deadline;
+        shape = ready_shape(di, now_us(), &deadline);
+      }
+      if (shape >= 0) {
+        auto& q = queues[shape];
+        const auto& cv = curves[di][shape];
+        const size_t take = lbx_batch_pick_rule(cv.empty() ? nullptr : cv.data(), (uint32_t)cv.size(),
+                                                (uint32_t)q.size(), desc.max_batch);
+        for (size_t i = 0; i < take; ++i) {
+          batch.push_back(std::move(q.front()));
+          q.pop_front();
+        }
+      }
+    }
+    if (shape >= 0) {
+      cv_work.notify_all();  // another idle worker may take the remainder
+      const uint64_t t_start = now_us();
+      lbx_status rs = st;
+      uint64_t ticket = 0;
+      if (rs == LBX_OK) {
+        blobs.clear();
+        sizes.clear();
+        outs.clear();
+        for (auto& r : batch) {
+          blobs.push_back(r.blob.data());
+          sizes.push_back(r.blob.size());
+          outs.push_back(r.rgb);
+        }
+        rs = lbx_reconstruct_submit(decs[shape], blobs.data(), sizes.data(), (uint32_t)batch.size(), outs.data(),
+                                    &ticket);
+      }
+      if (rs == LBX_OK) inflight.push_back(InFlight{ticket, shape, std::move(batch), t_start});
+      else complete(batch, rs, t_start);
+      continue;
+    }
+    if (inflight.empty()) break;  // stopping and drained
+    InFlight& f = inflight.front();
+    const lbx_status rs = lbx_reconstruct_wait(decs[f.shape], f.ticket);
+    complete(f.reqs, rs, f.t_start);
+    inflight.pop_front();
   }
   for (auto* d : decs)
     if (d) lbx_decoder_destroy(d);
@@ -215,6 +278,7 @@ lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out) {
   b->devices.assign(desc->devices, desc->devices + desc->n_devices);
   b->shapes.assign(desc->shapes, desc->shapes + desc->n_shapes);
   b->queues.resize(desc->n_shapes);
+  b->curves.assign(desc->n_devices, std::vector<std::vector<double>>(desc->n_shapes));
   for (int i = 0; i < desc->n_devices; ++i) b->workers.emplace_back(&lbx_batcher::worker, b, i);
   {
     std::unique_lock<std::mutex> lk(b->mu);
@@ -249,7 +313,10 @@ lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, co
   Request r{request_id, std::vector<uint8_t>(blob, blob + nbytes), rgb_out, now_us()};
   {
     std::lock_guard<std::mutex> g(b->mu);
-    if (b->stopping) return LBX_E_RUNTIME;
+    if (b->stopping) return lbx::set_last_error(LBX_E_RUNTIME, "lbx_batcher_submit: batcher is stopping");
+    if (!b->live_ids.insert(request_id).second)
+      return lbx::set_last_error(LBX_E_CONFIG, "lbx_batcher_submit: request_id " + std::to_string(request_id) +
+                                                   " is already in flight");
     b->queues[shape].push_back(std::move(r));
     ++b->pending;
   }
@@ -264,6 +331,7 @@ int lbx_batcher_poll(lbx_batcher* b, lbx_completion* out, int cap, uint32_t wait
     b->cv_done.wait_for(lk, std::chrono::microseconds(wait_us), [&] { return !b->done.empty(); });
   const int n = (int)(b->done.size() < (size_t)cap ? b->done.size() : (size_t)cap);
   std::memcpy(out, b->done.data(), n * sizeof(lbx_completion));
+  for (int i = 0; i < n; ++i) b->live_ids.erase(out[i].request_id);
   b->done.erase(b->done.begin(), b->done.begin() + n);
   b->pending -= (uint64_t)n;
   return n;

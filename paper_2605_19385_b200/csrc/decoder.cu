@@ -2,8 +2,12 @@
 //
 // One lbx_decoder per GPU owns: device weights in GEMM-ready layouts (fp16 K-major, conv taps
 // (ky,kx,ci) innermost-ci, upsample convs pre-folded into 4 sub-pixel 2x2 kernels), an activation
-// arena sized for max_batch (NHWC fp16), and a cache of CUDA graphs keyed by (n, in, out) -- the
-// paper wraps its TensorRT engine in a CUDA graph the same way.
+// arena sized for max_batch (NHWC fp16), and one CUDA graph per batch size n, captured once on the
+// decoder's own latent / RGB buffers (caller buffers are copied in and out, so new caller pointers
+// never trigger a capture) -- the paper wraps its TensorRT engine in a CUDA graph the same way
+// (PAPER.md:675).  Two asynchronous slots (lbx_reconstruct_submit / _wait) pipeline host blobs
+// through three streams: H2D + unpack of batch k+1 and the D2H of batch k-1 overlap batch k's graph
+// (the paper's fetch / decompress / encode pools around GPU inference).
 //
 // Layer plan per micro-batch, buffers X (residual stream), A (normalised
 // activations / shortcut / upsample output), H (conv1 output, normalised in place; attention QKV):
@@ -32,6 +36,7 @@
 
 #include "codec.h"
 #include "gemm_tc.cuh"
+#include "gnfix.cuh"
 #include "kernels.cuh"
 #include "lbx/reconstruct.h"
 #include "model.h"
@@ -92,22 +97,45 @@ class Decoder {
   void* arena = nullptr;
   __half *X = nullptr, *A = nullptr, *Hb = nullptr, *S = nullptr, *Vt = nullptr, *lat = nullptr;
   float* rowscale = nullptr;
-  double* stats = nullptr;
+  unsigned long long* stats = nullptr;  // GroupNorm sites, gnfix.cuh layout
   float2* ss = nullptr;
   uint8_t* rgb = nullptr;
   int* err = nullptr;
   static constexpr int kMaxSites = 64;
   int s_imgs = 1;                 // images whose attention scores fit the S buffer at once
 
-  // blob staging
-  uint8_t* blob_dev = nullptr;
-  size_t blob_dev_cap = 0;
-  uint8_t* blob_host = nullptr;  // pinned
-  size_t blob_host_cap = 0;
-  unsigned long long* offs_dev = nullptr;
-  unsigned int* sizes_dev = nullptr;
-  unsigned long long* offs_host = nullptr;  // pinned [max_batch] offsets + sizes
-  int* err_host = nullptr;
+  // host-blob staging: pinned host copy -> one H2D -> device blobs + offset/size table
+  struct Staging {
+    uint8_t* host = nullptr;  // pinned
+    uint8_t* dev = nullptr;
+    size_t cap = 0;
+    unsigned long long* offs_dev = nullptr;  // [max_batch] offsets, then [max_batch] u32 sizes
+    unsigned int* sizes_dev = nullptr;
+    unsigned long long* table_host = nullptr;  // pinned mirror of the table
+    cudaEvent_t copied = nullptr;  // the last H2D out of `host` has completed: host may be rewritten
+  };
+  Staging sync_st;        // the synchronous calls (lbx_unpack / lbx_reconstruct*)
+  int* err_host = nullptr;  // pinned
+  // asynchronous pipeline (lbx_reconstruct_submit / lbx_reconstruct_wait): two slots, three streams
+  struct Slot {
+    Staging st;
+    __half* lat = nullptr;
+    uint8_t* rgb = nullptr;
+    int* err = nullptr;
+    int* err_host = nullptr;  // pinned
+    cudaEvent_t unpacked = nullptr, computed = nullptr, drained = nullptr;
+    bool busy = false;
+    uint64_t ticket = 0;
+  };
+  Slot slots[2];
+  cudaStream_t in_stream = nullptr, out_stream = nullptr;
+  uint64_t next_ticket = 1;
+  // cross-stream ordering of the work that touches decoder-owned device buffers: a call on a
+  // different stream than the previous one first waits for the previous call's last enqueued work
+  cudaEvent_t last_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool last_valid = false;
+  uint64_t captures = 0;  // CUDA graphs captured so far (one per batch size n)
 
   // return path (lbx_reconstruct_png), allocated on first use
   uint8_t* png_dev = nullptr;    // max_batch PNGs back to back
@@ -115,7 +143,7 @@ class Decoder {
   uint32_t* png_sizes = nullptr;
   uint32_t* png_sizes_host = nullptr;  // pinned
 
-  std::map<std::tuple<int, const void*, const void*>, cudaGraphExec_t> graphs;
+  std::map<int, cudaGraphExec_t> graphs;
   std::map<int, int> launch_counts;
   struct ProfRec {
     std::string name;
@@ -130,13 +158,29 @@ class Decoder {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(desc.device);
+    if (stream) cudaStreamSynchronize(stream);
+    if (in_stream) cudaStreamSynchronize(in_stream);
+    if (out_stream) cudaStreamSynchronize(out_stream);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     graphs.clear();
     if (wblock) cudaFree(wblock);
     if (arena) cudaFree(arena);
-    if (blob_dev) cudaFree(blob_dev);
-    if (blob_host) cudaFreeHost(blob_host);
-    if (offs_host) cudaFreeHost(offs_host);
+    free_staging(sync_st);
+    for (Slot& sl : slots) {
+      free_staging(sl.st);
+      if (sl.lat) cudaFree(sl.lat);
+      if (sl.err_host) cudaFreeHost(sl.err_host);
+      for (cudaEvent_t e : {sl.unpacked, sl.computed, sl.drained})
+        if (e) cudaEventDestroy(e);
+      sl = Slot{};
+    }
+    if (err_host) cudaFreeHost(err_host);
+    err_host = nullptr;
+    if (last_ev) cudaEventDestroy(last_ev);
+    last_ev = nullptr;
+    if (in_stream) cudaStreamDestroy(in_stream);
+    if (out_stream) cudaStreamDestroy(out_stream);
+    in_stream = out_stream = nullptr;
     if (png_dev) cudaFree(png_dev);
     if (png_work) cudaFree(png_work);
     if (png_sizes) cudaFree(png_sizes);
@@ -145,8 +189,6 @@ class Decoder {
     png_sizes = png_sizes_host = nullptr;
     if (stream) cudaStreamDestroy(stream);
     wblock = arena = nullptr;
-    blob_dev = blob_host = nullptr;
-    offs_host = nullptr;
     stream = nullptr;
     cudaSetDevice(cur);
   }
@@ -159,8 +201,27 @@ class Decoder {
   lbx_status alloc_arena();
   lbx_status plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, bool counting);
   lbx_status run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s);
-  lbx_status graph_for(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, cudaGraphExec_t* out);
-  lbx_status stage_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, cudaStream_t s);
+  lbx_status graph_for(int n, cudaStream_t s, cudaGraphExec_t* out);
+  lbx_status validate_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, size_t* total);
+  lbx_status stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                         cudaStream_t s, __half* lat_out, int* err_dev);
+  lbx_status alloc_slot(Slot& sl);
+  static void free_staging(Staging& st) {
+    if (st.host) cudaFreeHost(st.host);
+    if (st.dev) cudaFree(st.dev);
+    if (st.table_host) cudaFreeHost(st.table_host);
+    if (st.copied) cudaEventDestroy(st.copied);
+    st = Staging{};
+  }
+  // call-ordering helpers (see last_ev)
+  void order(cudaStream_t s) {
+    if (last_valid && last_stream != s) cudaStreamWaitEvent(s, last_ev, 0);
+  }
+  void mark(cudaStream_t s) {
+    cudaEventRecord(last_ev, s);
+    last_stream = s;
+    last_valid = true;
+  }
 };
 
 // --------------------------------------------------------------------------- weights
@@ -350,7 +411,7 @@ lbx_status Decoder::alloc_arena() {
     return o;
   };
   const size_t oX = slot(x_el * 2), oA = slot(x_el * 2), oH = slot(h_el * 2), oS = slot(s_el * 2),
-               oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oSt = slot((size_t)kMaxSites * nb * 64 * 8),
+               oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oSt = slot((size_t)kMaxSites * nb * 32 * kGnStatWords * 8),
                oSs = slot(nb * 512 * 8), oLat = slot(nb * cl * hw * 2), oRgb = slot(nb * hw * 64 * 3),
                oErr = slot(64);
   LBX_CUDA_TRY(cudaMalloc(&arena, off));
@@ -361,14 +422,37 @@ lbx_status Decoder::alloc_arena() {
   S = (__half*)(b + oS);
   Vt = (__half*)(b + oVt);
   rowscale = (float*)(b + oR);
-  stats = (double*)(b + oSt);
+  stats = (unsigned long long*)(b + oSt);
   ss = (float2*)(b + oSs);
   lat = (__half*)(b + oLat);
   rgb = b + oRgb;
   err = (int*)(b + oErr);
   LBX_CUDA_TRY(cudaMemset(err, 0, 64));
-  LBX_CUDA_TRY(cudaMallocHost(&offs_host, nb * 16 + 64));
-  err_host = reinterpret_cast<int*>(offs_host + 2 * nb);
+  LBX_CUDA_TRY(cudaMallocHost(&err_host, 64));
+  LBX_CUDA_TRY(cudaMallocHost(&sync_st.table_host, nb * 16));
+  LBX_CUDA_TRY(cudaEventCreateWithFlags(&sync_st.copied, cudaEventDisableTiming));
+  LBX_CUDA_TRY(cudaEventCreateWithFlags(&last_ev, cudaEventDisableTiming));
+  return LBX_OK;
+}
+
+// An asynchronous slot: its own staging, latents, RGB and status word (allocated on first use).
+lbx_status Decoder::alloc_slot(Slot& sl) {
+  if (sl.lat) return LBX_OK;
+  const size_t lat_b = (lat_elems(max_batch) * 2 + 1023) & ~size_t(1023);
+  void* p = nullptr;
+  LBX_CUDA_TRY(cudaMalloc(&p, lat_b + rgb_bytes(max_batch) + 64));
+  sl.lat = reinterpret_cast<__half*>(p);
+  sl.rgb = reinterpret_cast<uint8_t*>(p) + lat_b;
+  sl.err = reinterpret_cast<int*>(sl.rgb + rgb_bytes(max_batch));
+  LBX_CUDA_TRY(cudaMemset(sl.err, 0, 64));
+  LBX_CUDA_TRY(cudaMallocHost(&sl.err_host, 64));
+  LBX_CUDA_TRY(cudaMallocHost(&sl.st.table_host, (size_t)max_batch * 16));
+  for (cudaEvent_t* e : {&sl.st.copied, &sl.unpacked, &sl.computed, &sl.drained})
+    LBX_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  if (!in_stream) {
+    LBX_CUDA_TRY(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
+    LBX_CUDA_TRY(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
+  }
   return LBX_OK;
 }
 
@@ -412,7 +496,7 @@ lbx_status Decoder::init(const lbx_decoder_desc& d) {
 lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, bool counting) {
   int launches = 0;
   int site = 0;
-  const size_t site_stride = (size_t)max_batch * 64;
+  const size_t site_stride = (size_t)max_batch * 32 * kGnStatWords;
   auto site_ptr = [&](int i) { return stats + (size_t)i * site_stride; };
   auto chk = [&](cudaError_t e, const std::string& what) -> lbx_status {
     if (e != cudaSuccess) return set_err(LBX_E_CUDA, what + ": " + cudaGetErrorString(e));
@@ -655,18 +739,13 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
 #undef LBX_LAUNCH
 }
 
-lbx_status Decoder::graph_for(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s, cudaGraphExec_t* out) {
-  auto key = std::make_tuple(n, (const void*)lat_in, (const void*)rgb_out);
-  auto it = graphs.find(key);
+lbx_status Decoder::graph_for(int n, cudaStream_t s, cudaGraphExec_t* out) {
+  auto it = graphs.find(n);
   if (it == graphs.end()) {
-    // one graph per (batch size, buffers): the internal-buffer graphs of every n <= max_batch fit
-    if (graphs.size() >= (size_t)(2 * max_batch + 16)) {
-      for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
-      graphs.clear();
-    }
+    // one graph per batch size, on the decoder's own buffers (lat -> rgb): at most max_batch graphs
     cudaGraph_t g = nullptr;
     LBX_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    lbx_status st = plan(n, lat_in, rgb_out, s, true);
+    lbx_status st = plan(n, lat, rgb, s, true);
     cudaError_t ce = cudaStreamEndCapture(s, &g);
     if (st != LBX_OK) {
       if (g) cudaGraphDestroy(g);
@@ -677,53 +756,68 @@ lbx_status Decoder::graph_for(int n, const __half* lat_in, uint8_t* rgb_out, cud
     ce = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return set_err(LBX_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-    it = graphs.emplace(key, ex).first;
+    ++captures;
+    it = graphs.emplace(n, ex).first;
   }
   *out = it->second;
   return LBX_OK;
 }
 
+// Decode n latents: caller latents are copied into the graph's input buffer and the RGB out of its
+// output buffer (D2D; 0.1% of a 1024^2 decode) unless they already are those buffers.
 lbx_status Decoder::run(int n, const __half* lat_in, uint8_t* rgb_out, cudaStream_t s) {
   cudaGraphExec_t ex = nullptr;
-  lbx_status st = graph_for(n, lat_in, rgb_out, s, &ex);
+  lbx_status st = graph_for(n, s, &ex);
   if (st != LBX_OK) return st;
+  if (lat_in != lat) LBX_CUDA_TRY(cudaMemcpyAsync(lat, lat_in, lat_elems(n) * 2, cudaMemcpyDeviceToDevice, s));
   LBX_CUDA_TRY(cudaGraphLaunch(ex, s));
+  if (rgb_out != rgb) LBX_CUDA_TRY(cudaMemcpyAsync(rgb_out, rgb, rgb_bytes(n), cudaMemcpyDeviceToDevice, s));
   return LBX_OK;
 }
 
-lbx_status Decoder::stage_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, cudaStream_t s) {
-  size_t total = 0;
+lbx_status Decoder::validate_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, size_t* total) {
+  *total = 0;
+  if (!blobs || !nbytes) return set_err(LBX_E_CONFIG, "blobs: null pointer");
   for (uint32_t i = 0; i < n; ++i) {
     std::string why;
-    if (!blobs || !nbytes || !blobs[i]) return set_err(LBX_E_CONFIG, "blobs: null pointer");
+    if (!blobs[i]) return set_err(LBX_E_CONFIG, "blobs: null pointer");
     if (!lblp_validate(blobs[i], nbytes[i], cl, h, w, &why))
       return set_err(LBX_E_FORMAT, "blob " + std::to_string(i) + ": " + why);
-    total += (nbytes[i] + 15) & ~size_t(15);
+    *total += (nbytes[i] + 15) & ~size_t(15);
   }
-  if (total > blob_host_cap) {
-    // the previous H2D from the pinned buffer must be complete before it is replaced
-    LBX_CUDA_TRY(cudaStreamSynchronize(s));
-    if (blob_host) cudaFreeHost(blob_host);
-    if (blob_dev) cudaFree(blob_dev);
-    blob_host_cap = blob_dev_cap = (total + (total >> 2) + 4096 + 255) & ~size_t(255);  // offs_dev follows: keep 8B+ alignment
-    LBX_CUDA_TRY(cudaMallocHost(&blob_host, blob_host_cap));
-    LBX_CUDA_TRY(cudaMalloc(&blob_dev, blob_dev_cap + (size_t)max_batch * 16));
-    offs_dev = reinterpret_cast<unsigned long long*>(blob_dev + blob_dev_cap);
-    sizes_dev = reinterpret_cast<unsigned int*>(offs_dev + max_batch);
-  } else {
-    LBX_CUDA_TRY(cudaStreamSynchronize(s));  // pinned staging is reused
+  return LBX_OK;
+}
+
+// Validate, copy into pinned staging, one H2D, unpack into lat_out (status into err_dev), all on s.
+lbx_status Decoder::stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                                cudaStream_t s, __half* lat_out, int* err_dev) {
+  size_t total = 0;
+  lbx_status vs = validate_blobs(blobs, nbytes, n, &total);
+  if (vs != LBX_OK) return vs;
+  // the previous H2D out of the pinned buffer must be complete before it is rewritten or replaced
+  LBX_CUDA_TRY(cudaEventSynchronize(st.copied));
+  if (total > st.cap) {
+    if (st.host) cudaFreeHost(st.host);
+    if (st.dev) cudaFree(st.dev);
+    st.host = st.dev = nullptr;
+    st.cap = (total + (total >> 2) + 4096 + 255) & ~size_t(255);  // the table follows: keep 8B+ alignment
+    LBX_CUDA_TRY(cudaMallocHost(&st.host, st.cap));
+    LBX_CUDA_TRY(cudaMalloc(&st.dev, st.cap + (size_t)max_batch * 16));
+    st.offs_dev = reinterpret_cast<unsigned long long*>(st.dev + st.cap);
+    st.sizes_dev = reinterpret_cast<unsigned int*>(st.offs_dev + max_batch);
   }
   size_t off = 0;
-  unsigned int* sizes_host = reinterpret_cast<unsigned int*>(offs_host + max_batch);
+  unsigned int* sizes_host = reinterpret_cast<unsigned int*>(st.table_host + max_batch);
   for (uint32_t i = 0; i < n; ++i) {
-    std::memcpy(blob_host + off, blobs[i], nbytes[i]);
-    offs_host[i] = off;
+    std::memcpy(st.host + off, blobs[i], nbytes[i]);
+    st.table_host[i] = off;
     sizes_host[i] = (unsigned int)nbytes[i];
     off += (nbytes[i] + 15) & ~size_t(15);
   }
-  LBX_CUDA_TRY(cudaMemcpyAsync(blob_dev, blob_host, off, cudaMemcpyHostToDevice, s));
-  LBX_CUDA_TRY(cudaMemcpyAsync(offs_dev, offs_host, (size_t)max_batch * 12, cudaMemcpyHostToDevice, s));
-  launch_lblp_unpack(blob_dev, offs_dev, sizes_dev, (int)n, cl, h, w, lat, err, s);
+  LBX_CUDA_TRY(cudaMemcpyAsync(st.dev, st.host, off, cudaMemcpyHostToDevice, s));
+  LBX_CUDA_TRY(cudaMemcpyAsync(st.offs_dev, st.table_host, (size_t)max_batch * 12, cudaMemcpyHostToDevice, s));
+  LBX_CUDA_TRY(cudaEventRecord(st.copied, s));
+  launch_lblp_unpack(st.dev, st.offs_dev, st.sizes_dev, (int)n, cl, h, w, lat_out, err_dev, s);
   LBX_CUDA_TRY(cudaPeekAtLastError());
   return LBX_OK;
 }
@@ -784,13 +878,16 @@ lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max) {
   Decoder& d = dec->d;
   if (n_max == 0 || (int)n_max > d.max_batch) return set_err(LBX_E_CONFIG, "n_max: must be in [1, desc.max_batch]");
   cudaSetDevice(d.desc.device);
+  d.order(d.stream);
   for (uint32_t n = 1; n <= n_max; ++n) {
     cudaGraphExec_t ex = nullptr;
-    lbx_status st = d.graph_for((int)n, d.lat, d.rgb, d.stream, &ex);
+    lbx_status st = d.graph_for((int)n, d.stream, &ex);
     if (st != LBX_OK) return st;
   }
   return LBX_OK;
 }
+
+uint64_t lbx_graph_captures(lbx_decoder* dec) { return dec ? dec->d.captures : 0; }
 
 lbx_status lbx_decoder_destroy(lbx_decoder* dec) {
   if (!dec) return set_err(LBX_E_CONFIG, "lbx_decoder_destroy: null decoder");
@@ -807,11 +904,10 @@ lbx_status lbx_unpack(lbx_decoder* dec, const uint8_t* const* blobs, const size_
   if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
   cudaSetDevice(d.desc.device);
   cudaStream_t s = pick(dec, stream);
-  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
-  if (st != LBX_OK) return st;
-  if (cudaMemcpyAsync(latents_dev, d.lat, d.lat_elems(n) * 2, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-    return set_err(LBX_E_CUDA, "lbx_unpack: copy out failed");
-  return LBX_OK;
+  d.order(s);
+  lbx_status st = d.stage_blobs(d.sync_st, blobs, nbytes, n, s, reinterpret_cast<__half*>(latents_dev), d.err);
+  d.mark(s);
+  return st;
 }
 
 lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uint8_t* rgb_dev, lbx_stream stream) {
@@ -821,9 +917,14 @@ lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uin
   if (n == 0) return LBX_OK;
   if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
   cudaSetDevice(d.desc.device);
-  return d.run((int)n, reinterpret_cast<const __half*>(latents_dev), rgb_dev, pick(dec, stream));
+  cudaStream_t s = pick(dec, stream);
+  d.order(s);
+  lbx_status st = d.run((int)n, reinterpret_cast<const __half*>(latents_dev), rgb_dev, s);
+  d.mark(s);
+  return st;
 }
 
+// Decode d.lat (already staged on s), D2H the RGB, wait, check the device status word.
 static lbx_status finish_reconstruct(Decoder& d, uint32_t n, uint8_t* rgb_host, cudaStream_t s,
                                      uint8_t* const* rgb_hosts = nullptr) {
   lbx_status st = d.run((int)n, d.lat, d.rgb, s);
@@ -838,6 +939,7 @@ static lbx_status finish_reconstruct(Decoder& d, uint32_t n, uint8_t* rgb_host, 
   }
   if (cudaMemcpyAsync(d.err_host, d.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return set_err(LBX_E_CUDA, "D2H of status failed");
+  d.mark(s);
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("reconstruct: ") + cudaGetErrorString(e));
   if (*d.err_host) {
@@ -856,7 +958,8 @@ lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const 
   if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
   cudaSetDevice(d.desc.device);
   cudaStream_t s = pick(dec, stream);
-  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  d.order(s);
+  lbx_status st = d.stage_blobs(d.sync_st, blobs, nbytes, n, s, d.lat, d.err);
   if (st != LBX_OK) return st;
   return finish_reconstruct(d, n, rgb_host, s);
 }
@@ -872,9 +975,84 @@ lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, cons
   if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
   cudaSetDevice(d.desc.device);
   cudaStream_t s = pick(dec, stream);
-  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  d.order(s);
+  lbx_status st = d.stage_blobs(d.sync_st, blobs, nbytes, n, s, d.lat, d.err);
   if (st != LBX_OK) return st;
   return finish_reconstruct(d, n, nullptr, s, rgb_hosts);
+}
+
+// Asynchronous pipeline.  Slot k % 2 carries ticket k:
+//   in_stream : H2D blobs -> unpack into slot.lat                               -> [unpacked]
+//   stream    : wait unpacked; lat <- slot.lat; graph; wait drained(previous use of the slot);
+//               slot.rgb <- rgb                                                  -> [computed]
+//   out_stream: wait computed; D2H slot.rgb -> rgb_hosts[i]; status word         -> [drained]
+// so batch k+1's copy-in and batch k-1's copy-out overlap batch k's graph.
+lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                                  uint8_t* const* rgb_hosts, uint64_t* ticket) {
+  if (!dec || !rgb_hosts || !ticket) return set_err(LBX_E_CONFIG, "lbx_reconstruct_submit: null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (!rgb_hosts[i]) return set_err(LBX_E_CONFIG, "rgb_hosts: null entry");
+  *ticket = 0;
+  lbx_status st = LBX_OK;
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder& d = dec->d;
+  if (n == 0 || (int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: must be in [1, desc.max_batch]");
+  cudaSetDevice(d.desc.device);
+  Decoder::Slot& sl = d.slots[d.next_ticket & 1];
+  if (sl.busy)
+    return set_err(LBX_E_RUNTIME, "lbx_reconstruct_submit: two batches in flight; wait for ticket " +
+                                      std::to_string(sl.ticket) + " first");
+  if ((st = d.alloc_slot(sl)) != LBX_OK) return st;
+  cudaGraphExec_t ex = nullptr;
+  d.order(d.stream);
+  if ((st = d.graph_for((int)n, d.stream, &ex)) != LBX_OK) return st;  // captured once per n
+  // the slot's latents were last read by its previous batch's copy on `stream`
+  LBX_CUDA_TRY(cudaStreamWaitEvent(d.in_stream, sl.computed, 0));
+  if ((st = d.stage_blobs(sl.st, blobs, nbytes, n, d.in_stream, sl.lat, sl.err)) != LBX_OK) return st;
+  LBX_CUDA_TRY(cudaEventRecord(sl.unpacked, d.in_stream));
+  LBX_CUDA_TRY(cudaStreamWaitEvent(d.stream, sl.unpacked, 0));
+  LBX_CUDA_TRY(cudaMemcpyAsync(d.lat, sl.lat, d.lat_elems(n) * 2, cudaMemcpyDeviceToDevice, d.stream));
+  LBX_CUDA_TRY(cudaGraphLaunch(ex, d.stream));
+  LBX_CUDA_TRY(cudaStreamWaitEvent(d.stream, sl.drained, 0));
+  LBX_CUDA_TRY(cudaMemcpyAsync(sl.rgb, d.rgb, d.rgb_bytes(n), cudaMemcpyDeviceToDevice, d.stream));
+  LBX_CUDA_TRY(cudaEventRecord(sl.computed, d.stream));
+  d.mark(d.stream);
+  LBX_CUDA_TRY(cudaStreamWaitEvent(d.out_stream, sl.computed, 0));
+  const size_t per = d.rgb_bytes(1);
+  for (uint32_t i = 0; i < n; ++i)
+    LBX_CUDA_TRY(cudaMemcpyAsync(rgb_hosts[i], sl.rgb + i * per, per, cudaMemcpyDeviceToHost, d.out_stream));
+  LBX_CUDA_TRY(cudaMemcpyAsync(sl.err_host, sl.err, 4, cudaMemcpyDeviceToHost, d.out_stream));
+  LBX_CUDA_TRY(cudaEventRecord(sl.drained, d.out_stream));
+  sl.busy = true;
+  sl.ticket = d.next_ticket++;
+  *ticket = sl.ticket;
+  return LBX_OK;
+}
+
+lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket) {
+  if (!dec) return set_err(LBX_E_CONFIG, "lbx_reconstruct_wait: null decoder");
+  cudaEvent_t ev = nullptr;
+  int slot = -1;
+  {
+    std::lock_guard<std::mutex> g(dec->mu);
+    Decoder& d = dec->d;
+    for (int i = 0; i < 2; ++i)
+      if (d.slots[i].busy && d.slots[i].ticket == ticket) slot = i;
+    if (slot < 0) return set_err(LBX_E_CONFIG, "lbx_reconstruct_wait: unknown or already retired ticket");
+    ev = d.slots[slot].drained;
+  }
+  const cudaError_t e = cudaEventSynchronize(ev);  // outside the lock: the next batch may be submitted
+  std::lock_guard<std::mutex> g(dec->mu);
+  Decoder::Slot& sl = dec->d.slots[slot];
+  sl.busy = false;
+  if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("reconstruct: ") + cudaGetErrorString(e));
+  if (*sl.err_host) {
+    const int code = *sl.err_host;
+    *sl.err_host = 0;
+    cudaMemsetAsync(sl.err, 0, 4, dec->d.in_stream);
+    return set_err(LBX_E_FORMAT, "device unpack reported a malformed blob (code " + std::to_string(code) + ")");
+  }
+  return LBX_OK;
 }
 
 lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
@@ -895,7 +1073,8 @@ lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, co
         cudaMallocHost(&d.png_sizes_host, 4 * (size_t)d.max_batch) != cudaSuccess)
       return set_err(LBX_E_CUDA, "lbx_reconstruct_png: PNG buffers");
   }
-  lbx_status st = d.stage_blobs(blobs, nbytes, n, s);
+  d.order(s);
+  lbx_status st = d.stage_blobs(d.sync_st, blobs, nbytes, n, s, d.lat, d.err);
   if (st != LBX_OK) return st;
   if ((st = d.run((int)n, d.lat, d.rgb, s)) != LBX_OK) return st;
   cudaError_t e = lbx::launch_png_encode(d.rgb, (int)n, H, W, d.png_dev, 0, d.png_sizes, d.png_work, s, true);
@@ -903,6 +1082,7 @@ lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, co
   if (cudaMemcpyAsync(d.png_sizes_host, d.png_sizes, 4 * (size_t)n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaMemcpyAsync(d.err_host, d.err, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     return set_err(LBX_E_CUDA, "D2H of PNG sizes failed");
+  d.mark(s);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess)
     return set_err(LBX_E_CUDA, std::string("reconstruct_png: ") + cudaGetErrorString(e));
   if (*d.err_host) {
@@ -929,6 +1109,7 @@ lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, u
   if ((int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: exceeds desc.max_batch");
   cudaSetDevice(d.desc.device);
   cudaStream_t s = pick(dec, stream);
+  d.order(s);
   if (cudaMemcpyAsync(d.lat, latents_host, d.lat_elems(n) * 2, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return set_err(LBX_E_CUDA, "H2D of latents failed");
   return finish_reconstruct(d, n, rgb_host, s);
@@ -950,7 +1131,7 @@ lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, ui
 // ------------------------------------------------------------------ op-level entry points
 lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
                        const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
-                       const float* row_scale, float alpha, double* gn_stats, int cta_group, int bn,
+                       const float* row_scale, float alpha, uint64_t* gn_stats, int cta_group, int bn,
                        lbx_stream stream) {
   lbx::GemmArgs g;
   g.mode = mode;
@@ -962,7 +1143,7 @@ lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, in
   g.bias = bias;
   g.resid = reinterpret_cast<const __half*>(resid); g.ldr = ldr;
   g.row_scale = row_scale; g.alpha = alpha;
-  g.gn_stats = gn_stats; g.gn_cpg = N / 32; g.rows_per_img = (mode == 0) ? (b > 0 ? M / b : M) : h * w;
+  g.gn_stats = reinterpret_cast<unsigned long long*>(gn_stats); g.gn_cpg = N / 32; g.rows_per_img = (mode == 0) ? (b > 0 ? M / b : M) : h * w;
   cudaError_t e = lbx::gemm_tc_launch(g, reinterpret_cast<cudaStream_t>(stream), cta_group, bn);
   if (e != cudaSuccess) return set_err(e == cudaErrorInvalidValue ? LBX_E_CONFIG : LBX_E_CUDA,
                                        std::string("lbx_op_gemm: ") + cudaGetErrorString(e));
@@ -982,7 +1163,7 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream) {
   g.bias = d->bias;
   g.resid = reinterpret_cast<const __half*>(d->resid); g.ldr = d->ldr;
   g.row_scale = d->row_scale; g.alpha = d->alpha;
-  g.gn_stats = d->gn_stats; g.gn_cpg = d->N / 32;
+  g.gn_stats = reinterpret_cast<unsigned long long*>(d->gn_stats); g.gn_cpg = d->N / 32;
   g.gn_ss = reinterpret_cast<const float2*>(d->gn_ss);
   g.b_mn_major = d->b_mn_major;
   g.rows_per_img = (d->mode == 0) ? (d->b > 0 ? d->M / d->b : d->M) : d->h * d->w;
@@ -1135,12 +1316,12 @@ lbx_status lbx_subpixel_weights(const float* w3, int N, int C, uint16_t* out) {
   return LBX_OK;
 }
 
-lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const float* gamma, const float* beta, int b,
+lbx_status lbx_op_groupnorm(const void* x, void* y, const uint64_t* stats, const float* gamma, const float* beta, int b,
                             int hw, int c, int silu, float eps, lbx_stream stream) {
   if (!x || !y || !stats || !gamma || !beta || !(c == 128 || c == 256 || c == 512))
     return set_err(LBX_E_CONFIG, "lbx_op_groupnorm: bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const lbx::GnSrc gs{stats, gamma, beta, 1.0 / ((double)hw * (c / 32)), eps};
+  const lbx::GnSrc gs{reinterpret_cast<const unsigned long long*>(stats), gamma, beta, 1.0 / ((double)hw * (c / 32)), eps};
   lbx::launch_gn_apply(reinterpret_cast<const __half*>(x), reinterpret_cast<__half*>(y), gs, (long long)b * hw, hw, c,
                        silu != 0, silu == 2, s);
   cudaError_t e = cudaPeekAtLastError();
@@ -1148,12 +1329,12 @@ lbx_status lbx_op_groupnorm(const void* x, void* y, const double* stats, const f
   return LBX_OK;
 }
 
-lbx_status lbx_op_gn_stats(const void* x, double* stats, int b, int hw, int c, lbx_stream stream) {
+lbx_status lbx_op_gn_stats(const void* x, uint64_t* stats, int b, int hw, int c, lbx_stream stream) {
   if (!x || !stats || c % 32 || c > 512 || b <= 0 || hw <= 0) return set_err(LBX_E_CONFIG, "lbx_op_gn_stats: bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(stats, 0, (size_t)b * 64 * sizeof(double), s) != cudaSuccess)
+  if (cudaMemsetAsync(stats, 0, (size_t)b * 32 * lbx::kGnStatWords * 8, s) != cudaSuccess)
     return set_err(LBX_E_CUDA, "memset");
-  lbx::launch_gn_stats(reinterpret_cast<const __half*>(x), stats, b, hw, c, s);
+  lbx::launch_gn_stats(reinterpret_cast<const __half*>(x), reinterpret_cast<unsigned long long*>(stats), b, hw, c, s);
   cudaError_t e = cudaPeekAtLastError();
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, cudaGetErrorString(e));
   return LBX_OK;
@@ -1166,9 +1347,11 @@ lbx_status lbx_profile(lbx_decoder* dec, uint32_t n, lbx_prof_entry* out, int ca
   if (n == 0 || (int)n > d.max_batch) return set_err(LBX_E_CONFIG, "n: must be in [1, desc.max_batch]");
   cudaSetDevice(d.desc.device);
   std::vector<Decoder::ProfRec> recs;
+  d.order(d.stream);
   d.prof = &recs;
   lbx_status st = d.plan((int)n, d.lat, d.rgb, d.stream, false);
   d.prof = nullptr;
+  d.mark(d.stream);
   cudaError_t e = cudaStreamSynchronize(d.stream);
   int k = 0;
   for (size_t i = 1; i < recs.size(); ++i) {

@@ -13,7 +13,7 @@
 //   warps 2..9  epilogue, two warps per TMEM lane quarter: tcgen05.ld -> (scale) + bias (+ residual)
 //               in fp32 -> fp16, stored with STG.256 (convs) or staged in smem and TMA-stored (plain
 //               GEMMs); GroupNorm-32 partial sums of the fp32 values (per lane, reduced at image
-//               changes, fp64 atomics); at 128 output channels the residual of the tile that will
+//               changes, exact fixed-point integer atomics, gnfix.cuh); at 128 output channels the residual of the tile that will
 //               reuse the accumulator is preloaded into it (tcgen05.st) -- wider outputs add it here.
 //   warps 11..14  (XF kernels only) GroupNorm + SiLU transform of each landed A halo.
 // CG = 2 runs the tile on a CTA pair (cta_group::2): each CTA stages its 128 A rows and half of B
@@ -29,6 +29,7 @@
 
 #include "act.cuh"
 #include "gemm_tc.cuh"
+#include "gnfix.cuh"
 #include "ptx.cuh"
 
 namespace lbx {
@@ -47,7 +48,7 @@ struct KParams {
   int ldr;
   const float* row_scale;
   float alpha;
-  double* gn_stats;
+  unsigned long long* gn_stats;
   int gn_cpg;
   int rows_per_img;
   // operand staging (host-computed, see stage_plan())
@@ -505,8 +506,11 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     const int cbase = p.cmap ? hsel * NCH : hsel, cstep = p.cmap ? 1 : (EPI_WARPS / 4);
     // GroupNorm partials: each lane accumulates its own per-chunk (group sum, group sumsq) values in
     // fp32 registers across tiles (NCH x NV <= 32 of them); at a flush -- when the (image, n-tile)
-    // changes -- the warp reduce-scatters them (lane L owns value L) and adds them with one fp64
-    // atomic per value.
+    // changes -- the warp reduce-scatters them (lane L owns value L) and adds them as one exact
+    // fixed-point integer pair per value (gnfix.cuh).  Which tiles a lane sums in fp32 is fixed by
+    // the tile index within its image (residue class mod the cluster count, see gemm_tc_launch), so
+    // together with the order-independent integer totals an image's statistics do not depend on
+    // its position in the batch or on the batch size.
     float sacc[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
@@ -528,7 +532,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         const int kind = i >= gpc;
         const int c = cbase + cstep * j;
         const int grp = (g_ntile * BN + c * 32) / p.gn_cpg + (i - kind * gpc);
-        atomicAdd(p.gn_stats + ((size_t)g_img * 32 + grp) * 2 + kind, (double)tot);
+        gnfix_add(p.gn_stats + (((size_t)g_img * 32 + grp) * 2 + kind) * 2, tot);  // order-independent
       }
 #pragma unroll
       for (int i = 0; i < 32; ++i) sacc[i] = 0.f;
@@ -985,6 +989,16 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   auto kern = gemm_tc_kernel<BN, CG, XF>;
   const int sms = num_sms();
   int clusters = (g_gemm_max_sms > 0 && g_gemm_max_sms < sms ? g_gemm_max_sms : sms) / CG;
+  if (kp.gn_stats && !kp.sched) {
+    // GroupNorm statistics are summed per lane over the tiles of one image that a cluster visits:
+    // tile j of an image goes to cluster (img * T + j) mod G, so the tiles summed together are a
+    // residue class of j mod G -- the same for every image as long as G does not change with the
+    // batch.  G = the full grid when an image has >= that many tiles; otherwise a multiple of T
+    // (each cluster then sees at most one tile per image, exactly as a solo decode does).
+    const long long imgs = (long long)a.M / a.rows_per_img;
+    const int T = imgs > 0 ? (int)(kp.tiles / imgs) : kp.tiles;
+    if (T > 0 && T < clusters) clusters = T * (clusters / T);
+  }
   if (clusters > kp.tiles) clusters = kp.tiles;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CG);

@@ -47,7 +47,7 @@ struct GemmArgs {
   int ldr = 0;
   const float* row_scale = nullptr;
   float alpha = 1.f;
-  double* gn_stats = nullptr;     // [img][32][2] (sum, sumsq); zeroed by the caller
+  unsigned long long* gn_stats = nullptr;  // [img][32][2][2] fixed point (gnfix.cuh); zeroed by the caller
   int gn_cpg = 0;                 // channels per group = N / 32
   int rows_per_img = 0;           // M rows per image (GN image index = m / rows_per_img)
 };

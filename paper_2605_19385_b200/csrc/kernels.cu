@@ -5,6 +5,7 @@
 
 #include "act.cuh"
 #include "gemm_tc.cuh"
+#include "gnfix.cuh"
 #include "kernels.cuh"
 #include "ptx.cuh"
 
@@ -70,17 +71,18 @@ void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, in
 }
 
 // ----------------------------------------------------------------------------- GroupNorm
-__global__ void gn_finalize_kernel(const double* __restrict__ stats, const float* __restrict__ gamma,
+__global__ void gn_finalize_kernel(const unsigned long long* __restrict__ stats, const float* __restrict__ gamma,
                                    const float* __restrict__ beta, float2* __restrict__ ss, int n, int C,
                                    double inv_count, float eps) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n * C) return;
   const int img = i / C, c = i - img * C;
   const int g = c / (C / 32);
-  ss[i] = gn_affine(stats[(img * 32 + g) * 2], stats[(img * 32 + g) * 2 + 1], inv_count, gamma[c], beta[c], eps);
+  const unsigned long long* st = stats + ((size_t)img * 32 + g) * kGnStatWords;
+  ss[i] = gn_affine(gnfix_value(st), gnfix_value(st + 2), inv_count, gamma[c], beta[c], eps);
 }
 
-void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
+void launch_gn_finalize(const unsigned long long* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
                         double count, float eps, cudaStream_t s) {
   gn_finalize_kernel<<<(n * C + 255) / 256, 256, 0, s>>>(stats, gamma, beta, ss, n, C, 1.0 / count, eps);
 }
@@ -88,8 +90,9 @@ void launch_gn_finalize(const double* stats, const float* gamma, const float* be
 // The apply kernels finalize the statistics themselves (the same gn_affine arithmetic as
 // gn_finalize_kernel, so results are bit-identical): one launch per GroupNorm site instead of two.
 __device__ __forceinline__ float2 site_affine(const GnSrc& g, int img, int c, int cpg) {
-  const double* st = g.stats + ((size_t)img * 32 + c / cpg) * 2;
-  return gn_affine(__ldg(st), __ldg(st + 1), g.inv_count, __ldg(g.gamma + c), __ldg(g.beta + c), g.eps);
+  const unsigned long long* st = g.stats + ((size_t)img * 32 + c / cpg) * kGnStatWords;
+  const unsigned long long w[4] = {__ldg(st), __ldg(st + 1), __ldg(st + 2), __ldg(st + 3)};
+  return gn_affine(gnfix_value(w), gnfix_value(w + 2), g.inv_count, __ldg(g.gamma + c), __ldg(g.beta + c), g.eps);
 }
 
 // y = act(x * a_c + b_c).  The launch is exactly one resident wave; block b covers a contiguous
@@ -290,12 +293,14 @@ void launch_gn_apply(const __half* x, __half* y, const GnSrc& g, long long rows,
   }
 }
 
-__global__ void gn_stats_kernel(const __half* __restrict__ x, double* stats, int hw, int C) {
-  __shared__ float acc[64];
+// Deterministic: each thread sums a fixed pixel subset of one channel octet in fp32, the block
+// combines its threads in a fixed order through shared memory, and the block totals are added as
+// exact fixed-point integers (gnfix.cuh) -- bit-identical across runs and schedules.
+__global__ void __launch_bounds__(256) gn_stats_kernel(const __half* __restrict__ x, unsigned long long* stats,
+                                                       int hw, int C) {
+  __shared__ float part[256][17];
   const int img = blockIdx.y;
   const int cpg = C / 32;
-  if (threadIdx.x < 64) acc[threadIdx.x] = 0.f;
-  __syncthreads();
   const int cv = C / 8;
   const long long vecs = (long long)hw * cv;
   const uint4* xv = reinterpret_cast<const uint4*>(x + (size_t)img * hw * C);
@@ -303,32 +308,38 @@ __global__ void gn_stats_kernel(const __half* __restrict__ x, double* stats, int
 #pragma unroll
   for (int j = 0; j < 8; ++j) { s[j] = 0.f; s2[j] = 0.f; }
   // each thread keeps a fixed channel octet so its partial sums stay per channel
-  const int stride = gridDim.x * blockDim.x;
-  int first = blockIdx.x * blockDim.x + threadIdx.x;
-  if (stride % cv == 0) {
-    const int c0 = (first % cv) * 8;
-    for (long long v = first; v < vecs; v += stride) {
-      uint4 u = xv[v];
-      const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+  const int stride = gridDim.x * blockDim.x;  // a multiple of C/8 (see launch_gn_stats)
+  const int first = blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long v = first; v < vecs; v += stride) {
+    uint4 u = xv[v];
+    const __half2* h2 = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 f = __half22float2(h2[j]);
-        s[2 * j] += f.x; s2[2 * j] += f.x * f.x;
-        s[2 * j + 1] += f.y; s2[2 * j + 1] += f.y * f.y;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int g = (c0 + j) / cpg;
-      atomicAdd(&acc[2 * g], s[j]);
-      atomicAdd(&acc[2 * g + 1], s2[j]);
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __half22float2(h2[j]);
+      s[2 * j] += f.x; s2[2 * j] += f.x * f.x;
+      s[2 * j + 1] += f.y; s2[2 * j + 1] += f.y * f.y;
     }
   }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    part[threadIdx.x][j] = s[j];
+    part[threadIdx.x][8 + j] = s2[j];
+  }
   __syncthreads();
-  if (threadIdx.x < 64) atomicAdd(&stats[(size_t)img * 64 + threadIdx.x], (double)acc[threadIdx.x]);
+  if (threadIdx.x < 64) {  // value (group g, kind k): fixed-order sum over the block's threads
+    const int g = threadIdx.x >> 1, k = threadIdx.x & 1;
+    float acc = 0.f;
+    for (int t = 0; t < 256; ++t) {
+      const int c0 = ((blockIdx.x * blockDim.x + t) % cv) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if ((c0 + j) / cpg == g) acc += part[t][8 * k + j];
+    }
+    gnfix_add(stats + ((size_t)img * 32 + g) * kGnStatWords + 2 * k, acc);
+  }
 }
 
-void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaStream_t s) {
+void launch_gn_stats(const __half* x, unsigned long long* stats, int n, int hw, int C, cudaStream_t s) {
   // 256 threads x 64 blocks per image: stride 16384 vectors, a multiple of C/8 for C <= 512
   dim3 grid(64, n);
   gn_stats_kernel<<<grid, 256, 0, s>>>(x, stats, hw, C);

@@ -11,14 +11,15 @@ namespace lbx {
 void launch_latent_prep(const __half* lat, __half* out, int n, int cl, int h, int w, float scaling, float shift,
                         const float* pq_w, const float* pq_b, cudaStream_t s);
 
-// GroupNorm-32 finalize: stats [n][32][2] (sum, sumsq of `count` values per group) -> per-channel
-// affine ss[n][C] = (gamma*rstd, beta - mean*gamma*rstd).
-void launch_gn_finalize(const double* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
+// GroupNorm-32 finalize: stats [n][32][2][2] (sum, sumsq of `count` values per group, gnfix.cuh
+// fixed point) -> per-channel affine ss[n][C] = (gamma*rstd, beta - mean*gamma*rstd).
+void launch_gn_finalize(const unsigned long long* stats, const float* gamma, const float* beta, float2* ss, int n, int C,
                         double count, float eps, cudaStream_t s);
 
-// One GroupNorm site: fp64 statistics [n][32][2] over 1/inv_count values per group, affine, eps.
+// One GroupNorm site: fixed-point statistics [n][32][2][2] (gnfix.cuh) over 1/inv_count values per
+// group, affine, eps.
 struct GnSrc {
-  const double* stats;
+  const unsigned long long* stats;
   const float* gamma;
   const float* beta;
   double inv_count;
@@ -53,8 +54,9 @@ void kernels_set_apply_max_sms(int n);
 bool kernels_conv_out_legacy();
 
 // GroupNorm-32 statistics (sum, sumsq per image and group) of x [n][hw][C] fp16 into stats
-// [n][32][2] (accumulated; zero it first).  Standalone form of what the conv epilogue fuses.
-void launch_gn_stats(const __half* x, double* stats, int n, int hw, int C, cudaStream_t s);
+// [n][32][2][2] (gnfix.cuh fixed point, accumulated; zero it first).  Standalone form of what the
+// conv epilogue fuses.
+void launch_gn_stats(const __half* x, unsigned long long* stats, int n, int hw, int C, cudaStream_t s);
 
 // LBLP v1 device unpack (include/lbx/lblp.h).  `blobs` is one device buffer holding n blobs at
 // byte offsets `offs[i]` (device array); output fp16 NCHW [n][C][H][W].  Any malformed blob sets

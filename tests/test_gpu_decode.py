@@ -1,10 +1,11 @@
 """End-to-end parity of the reconstruction path (C ABI -> sm_100a kernels) against the CPU oracle
 (oracle/vae_ref.py, fp32) on the same seeded weights and latents.
 
-Bar (BASELINE.json north_star): uint8 pixels within +-1 LSB, PSNR >= 50 dB, stated per config.
-The decoder computes in fp16 with fp32 accumulation (FP16 engine), so a small
-fraction of pixels may sit 2 LSB away; the asserted bounds are written in each test and the
-measured statistics are printed (pytest -s) and recorded in DESIGN.md.
+Bar (BASELINE.json north_star), asserted by every decode test unless it says otherwise: every
+uint8 pixel within +-1 LSB of the oracle (max |diff| <= 1, 100% within 1 LSB) and PSNR >= 50 dB.
+The decoder computes in fp16 with fp32 accumulation (FP16 engine); the measured
+statistics are printed (pytest -s) and recorded in DESIGN.md.  The oracle itself is pinned to an
+independent implementation of the same decoder (tests/golden/pin_vllm_cheers.py).
 """
 import os
 
@@ -21,7 +22,7 @@ def _stats(got, ref):
     return vae_ref.pixel_stats(got, ref)
 
 
-def _check(st, name, min_psnr=50.0, min_le1=0.999, max_abs=4):
+def _check(st, name, min_psnr=50.0, min_le1=1.0, max_abs=1):
     print(f"\n[{name}] max|d|={st['max_abs']} exact={st['frac_exact']:.4f} "
           f"<=1LSB={st['frac_le1']:.6f} PSNR={st['psnr_db']:.2f} dB")
     assert st["psnr_db"] >= min_psnr, st
@@ -169,9 +170,8 @@ def test_config2_shape_sd15_1024_vs_oracle(lbx):
 
 def test_batch_invariance_full_size(lbx):
     """At the benchmarked size (32 x 4x128x128 -> 1024^2, attention in 8-image groups) image i of
-    the batch equals the same latent decoded alone.  GroupNorm statistics are summed with fp64
-    atomics whose order depends on the tiling, so the bar is: max |diff| <= 1 and > 99.99% of the
-    pixels identical (bit-identical in practice)."""
+    the batch is bit-identical to the same latent decoded alone: GroupNorm statistics are exact
+    fixed-point integer sums (csrc/gnfix.cuh), independent of the batch and the tile schedule."""
     import torch
     dev = torch.device("cuda")
     g = torch.Generator(device=dev).manual_seed(21)
@@ -185,7 +185,56 @@ def test_batch_invariance_full_size(lbx):
         zi = z[i:i + 1].contiguous()
         dec.decode_ptr(zi.data_ptr(), 1, one.data_ptr(), s)
         torch.cuda.synchronize()
-        d = (one[0].int() - rgb[i].int()).abs()
-        assert int(d.max()) <= 1, i
-        assert float((d == 0).float().mean()) > 0.9999, i
+        assert torch.equal(one[0], rgb[i]), i
     dec.close()
+
+
+def _batch_vs_oracle(lbx, fam, c, batch, seed, picks, name, q8=False):
+    """Decode a full benchmark batch on the GPU and compare images taken from INSIDE it with the
+    fp32 oracle on the same latents.  q8: the e2e path is fed LBLP q8 blobs (config 3); the oracle
+    decodes the latents the C oracle dequantizes from the same blobs."""
+    import lblp
+    import vae_ref
+    import weights_ref
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((batch, c, 128, 128), dtype=np.float32).astype(np.float16)
+    dec = lbx.Decoder(fam, (128, 128), seed=0, max_batch=batch)
+    if q8:
+        blobs = [lbx.pack(z[i], 2) for i in range(batch)]
+        got = dec.reconstruct(blobs)
+        zref = np.stack([lblp.decode(blobs[i], c, 128, 128) for i in picks])
+    else:
+        got = dec.reconstruct_latents(z)
+        zref = z[list(picks)]
+    dec.close()
+    W = weights_ref.make_weights(fam, 0)
+    for k, i in enumerate(picks):
+        ref = vae_ref.decode(zref[k:k + 1], W, fam)
+        _check(_stats(got[i:i + 1], ref), f"{name} image {i} of {batch}")
+
+
+def test_config2_batch32_images_vs_oracle(lbx):
+    """Config 2 as benchmarked (sd15 4x128x128 -> 1024^2, batch 32): images 0, 17, 31 of the batch."""
+    _batch_vs_oracle(lbx, "sd15", 4, 32, 1_000_003 * 2, (0, 17, 31), "config2")
+
+
+def test_config4_batch64_images_vs_oracle(lbx):
+    """Config 4 per-GPU batch (sd3 16x128x128 -> 1024^2, batch 64): images 0, 40, 63."""
+    _batch_vs_oracle(lbx, "sd3", 16, 64, 4, (0, 40, 63), "config4")
+
+
+def test_config3_q8_batch64_images_vs_oracle(lbx):
+    """Config 3 (packed q8 latents -> GPU unpack + decode, batch 64): images 5 and 62 against the
+    oracle decode of the C oracle's dequantization of the same blobs."""
+    _batch_vs_oracle(lbx, "sd3", 16, 64, 3, (5, 62), "config3 q8", q8=True)
+
+
+def test_product_vs_independent_decoder_fixture(lbx):
+    """The GPU decode against the committed output of the independent implementation the oracle is
+    pinned to (vllm CheersVAEDecoder, tests/golden/pin_vllm_cheers.py), config 1.  Chained bar: the
+    oracle sits within 1 LSB of it on 99.99% of pixels and the product within 1 LSB of the oracle,
+    so max |diff| <= 2 and >= 99.99% within 1 LSB, PSNR >= 50 dB."""
+    g = np.load(os.path.join(GOLD, "pin_cheers_sd15_64_seed1.npz"))
+    dec = lbx.Decoder("sd15", (64, 64), seed=int(g["weight_seed"]), max_batch=1)
+    got = dec.reconstruct_latents(g["latents"])
+    _check(_stats(got, g["rgb"]), "vs vllm CheersVAEDecoder sd15 512^2", min_le1=0.9999, max_abs=2)

@@ -90,7 +90,7 @@ def test_epilogue_store_variants(lbx, bits):
         for bb in (1, bits):
             lbx.check(lbx.lib().lbx_op_set_debug(bb, 0))
             out = torch.empty(b, h, w, c, dtype=torch.half, device="cuda")
-            stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+            stats = lbx.gn_stats_buffer(b)
             lbx.op_gemm(1, b * h * w, c, 9 * c, x.data_ptr(), 0, wk.data_ptr(), 9 * c, out.data_ptr(), c, b=b, h=h,
                         w=w, c=c, bias=bias.data_ptr(), resid=resid.data_ptr(), ldr=c, gn_stats=stats.data_ptr())
             A = _rand(512, 512, seed=74)
@@ -125,8 +125,10 @@ def _check_gn_stats(stats, out, b, hw, n):
     cnt = hw * (n // 32)
     mean_r = o.sum(dim=(1, 3)) / cnt
     var_r = (o * o).sum(dim=(1, 3)) / cnt - mean_r ** 2
-    mean = stats[..., 0] / cnt
-    var = stats[..., 1] / cnt - mean ** 2
+    import paper_2605_19385_b200 as lbxm
+    st = lbxm.gn_stats_values(stats)
+    mean = st[..., 0] / cnt
+    var = st[..., 1] / cnt - mean ** 2
     rms = (var_r + mean_r ** 2).sqrt()
     assert ((mean - mean_r).abs() <= 2e-4 * rms + 1e-6).all(), (mean - mean_r).abs().max()
     assert ((var - var_r).abs() <= 1e-3 * var_r + 1e-6).all(), ((var - var_r).abs() / var_r).max()
@@ -161,7 +163,7 @@ def test_conv3x3_resid_gnstats(lbx, cg):
     wk = wt.permute(0, 2, 3, 1).contiguous()
     resid = _rand(b, h, w, n, seed=11)
     out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
-    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    stats = lbx.gn_stats_buffer(b)
     lbx.op_gemm(1, b * h * w, n, 9 * c, x.data_ptr(), 0, wk.data_ptr(), 9 * c, out.data_ptr(), n, b=b, h=h, w=w,
                 c=c, resid=resid.data_ptr(), ldr=n, gn_stats=stats.data_ptr(), cta_group=cg)
     torch.cuda.synchronize()
@@ -195,7 +197,7 @@ def test_gn_stats_and_apply(lbx, c, silu, inplace):
     register-staged one); silu 0 identity, 1 fp32 SiLU, 2 packed-half SiLU (looser bound)."""
     b, hw = 3, 4096
     x = _rand(b, hw, c, seed=14) * 2 + 0.5
-    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    stats = lbx.gn_stats_buffer(b)
     lbx.op_gn_stats(x.data_ptr(), stats.data_ptr(), b, hw, c)
     gamma = torch.rand(c, device="cuda") + 0.5
     beta = torch.randn(c, device="cuda") * 0.1
@@ -225,7 +227,7 @@ def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
     wk = torch.cat([wt.permute(0, 2, 3, 1).reshape(n, 9 * c), wsc], dim=1).contiguous()
     bias = torch.randn(n, device="cuda")
     out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
-    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    stats = lbx.gn_stats_buffer(b)
     lbx.op_gemm(1, b * h * w, n, 9 * c, hin.data_ptr(), 0, wk.data_ptr(), 9 * c + cin, out.data_ptr(), n, b=b, h=h,
                 w=w, c=c, bias=bias.data_ptr(), gn_stats=stats.data_ptr(), cta_group=cg, a2=x.data_ptr(), lda2=cin,
                 k2=cin)
@@ -253,7 +255,7 @@ def test_conv3x3_fused_groupnorm_silu(lbx, cg, b, h, w, c, n, fold):
     wk = wk.contiguous()
     bias = torch.randn(n, device="cuda")
     out = torch.empty(b, h, w, n, dtype=torch.half, device="cuda")
-    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device="cuda")
+    stats = lbx.gn_stats_buffer(b)
     lbx.op_gemm(1, b * h * w, n, 9 * c, x.data_ptr(), 0, wk.data_ptr(), wk.shape[1], out.data_ptr(), n, b=b, h=h,
                 w=w, c=c, bias=bias.data_ptr(), gn_stats=stats.data_ptr(), cta_group=cg, gn_ss=ss.data_ptr(),
                 a2=xr.data_ptr() if fold else 0, lda2=n if fold else 0, k2=n if fold else 0)
