@@ -44,12 +44,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, choices=[2, 3, 4], default=2)
+    ap.add_argument("--config", type=int, choices=[0, 2, 3, 4], default=0,
+                    help="0 (default): config 2 at N=1, config 4 (batch 64 per GPU) at N>1")
     ap.add_argument("--batch", type=int, default=0, help="override batch per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-kernels", action="store_true", help="skip the codec / PNG kernel rates")
     ap.add_argument("--no-latency", action="store_true", help="skip the config-5 live replay (p50/p99)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the config-1/3/4 and batcher legs (N=1)")
     ap.add_argument("--profile-json", default="", help="write the per-launch profile here")
     return ap.parse_args()
 
@@ -200,16 +202,19 @@ def codec_rates(lbx, torch, dev, stream, hbm_peak):
             "bytes": "algorithmic: packed blob bytes + 2 B per latent value; peak = MEASURED_PEAKS hbm"}
 
 
-def c5_latency(device, scale=25):
+def c5_latency(device, scale=25, devices=1):
     """BASELINE's p50/p99 miss-decode latency: a 20 s wall-clock window of the config-5 trace's decode
-    jobs replayed through lbx_batcher on this GPU (tools/c5_replay live)."""
+    jobs replayed through lbx_batcher on `devices` GPUs (tools/c5_replay live)."""
     exe = os.path.join(ROOT, "tools", "c5_replay")
     if not os.path.exists(exe):
         return {"unavailable": "tools/c5_replay not built"}
     out = os.path.join("/tmp", f"lbx_c5_{os.getpid()}.json")
-    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(device)))
+    env = dict(os.environ)
+    if devices == 1:
+        env["CUDA_VISIBLE_DEVICES"] = os.environ.get("CUDA_VISIBLE_DEVICES", str(device))
     try:
-        subprocess.run([exe, "live", "--scale", str(scale), "--devices", "1", "--gpus", "1", "--json", out],
+        subprocess.run([exe, "live", "--scale", str(scale), "--devices", str(devices), "--gpus", str(devices),
+                        "--json", out],
                        stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=240, check=True, env=env)
         with open(out) as f:
             d = json.load(f)
@@ -217,7 +222,7 @@ def c5_latency(device, scale=25):
     except Exception as e:  # report, do not fail the bench line
         return {"unavailable": f"c5_replay: {type(e).__name__}"}
     live = d.get("live", {})
-    return {"workload": f"config 5 trace (Zipf x decay, 10 M requests), {scale}x replay, 20 s window, 1 GPU, "
+    return {"workload": f"config 5 trace (Zipf x decay, 10 M requests), {scale}x replay, 20 s window, {devices} GPU(s), "
                         f"sd3 16x128x128 -> 1024^2, batch rule '{d.get('policy')}'",
             "decode_p50_ms": live.get("decode_p50_ms"), "decode_p99_ms": live.get("decode_p99_ms"),
             "decodes_per_s": live.get("throughput_img_s"), "jobs": live.get("jobs"),
@@ -250,7 +255,7 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
         "config": {"workload": name, "family": fam, "latent": [c, 128, 128], "batch_per_step": 1,
                    "note": "reference has no decoder (SPEC.md:8); this is the oracle port, oracle/vae_ref.py"},
-        "cpu_baseline": {"value": v, "unit": "img/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "img/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{len(per)} x one 1024^2 image, torch fp32 on {threads} threads"},
         "e2e": {"value": v, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -258,26 +263,195 @@ def run_reference(args):
     return 0
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def timed_events(stream, fn, reps):
+    """Device time of `reps` calls of fn on `stream` (CUDA events, synchronize on both sides)."""
+    import torch
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def leg_config1(lbx, torch, dev, stream, steps):
+    """BASELINE configs[0]: one sd15 4x64x64 latent -> 512^2 RGB, batch 1.  Latency (device-resident
+    and end to end through lbx_reconstruct) and the images/s it implies."""
+    fam, c, h = "sd15", 4, 64
+    dec = lbx.Decoder(fam, (h, h), seed=0, device=dev.index, max_batch=1)
+    rng = np.random.default_rng(1)
+    z = rng.standard_normal((1, c, h, h), dtype=np.float32).astype(np.float16)
+    lat = torch.from_numpy(z.view(np.int16)).to(dev)
+    rgb = torch.empty((1, 8 * h, 8 * h, 3), dtype=torch.uint8, device=dev)
+    sp = stream.cuda_stream
+    blob = [lbx.pack(z[0], 1)]
+    out = torch.empty((1, 8 * h, 8 * h, 3), dtype=torch.uint8, pin_memory=True).numpy()
+    for _ in range(5):
+        dec.decode_ptr(lat.data_ptr(), 1, rgb.data_ptr(), sp)
+        dec.reconstruct(blob, out, stream=sp)
+    k = max(20, steps * 5)
+    clk = ClockSampler(dev.index)
+    clk.start()
+    ms = timed_events(stream, lambda: dec.decode_ptr(lat.data_ptr(), 1, rgb.data_ptr(), sp), k) / k
+    # end to end: host blob -> H2D -> unpack -> decode -> D2H, each call synchronous (a real miss)
+    per = []
+    for _ in range(k):
+        t = time.perf_counter()
+        dec.reconstruct(blob, out, stream=sp)
+        per.append((time.perf_counter() - t) * 1e3)
+    clocks = clk.stop()
+    dec.close()
+    per.sort()
+    return {"workload": "config1: sd15 4x64x64 -> 512x512 uint8 RGB, batch 1", "steps": k,
+            "device_ms_per_img": round(ms, 3), "device_img_s": round(1e3 / ms, 1),
+            "e2e_p50_ms": round(per[len(per) // 2], 3), "e2e_p99_ms": round(per[min(len(per) - 1, int(0.99 * len(per)))], 3),
+            "e2e_img_s": round(1e3 / statistics.mean(per), 1),
+            "e2e_path": "lbx_reconstruct (host LBLP blob -> RGB in pinned host memory), wall clock per call",
+            "clocks": clocks}
+
+
+def leg_config34(lbx, torch, dev, stream, steps, root):
+    """BASELINE configs[3] (sd3 16x128x128 -> 1024^2, batch 64 per GPU: device-resident and end to
+    end with lossless blobs) and configs[2] (the same batch stored as quantized LBLP q8 blobs: GPU
+    unpack + dequantize + decode, end to end).  Returns (config4, config3, q8 blobs, decoder)."""
+    fam, c, batch = "sd3", 16, 64
+    dec = lbx.Decoder(fam, (128, 128), seed=0, device=dev.index, max_batch=batch)
+    rng = np.random.default_rng(4)
+    z = rng.standard_normal((batch, c, 128, 128), dtype=np.float32).astype(np.float16)
+    lat = torch.from_numpy(z.view(np.int16)).to(dev)
+    rgb = torch.empty((batch, 1024, 1024, 3), dtype=torch.uint8, device=dev)
+    sp = stream.cuda_stream
+    k = max(2, min(steps, 5))
+    for _ in range(2):
+        dec.decode_ptr(lat.data_ptr(), batch, rgb.data_ptr(), sp)
+    clk = ClockSampler(dev.index)
+    clk.start()
+    ms = timed_events(stream, lambda: dec.decode_ptr(lat.data_ptr(), batch, rgb.data_ptr(), sp), k) / k
+    out = torch.empty((batch, 1024, 1024, 3), dtype=torch.uint8, pin_memory=True).numpy()
+    res = {}
+    for mode, name in ((1, "config4"), (2, "config3")):
+        blobs = [lbx.pack(z[i], mode) for i in range(batch)]
+        dec.reconstruct(blobs, out, stream=sp)
+        e2e_ms = timed_events(stream, lambda: dec.reconstruct(blobs, out, stream=sp), k) / k
+        res[name] = {"e2e_img_s": round(batch * 1e3 / e2e_ms, 2), "e2e_ms_per_step": round(e2e_ms, 2),
+                     "h2d_bytes_per_step": int(sum(len(b) for b in blobs)), "d2h_bytes_per_step": int(out.nbytes),
+                     "blobs": blobs}
+    clocks = clk.stop()
+    c4 = {"workload": "config4: sd3 16x128x128 -> 1024^2, batch 64 per GPU", "steps": k,
+          "device_img_s": round(batch * 1e3 / ms, 2), "device_ms_per_step": round(ms, 2),
+          "e2e_img_s": res["config4"]["e2e_img_s"], "e2e_path": "lbx_reconstruct, LBLP mode-1 (lossless) blobs",
+          "h2d_bytes_per_step": res["config4"]["h2d_bytes_per_step"],
+          "d2h_bytes_per_step": res["config4"]["d2h_bytes_per_step"], "clocks": clocks}
+    q8 = res["config3"].pop("blobs")
+    c3 = dict(res["config3"], workload="config3: the config-4 batch stored as LBLP q8 (quantized) blobs -> H2D -> "
+              "GPU unpack + dequantize -> decode -> RGB D2H, batch 64", steps=k,
+              packed_bytes_per_latent=round(statistics.mean(len(b) for b in q8)), clocks=clocks)
+    return c4, c3, q8, dec
+
+
+def leg_batcher_service(lbx, torch, dev, stream, seconds=4.0):
+    """North-star item 3 at batch 1: the service rate of one GPU through the pipelined batcher
+    (host blobs in, RGB in pinned host memory out, requests kept queued) against the device-only
+    decode loop, both sustained for `seconds` back to back (same power-capped conditions)."""
+    fam, c = "sd3", 16
+    rng = np.random.default_rng(9)
+    z = rng.standard_normal((8, c, 128, 128), dtype=np.float32).astype(np.float16)
+    blobs = [lbx.pack(z[i], 1) for i in range(8)]
+    dec = lbx.Decoder(fam, (128, 128), seed=0, device=dev.index, max_batch=1)
+    lat = torch.from_numpy(z[:1].view(np.int16)).to(dev)
+    rgb = torch.empty((1, 1024, 1024, 3), dtype=torch.uint8, device=dev)
+    sp = stream.cuda_stream
+    for _ in range(3):
+        dec.decode_ptr(lat.data_ptr(), 1, rgb.data_ptr(), sp)
+    torch.cuda.synchronize()
+    n_dev, t0 = 0, time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(10):
+            dec.decode_ptr(lat.data_ptr(), 1, rgb.data_ptr(), sp)
+        n_dev += 10
+        stream.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms = e0.elapsed_time(e1) / n_dev
+    dec.close()
+    b = lbx.Batcher([dev.index], [(fam, 128, 128)], max_batch=4, max_wait_us=0, policy="cost")
+    outs = [torch.empty((1024, 1024, 3), dtype=torch.uint8, pin_memory=True).numpy() for _ in range(8)]
+    free, rid, done = list(range(8)), 0, 0
+    owner = {}
+    t0 = time.perf_counter()
+    t_first = None
+    while time.perf_counter() - t0 < seconds:
+        while free:
+            i = free.pop()
+            owner[rid] = i
+            b.submit(rid, 0, blobs[rid % 8], outs[i])
+            rid += 1
+        for cpl in b.poll(wait_us=20000):
+            free.append(owner.pop(cpl["id"]))
+            done += 1
+            if t_first is None:
+                t_first, n0 = time.perf_counter(), done
+    t_last = time.perf_counter()
+    while b.pending():
+        b.poll(wait_us=20000)
+    b.close()
+    bat_ms = (t_last - t_first) * 1e3 / max(1, done - n0)
+    return {"workload": "sd3 16x128x128 -> 1024^2, batch 1, 8 requests kept queued, 1 worker, policy cost",
+            "device_only_ms_per_img": round(dev_ms, 3), "batcher_ms_per_img": round(bat_ms, 3),
+            "batcher_overhead": round(bat_ms / dev_ms - 1.0, 4), "seconds_each": seconds,
+            "note": "batcher = host blob validate/stage + H2D + unpack + graph + D2H, two batches in flight"}
+
+
 def main():
     args = parse()
+    import torch
+    from paper_2605_19385_b200.dist import launch_plan, spawn_argv
+
+    try:
+        plan = launch_plan(args.gpus, dict(os.environ), torch.cuda.device_count() if args.impl == "ours" else args.gpus)
+    except ValueError as e:
+        print(f"bench.py: {e}", file=sys.stderr, flush=True)
+        return 2
+    if plan == "spawn":  # one rank per GPU through torch.distributed.run; rank 0 prints the line
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        return subprocess.call(spawn_argv(sys.executable, os.path.abspath(__file__), sys.argv[1:], args.gpus, port))
     if args.impl == "reference":
         return run_reference(args)
 
-    import torch
     import torch.distributed as dist
     import paper_2605_19385_b200 as lbx
-    from paper_2605_19385_b200.dist import reduce_max, shard_range
+    from paper_2605_19385_b200.dist import gather_floats, reduce_max, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.config == 0:
+        args.config = 2 if world == 1 else 4  # N > 1: BASELINE configs[3], sharded whole requests
     fam, c, batch, name = workload(args)
 
     def barrier():
@@ -285,10 +459,9 @@ def main():
             dist.barrier()
 
     dec = lbx.Decoder(fam, (128, 128), seed=0, device=local, max_batch=batch)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     # this rank's shard of the global request stream (whole requests; weak scaling)
     first, last = shard_range(world * batch, rank, world)
-    rng = np.random.default_rng(1_000_003 * 2 + first)
+    rng = np.random.default_rng(1_000_003 * args.config + first)
     lat_np = rng.standard_normal((last - first, c, 128, 128), dtype=np.float32).astype(np.float16)
     lat = torch.from_numpy(lat_np.view(np.int16)).to(dev)
     rgb = torch.empty((batch, 1024, 1024, 3), dtype=torch.uint8, device=dev)
@@ -318,6 +491,7 @@ def main():
     ms = e0.elapsed_time(e1)
     if clocks.get("power_w"):  # energy per image at the median board power of the timed region
         clocks["joules_per_img"] = round(clocks["power_w"] * (ms / 1e3) / (batch * args.steps), 3)
+    per_rank = [batch * args.steps / (m / 1e3) for m in gather_floats(ms, dev)]
     ms_max = reduce_max(ms, dev)
     value = world * batch * args.steps / (ms_max / 1e3)
     launches = dec.launch_count(batch)
@@ -386,33 +560,74 @@ def main():
         with open(tp) as f:
             roof["traffic"] = json.load(f).get(dom_name)
     flop_img = FLOP_PER_IMG_1024[fam]
+    exec_img = sum(g["flops"] for g in groups.values()) / batch  # what the tensor cores actually execute
     ach = value / world * flop_img / 1e12
+    ach_x = value / world * exec_img / 1e12
     step_roof = {"algo_tflop_per_img": flop_img / 1e12, "achieved_tflops": ach, "frac_of_peak": ach / peak,
                  "frac_of_sustained_peak": ach / peak_sus, "tensor_kernel_share": tensor_ms / total_ms,
-                 "note": "whole decode (all kernels incl. GroupNorm/softmax/u8), per GPU, vs measured cuBLAS bf16"}
+                 "executed_tflop_per_img": exec_img / 1e12, "executed_tflops": ach_x,
+                 "executed_frac_of_peak": ach_x / peak, "executed_frac_of_sustained_peak": ach_x / peak_sus,
+                 "note": "whole decode (all kernels incl. GroupNorm/softmax/u8), per GPU, vs measured cuBLAS bf16; "
+                         "algorithmic = standard FLOPs (nearest-2x + full 3x3 conv), executed = what the tensor "
+                         "cores run (the sub-pixel upsample executes 4/9 of its standard FLOPs)"}
     if args.profile_json and rank == 0:
         with open(args.profile_json, "w") as f:
             json.dump({"groups": groups, "launches": prof}, f, indent=1)
+    dec.close()
+    del lat, rgb
+    torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- the other BASELINE configs (rank 0, N=1)
+    configs, q8_check, cpu = None, None, None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = {}
+        c4, c3, q8, dec34 = leg_config34(lbx, torch, dev, stream, args.steps, ROOT)
+        configs["config4"], configs["config3"] = c4, c3
+        # bit-exact unpack of the config-3 q8 blobs: GPU unpack vs the CPU oracle's decode of the
+        # same bytes (the CPU-baseline leg of K1; oracle = checker, never the thing measured)
+        glat = torch.empty((len(q8), 16, 128, 128), dtype=torch.int16, device=dev)
+        dec34.unpack_ptr(q8, glat.data_ptr(), sp)
+        torch.cuda.synchronize(dev)
+        dec34.close()
+        del dec34
+        torch.cuda.empty_cache()
+        g_np = glat.cpu().numpy().view(np.uint16)
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import lblp
+        t = time.perf_counter()
+        ref = np.stack([lblp.decode(b, 16, 128, 128).view(np.uint16) for b in q8])
+        cpu_unpack_s = time.perf_counter() - t
+        configs["config3"]["unpack_bit_exact"] = bool(np.array_equal(g_np, ref))
+        configs["config3"]["cpu_unpack_baseline"] = {"latents_per_s": round(len(q8) / cpu_unpack_s, 1), "cores": 1,
+                                                     "kind": "port", "sample": f"{len(q8)} q8 blobs, oracle/lblp_ref.c"}
+        configs["config1"] = leg_config1(lbx, torch, dev, stream, args.steps)
+        torch.cuda.empty_cache()
+    batcher = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        batcher = leg_batcher_service(lbx, torch, dev, stream)
+        torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
-    cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sec = cpu_decode_sample(fam, c, threads)
-        cpu = {"value": 1.0 / sec, "unit": "img/s", "cores": threads, "kind": "port",
+        cpu = {"value": 1.0 / sec, "unit": "img/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"one 1024^2 image ({fam}), oracle/vae_ref.py torch fp32 on {threads} threads"}
 
     # ---------------------------------------------------------------- codec / return-path kernels (rank 0, N=1)
     kernels = None
     if rank == 0 and world == 1 and not args.no_kernels:
         kernels = codec_rates(lbx, torch, dev, stream, hbm)
-
-    # ---------------------------------------------------------------- miss-decode latency (rank 0, N=1)
-    latency = None
-    if rank == 0 and world == 1 and not args.no_latency:
-        dec.close()  # the replay builds its own decoder (batcher)
         torch.cuda.empty_cache()
-        latency = c5_latency(local)
+
+    # ---------------------------------------------------------------- miss-decode latency (config 5)
+    # N = 1: one GPU at 25x.  N > 1: every rank has released its decoder; rank 0 replays the trace
+    # through one batcher driving all N GPUs of the box at 25x per GPU.
+    latency = None
+    barrier()
+    if rank == 0 and not args.no_latency:
+        latency = c5_latency(local, scale=25 * world, devices=world)
+    barrier()
 
     if rank == 0:
         line = {
@@ -424,8 +639,10 @@ def main():
                        "global_batch": batch * world, "output": "1024x1024x3 uint8",
                        "l2": "no flush: per-step working set ~40 GB of activations >> 126 MB L2",
                        "parallelism": f"dp{world} (whole-request sharding, no collective)"},
+            "per_rank_img_s": [round(v, 2) for v in per_rank],
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,
+            "configs": configs, "batcher_service": batcher,
             "kernels": kernels,
             "latency": latency,
         }

@@ -51,6 +51,7 @@ typedef struct {
   int device;                  /* CUDA ordinal that decoded it */
   uint32_t batch_size;         /* requests in that batch */
   uint64_t t_submit_us, t_start_us, t_end_us; /* steady-clock microseconds */
+  int worker;                  /* index into desc.devices of the worker that decoded it */
 } lbx_completion;
 
 typedef struct lbx_batcher lbx_batcher;

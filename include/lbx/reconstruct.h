@@ -112,6 +112,24 @@ lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket);
 /* CUDA graphs this decoder has captured (one per batch size; caller buffers never cause one). */
 uint64_t lbx_graph_captures(lbx_decoder* dec);
 
+/* Same pipeline for blobs resident in GPU memory (an HBM latent tier): blob i is nbytes[i] bytes at
+ * device pointer blobs_dev[i] on CUDA device blob_devices[i] (-1: host memory, handled as in
+ * lbx_reconstruct_submit, so one batch may mix both).  A blob on this decoder's device is
+ * copied D2D; a blob on another GPU is fetched with a peer copy over NVLink -- the latent shipping
+ * of a spilled decode, which the reference models as LatencyModel::intra_cluster_ms = 5
+ * (proj/include/latentbox/sim.hpp:20, proj/src/sim.cpp:369-373, proj/src/router.cpp:99-114).  Blob
+ * headers are validated by the device unpack (LBX_E_FORMAT at the wait). */
+lbx_status lbx_reconstruct_submit_dev(lbx_decoder* dec, const uint8_t* const* blobs_dev, const int* blob_devices,
+                                      const size_t* nbytes, uint32_t n, uint8_t* const* rgb_hosts, uint64_t* ticket);
+
+typedef struct {
+  uint64_t graph_captures; /* CUDA graphs captured (one per batch size) */
+  uint64_t peer_copies;    /* blobs fetched from another GPU (lbx_reconstruct_submit_dev) */
+  uint64_t peer_bytes;     /* their bytes */
+  double peer_ms;          /* device time of the batches' peer-copy phases, summed (CUDA events) */
+} lbx_decoder_counters;
+lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out);
+
 /* Same path from fp16 NCHW latents in HOST memory (no codec): H2D -> decode -> D2H.  Synchronous. */
 lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
                                    lbx_stream stream);

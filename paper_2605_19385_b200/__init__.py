@@ -412,7 +412,7 @@ class BatcherDesc(ctypes.Structure):
 class Completion(ctypes.Structure):
     _fields_ = [("request_id", ctypes.c_uint64), ("status", ctypes.c_int), ("device", ctypes.c_int),
                 ("batch_size", ctypes.c_uint32), ("t_submit_us", ctypes.c_uint64), ("t_start_us", ctypes.c_uint64),
-                ("t_end_us", ctypes.c_uint64)]
+                ("t_end_us", ctypes.c_uint64), ("worker", ctypes.c_int)]
 
 
 def _batcher_lib():
@@ -473,7 +473,8 @@ class Batcher:
             c = arr[i]
             self._keep.pop(c.request_id, None)
             res.append({"id": c.request_id, "status": c.status, "device": c.device, "batch": c.batch_size,
-                        "t_submit": c.t_submit_us, "t_start": c.t_start_us, "t_end": c.t_end_us})
+                        "t_submit": c.t_submit_us, "t_start": c.t_start_us, "t_end": c.t_end_us,
+                        "worker": c.worker})
         return res
 
     def pending(self) -> int:

@@ -189,7 +189,7 @@ void lbx_batcher::worker(int di) {
     {
       std::lock_guard<std::mutex> g(mu);
       for (auto& r : reqs)
-        done.push_back(lbx_completion{r.id, (int)rs, device, (uint32_t)reqs.size(), r.t_submit, t_start, t_end});
+        done.push_back(lbx_completion{r.id, (int)rs, device, (uint32_t)reqs.size(), r.t_submit, t_start, t_end, di});
     }
     cv_done.notify_all();
   };

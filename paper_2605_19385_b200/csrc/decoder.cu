@@ -124,7 +124,8 @@ class Decoder {
     int* err = nullptr;
     int* err_host = nullptr;  // pinned
     cudaEvent_t unpacked = nullptr, computed = nullptr, drained = nullptr;
-    bool busy = false;
+    cudaEvent_t peer0 = nullptr, peer1 = nullptr;  // timing: around this batch's peer copies
+    bool busy = false, timed_peer = false;
     uint64_t ticket = 0;
   };
   Slot slots[2];
@@ -136,6 +137,10 @@ class Decoder {
   cudaStream_t last_stream = nullptr;
   bool last_valid = false;
   uint64_t captures = 0;  // CUDA graphs captured so far (one per batch size n)
+  // HBM-resident blobs fetched from another GPU (latent spillover over NVLink): counters, and a
+  // timing event pair per slot around its peer copies
+  uint64_t peer_copies = 0, peer_bytes = 0;
+  double peer_ms = 0.0;
 
   // return path (lbx_reconstruct_png), allocated on first use
   uint8_t* png_dev = nullptr;    // max_batch PNGs back to back
@@ -170,7 +175,7 @@ class Decoder {
       free_staging(sl.st);
       if (sl.lat) cudaFree(sl.lat);
       if (sl.err_host) cudaFreeHost(sl.err_host);
-      for (cudaEvent_t e : {sl.unpacked, sl.computed, sl.drained})
+      for (cudaEvent_t e : {sl.unpacked, sl.computed, sl.drained, sl.peer0, sl.peer1})
         if (e) cudaEventDestroy(e);
       sl = Slot{};
     }
@@ -204,7 +209,8 @@ class Decoder {
   lbx_status graph_for(int n, cudaStream_t s, cudaGraphExec_t* out);
   lbx_status validate_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, size_t* total);
   lbx_status stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
-                         cudaStream_t s, __half* lat_out, int* err_dev);
+                         cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs = nullptr);
+  lbx_status grow_staging(Staging& st, size_t total);
   lbx_status alloc_slot(Slot& sl);
   static void free_staging(Staging& st) {
     if (st.host) cudaFreeHost(st.host);
@@ -449,6 +455,8 @@ lbx_status Decoder::alloc_slot(Slot& sl) {
   LBX_CUDA_TRY(cudaMallocHost(&sl.st.table_host, (size_t)max_batch * 16));
   for (cudaEvent_t* e : {&sl.st.copied, &sl.unpacked, &sl.computed, &sl.drained})
     LBX_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  LBX_CUDA_TRY(cudaEventCreate(&sl.peer0));
+  LBX_CUDA_TRY(cudaEventCreate(&sl.peer1));
   if (!in_stream) {
     LBX_CUDA_TRY(cudaStreamCreateWithFlags(&in_stream, cudaStreamNonBlocking));
     LBX_CUDA_TRY(cudaStreamCreateWithFlags(&out_stream, cudaStreamNonBlocking));
@@ -788,33 +796,72 @@ lbx_status Decoder::validate_blobs(const uint8_t* const* blobs, const size_t* nb
   return LBX_OK;
 }
 
-// Validate, copy into pinned staging, one H2D, unpack into lat_out (status into err_dev), all on s.
+lbx_status Decoder::grow_staging(Staging& st, size_t total) {
+  if (total <= st.cap) return LBX_OK;
+  if (st.host) cudaFreeHost(st.host);
+  if (st.dev) cudaFree(st.dev);
+  st.host = st.dev = nullptr;
+  st.cap = (total + (total >> 2) + 4096 + 255) & ~size_t(255);  // the table follows: keep 8B+ alignment
+  LBX_CUDA_TRY(cudaMallocHost(&st.host, st.cap));
+  LBX_CUDA_TRY(cudaMalloc(&st.dev, st.cap + (size_t)max_batch * 16));
+  st.offs_dev = reinterpret_cast<unsigned long long*>(st.dev + st.cap);
+  st.sizes_dev = reinterpret_cast<unsigned int*>(st.offs_dev + max_batch);
+  return LBX_OK;
+}
+
+// Gather n blobs into device staging and unpack them into lat_out (status into err_dev), all on s.
+// Host blobs (blob_devs == NULL): headers validated here, copied into pinned staging, one H2D.
+// Device blobs (blob_devs[i] = the GPU holding blob i, an HBM-resident latent tier): a D2D copy,
+// or a peer copy over NVLink when the blob lives on another GPU (the reference ships such a latent
+// to the executing node at LatencyModel::intra_cluster_ms, proj/include/latentbox/sim.hpp:20,
+// proj/src/sim.cpp:369-373); their headers are validated by the device unpack (err_dev).
 lbx_status Decoder::stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
-                                cudaStream_t s, __half* lat_out, int* err_dev) {
+                                cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs) {
   size_t total = 0;
-  lbx_status vs = validate_blobs(blobs, nbytes, n, &total);
-  if (vs != LBX_OK) return vs;
+  if (!blob_devs) {
+    lbx_status vs = validate_blobs(blobs, nbytes, n, &total);
+    if (vs != LBX_OK) return vs;
+  } else {  // per blob: host (blob_devs[i] < 0, validated here) or device memory
+    if (!blobs || !nbytes) return set_err(LBX_E_CONFIG, "blobs: null pointer");
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!blobs[i] || nbytes[i] == 0 || nbytes[i] > 0xFFFFFFFFull)
+        return set_err(LBX_E_CONFIG, "blob " + std::to_string(i) + ": null or bad size");
+      std::string why;
+      if (blob_devs[i] < 0 && !lblp_validate(blobs[i], nbytes[i], cl, h, w, &why))
+        return set_err(LBX_E_FORMAT, "blob " + std::to_string(i) + ": " + why);
+      total += (nbytes[i] + 15) & ~size_t(15);
+    }
+  }
   // the previous H2D out of the pinned buffer must be complete before it is rewritten or replaced
   LBX_CUDA_TRY(cudaEventSynchronize(st.copied));
-  if (total > st.cap) {
-    if (st.host) cudaFreeHost(st.host);
-    if (st.dev) cudaFree(st.dev);
-    st.host = st.dev = nullptr;
-    st.cap = (total + (total >> 2) + 4096 + 255) & ~size_t(255);  // the table follows: keep 8B+ alignment
-    LBX_CUDA_TRY(cudaMallocHost(&st.host, st.cap));
-    LBX_CUDA_TRY(cudaMalloc(&st.dev, st.cap + (size_t)max_batch * 16));
-    st.offs_dev = reinterpret_cast<unsigned long long*>(st.dev + st.cap);
-    st.sizes_dev = reinterpret_cast<unsigned int*>(st.offs_dev + max_batch);
-  }
+  lbx_status gs = grow_staging(st, total);
+  if (gs != LBX_OK) return gs;
   size_t off = 0;
   unsigned int* sizes_host = reinterpret_cast<unsigned int*>(st.table_host + max_batch);
   for (uint32_t i = 0; i < n; ++i) {
-    std::memcpy(st.host + off, blobs[i], nbytes[i]);
+    if (!blob_devs || blob_devs[i] < 0) std::memcpy(st.host + off, blobs[i], nbytes[i]);
     st.table_host[i] = off;
     sizes_host[i] = (unsigned int)nbytes[i];
     off += (nbytes[i] + 15) & ~size_t(15);
   }
-  LBX_CUDA_TRY(cudaMemcpyAsync(st.dev, st.host, off, cudaMemcpyHostToDevice, s));
+  bool any_host = !blob_devs;
+  for (uint32_t i = 0; blob_devs && i < n; ++i) any_host |= blob_devs[i] < 0;
+  // host blobs: one H2D of the whole staging region (device blobs' slots are overwritten below,
+  // in stream order)
+  if (any_host) LBX_CUDA_TRY(cudaMemcpyAsync(st.dev, st.host, off, cudaMemcpyHostToDevice, s));
+  if (blob_devs) {
+    for (uint32_t i = 0; i < n; ++i) {
+      uint8_t* dst = st.dev + st.table_host[i];
+      if (blob_devs[i] < 0) continue;
+      if (blob_devs[i] == desc.device) {
+        LBX_CUDA_TRY(cudaMemcpyAsync(dst, blobs[i], nbytes[i], cudaMemcpyDeviceToDevice, s));
+      } else {
+        LBX_CUDA_TRY(cudaMemcpyPeerAsync(dst, desc.device, blobs[i], blob_devs[i], nbytes[i], s));
+        ++peer_copies;
+        peer_bytes += nbytes[i];
+      }
+    }
+  }
   LBX_CUDA_TRY(cudaMemcpyAsync(st.offs_dev, st.table_host, (size_t)max_batch * 12, cudaMemcpyHostToDevice, s));
   LBX_CUDA_TRY(cudaEventRecord(st.copied, s));
   launch_lblp_unpack(st.dev, st.offs_dev, st.sizes_dev, (int)n, cl, h, w, lat_out, err_dev, s);
@@ -987,8 +1034,8 @@ lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, cons
 //               slot.rgb <- rgb                                                  -> [computed]
 //   out_stream: wait computed; D2H slot.rgb -> rgb_hosts[i]; status word         -> [drained]
 // so batch k+1's copy-in and batch k-1's copy-out overlap batch k's graph.
-lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
-                                  uint8_t* const* rgb_hosts, uint64_t* ticket) {
+static lbx_status submit_impl(lbx_decoder* dec, const uint8_t* const* blobs, const int* blob_devs,
+                              const size_t* nbytes, uint32_t n, uint8_t* const* rgb_hosts, uint64_t* ticket) {
   if (!dec || !rgb_hosts || !ticket) return set_err(LBX_E_CONFIG, "lbx_reconstruct_submit: null argument");
   for (uint32_t i = 0; i < n; ++i)
     if (!rgb_hosts[i]) return set_err(LBX_E_CONFIG, "rgb_hosts: null entry");
@@ -1008,7 +1055,12 @@ lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs,
   if ((st = d.graph_for((int)n, d.stream, &ex)) != LBX_OK) return st;  // captured once per n
   // the slot's latents were last read by its previous batch's copy on `stream`
   LBX_CUDA_TRY(cudaStreamWaitEvent(d.in_stream, sl.computed, 0));
-  if ((st = d.stage_blobs(sl.st, blobs, nbytes, n, d.in_stream, sl.lat, sl.err)) != LBX_OK) return st;
+  sl.timed_peer = false;
+  if (blob_devs)
+    for (uint32_t i = 0; i < n; ++i) sl.timed_peer |= blob_devs[i] >= 0 && blob_devs[i] != d.desc.device;
+  if (sl.timed_peer) LBX_CUDA_TRY(cudaEventRecord(sl.peer0, d.in_stream));
+  if ((st = d.stage_blobs(sl.st, blobs, nbytes, n, d.in_stream, sl.lat, sl.err, blob_devs)) != LBX_OK) return st;
+  if (sl.timed_peer) LBX_CUDA_TRY(cudaEventRecord(sl.peer1, d.in_stream));
   LBX_CUDA_TRY(cudaEventRecord(sl.unpacked, d.in_stream));
   LBX_CUDA_TRY(cudaStreamWaitEvent(d.stream, sl.unpacked, 0));
   LBX_CUDA_TRY(cudaMemcpyAsync(d.lat, sl.lat, d.lat_elems(n) * 2, cudaMemcpyDeviceToDevice, d.stream));
@@ -1029,6 +1081,27 @@ lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs,
   return LBX_OK;
 }
 
+lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+                                  uint8_t* const* rgb_hosts, uint64_t* ticket) {
+  return submit_impl(dec, blobs, nullptr, nbytes, n, rgb_hosts, ticket);
+}
+
+lbx_status lbx_reconstruct_submit_dev(lbx_decoder* dec, const uint8_t* const* blobs_dev, const int* blob_devices,
+                                      const size_t* nbytes, uint32_t n, uint8_t* const* rgb_hosts, uint64_t* ticket) {
+  if (!blob_devices) return set_err(LBX_E_CONFIG, "lbx_reconstruct_submit_dev: null blob_devices");
+  return submit_impl(dec, blobs_dev, blob_devices, nbytes, n, rgb_hosts, ticket);
+}
+
+lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out) {
+  if (!dec || !out) return set_err(LBX_E_CONFIG, "lbx_decoder_get_counters: null argument");
+  std::lock_guard<std::mutex> g(dec->mu);
+  out->graph_captures = dec->d.captures;
+  out->peer_copies = dec->d.peer_copies;
+  out->peer_bytes = dec->d.peer_bytes;
+  out->peer_ms = dec->d.peer_ms;
+  return LBX_OK;
+}
+
 lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket) {
   if (!dec) return set_err(LBX_E_CONFIG, "lbx_reconstruct_wait: null decoder");
   cudaEvent_t ev = nullptr;
@@ -1045,6 +1118,10 @@ lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket) {
   std::lock_guard<std::mutex> g(dec->mu);
   Decoder::Slot& sl = dec->d.slots[slot];
   sl.busy = false;
+  if (sl.timed_peer && e == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, sl.peer0, sl.peer1) == cudaSuccess) dec->d.peer_ms += ms;
+  }
   if (e != cudaSuccess) return set_err(LBX_E_CUDA, std::string("reconstruct: ") + cudaGetErrorString(e));
   if (*sl.err_host) {
     const int code = *sl.err_host;

@@ -178,11 +178,13 @@ def test_batch_invariance_full_size(lbx):
     z = torch.randn((32, 4, 128, 128), generator=g, device=dev).half()
     dec = lbx.Decoder("sd15", (128, 128), seed=0, max_batch=32)
     rgb = torch.empty((32, 1024, 1024, 3), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()  # stream 0 = the decoder's own (non-blocking) stream
     s = torch.cuda.current_stream().cuda_stream
     dec.decode_ptr(z.data_ptr(), 32, rgb.data_ptr(), s)
     one = torch.empty((1, 1024, 1024, 3), dtype=torch.uint8, device=dev)
     for i in (0, 13, 31):
         zi = z[i:i + 1].contiguous()
+        torch.cuda.synchronize()
         dec.decode_ptr(zi.data_ptr(), 1, one.data_ptr(), s)
         torch.cuda.synchronize()
         assert torch.equal(one[0], rgb[i]), i

@@ -67,3 +67,56 @@ def test_shard_range_balanced():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_launch_plan():
+    from paper_2605_19385_b200.dist import launch_plan, spawn_argv
+    assert launch_plan(1, {}, 1) == "single"
+    assert launch_plan(8, {}, 8) == "spawn"
+    assert launch_plan(8, {"WORLD_SIZE": "8"}, 8) == "ranked"
+    assert launch_plan(1, {"WORLD_SIZE": "1"}, 1) == "single"
+    for gpus, env, vis in ((2, {}, 1), (8, {"WORLD_SIZE": "4"}, 8), (0, {}, 8)):
+        with pytest.raises(ValueError):
+            launch_plan(gpus, env, vis)
+    cmd = spawn_argv("py", "bench.py", ["--gpus", "4"], 4, 29500)
+    assert cmd[:3] == ["py", "-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-3:] == ["bench.py", "--gpus", "4"]
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`python bench.py --gpus 2` on a box with fewer GPUs must fail loudly, not time one GPU and
+    report n_gpus = 1."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    visible = torch.cuda.device_count()
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(visible + 1), "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 2, r.stdout + r.stderr
+    assert f"needs {visible + 1} GPUs" in r.stderr
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_19385_b200.dist import gather_floats
+    vals = gather_floats(100.0 + rank)
+    if rank == 0:
+        q.put(vals)
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_per_rank_gather():
+    """The bench's per-rank img/s gather (rank order) over gloo, world size 2."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    vals = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert vals == [100.0, 101.0]
