@@ -418,6 +418,28 @@ def leg_batcher_service(lbx, torch, dev, stream, seconds=4.0):
             "note": "batcher = host blob validate/stage + H2D + unpack + graph + D2H, two batches in flight"}
 
 
+def leg_peer_spill(torch, world):
+    """Latent spillover over NVLink: a batch of 64 sd3 latent blobs (LBLP mode 1,
+    ~0.55 MB each) resident in GPU 1's HBM copied peer-to-peer into GPU 0, the copy a spilled
+    decode's worker issues (lbx_reconstruct_submit_dev).  Replaces the reference's modeled
+    LatencyModel::intra_cluster_ms = 5 (proj/include/latentbox/sim.hpp:20).  Rank 0, N > 1."""
+    if world < 2 or torch.cuda.device_count() < 2:
+        return None
+    nbytes, n = 548 * 1024, 64
+    src = torch.randint(0, 255, (n, nbytes), dtype=torch.uint8, device="cuda:1")
+    dst = torch.empty((n, nbytes), dtype=torch.uint8, device="cuda:0")
+    s = torch.cuda.Stream("cuda:0")
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        one = timed_events(s, lambda: dst[0].copy_(src[0], non_blocking=True), 50) / 50
+        many = timed_events(s, lambda: dst.copy_(src, non_blocking=True), 10) / 10
+    torch.cuda.synchronize()
+    return {"workload": f"{n} x {nbytes} B latent blobs, cuda:1 -> cuda:0 peer copy (torch copy_ = cudaMemcpyPeerAsync)",
+            "one_blob_ms": round(one, 4), "batch_ms": round(many, 4), "GBps": round(n * nbytes / many / 1e6, 1),
+            "reference_intra_cluster_ms": 5.0}
+
+
 def main():
     args = parse()
     import torch
@@ -625,6 +647,7 @@ def main():
     # through one batcher driving all N GPUs of the box at 25x per GPU.
     latency = None
     barrier()
+    spill = leg_peer_spill(torch, world) if rank == 0 else None
     if rank == 0 and not args.no_latency:
         latency = c5_latency(local, scale=25 * world, devices=world)
     barrier()
@@ -642,7 +665,7 @@ def main():
             "per_rank_img_s": [round(v, 2) for v in per_rank],
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,
-            "configs": configs, "batcher_service": batcher,
+            "configs": configs, "batcher_service": batcher, "nvlink_spill": spill,
             "kernels": kernels,
             "latency": latency,
         }

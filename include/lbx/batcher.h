@@ -56,21 +56,39 @@ typedef struct {
 
 typedef struct lbx_batcher lbx_batcher;
 
-lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out);
+LBX_API lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out);
 /* Stops the workers after draining queued requests, then frees everything. */
-lbx_status lbx_batcher_destroy(lbx_batcher* b);
+LBX_API lbx_status lbx_batcher_destroy(lbx_batcher* b);
 
 /* Enqueue one request.  The blob is copied.  rgb_out (8h x 8w x 3 bytes, host memory; pinned is
  * fastest) must stay valid until the request's completion is returned by lbx_batcher_poll.  A
  * request_id still in flight (submitted, completion not yet polled) is rejected with LBX_E_CONFIG. */
-lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob, size_t nbytes,
+LBX_API lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob, size_t nbytes,
                               uint8_t* rgb_out);
 
+/* Enqueue one request whose blob is resident in GPU memory (an HBM latent tier): nbytes at device
+ * pointer blob_dev on CUDA device blob_device, valid until the completion is polled.  Whichever
+ * worker takes it copies the blob D2D (same GPU) or fetches it over NVLink with a peer copy (another
+ * GPU): a spilled decode's latent shipping, LatencyModel::intra_cluster_ms = 5 in the reference
+ * (proj/include/latentbox/sim.hpp:20, proj/src/router.cpp:99-114).  Headers are checked by the
+ * device unpack (the completion's status is LBX_E_FORMAT for a malformed blob). */
+LBX_API lbx_status lbx_batcher_submit_device(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob_dev,
+                                     size_t nbytes, int blob_device, uint8_t* rgb_out);
+
+typedef struct {
+  uint64_t spills;         /* device-resident blobs decoded on a GPU other than their own */
+  uint64_t spill_bytes;    /* their bytes */
+  uint64_t peer_copies;    /* peer copies the decoders issued (== spills) */
+  double peer_ms;          /* device time of the batches' peer-copy phases, summed */
+  uint64_t graph_captures; /* CUDA graphs captured by the workers' decoders */
+} lbx_batcher_stats;
+LBX_API lbx_status lbx_batcher_get_stats(lbx_batcher* b, lbx_batcher_stats* out);
+
 /* Up to cap completions.  Waits up to wait_us for the first one.  Returns the count (>= 0). */
-int lbx_batcher_poll(lbx_batcher* b, lbx_completion* out, int cap, uint32_t wait_us);
+LBX_API int lbx_batcher_poll(lbx_batcher* b, lbx_completion* out, int cap, uint32_t wait_us);
 
 /* Requests submitted but not yet returned by poll. */
-uint64_t lbx_batcher_pending(lbx_batcher* b);
+LBX_API uint64_t lbx_batcher_pending(lbx_batcher* b);
 
 /* Batch size to close from `queued` waiting requests, 1 <= result <= min(queued, max_batch) (0 if
  * queued == 0), given a service curve cost_ms[b-1] = GPU time of a batch of b, b = 1..n_cost
@@ -78,10 +96,10 @@ uint64_t lbx_batcher_pending(lbx_batcher* b);
  * batch must beat the best smaller one by 2%.  cost_ms == NULL: min(queued, max_batch) (greedy).
  * On B200 the decode's time per image is flat in the batch size, so this returns 1 and batching
  * adds only latency; on engines with a fixed per-launch cost it batches. */
-uint32_t lbx_batch_pick(const double* cost_ms, uint32_t n_cost, uint32_t queued, uint32_t max_batch);
+LBX_API uint32_t lbx_batch_pick(const double* cost_ms, uint32_t n_cost, uint32_t queued, uint32_t max_batch);
 
 /* Steady-clock microseconds, the time base of lbx_completion. */
-uint64_t lbx_now_us(void);
+LBX_API uint64_t lbx_now_us(void);
 
 #ifdef __cplusplus
 }

@@ -32,6 +32,16 @@
 
 #include "lbx/lblp.h"
 
+/* The library is built with hidden visibility: exactly the functions declared LBX_API are exported
+ * (its C++ internals never clash with a host program's symbols). */
+#ifndef LBX_API
+#if defined(__GNUC__)
+#define LBX_API __attribute__((visibility("default")))
+#else
+#define LBX_API
+#endif
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -65,35 +75,35 @@ typedef struct lbx_decoder lbx_decoder;
 typedef void* lbx_stream; /* cudaStream_t; NULL = the decoder's own stream */
 
 /* Number of fp32 parameters of a family's decoder (49,490,199 for SD1.5, 49,545,475 for SD3/FLUX). */
-size_t lbx_param_count(int family);
+LBX_API size_t lbx_param_count(int family);
 
 /* The deterministic parameters a seed selects (fp32, canonical order; `out` holds count floats). */
-lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t count);
+LBX_API lbx_status lbx_generate_params(int family, uint64_t seed, float* out, size_t count);
 
-lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out);
-lbx_status lbx_decoder_destroy(lbx_decoder* dec);
+LBX_API lbx_status lbx_decoder_create(const lbx_decoder_desc* desc, lbx_decoder** out);
+LBX_API lbx_status lbx_decoder_destroy(lbx_decoder* dec);
 /* Capture (without running) the CUDA graphs for every batch size 1..n_max, so the first request of
  * each size does not pay graph capture (~tens of ms).  Graphs run on the decoder's own latent / RGB
  * buffers; every entry point (including lbx_decode on caller device buffers) reuses them. */
-lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max);
+LBX_API lbx_status lbx_decoder_prepare(lbx_decoder* dec, uint32_t n_max);
 
 /* Packed LBLP blobs (HOST memory) -> fp16 NCHW latents on the device, bit-exact.  Blob shapes must
  * equal the decoder's (C, latent_h, latent_w).  Asynchronous on `stream`; a malformed blob is
  * reported as LBX_E_FORMAT (host-side header validation) or at the next synchronising call. */
-lbx_status lbx_unpack(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+LBX_API lbx_status lbx_unpack(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                       void* latents_dev, lbx_stream stream);
 
 /* fp16 NCHW latents (device) -> uint8 RGB NHWC (device), n x 8h x 8w x 3.  Asynchronous. */
-lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uint8_t* rgb_dev,
+LBX_API lbx_status lbx_decode(lbx_decoder* dec, const void* latents_dev, uint32_t n, uint8_t* rgb_dev,
                       lbx_stream stream);
 
 /* The call the cache tiers make on a miss: host blobs -> H2D -> unpack -> decode (CUDA graph) ->
  * D2H into rgb_host (n x 8h x 8w x 3).  Synchronous: returns when rgb_host is filled. */
-lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+LBX_API lbx_status lbx_reconstruct(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                            uint8_t* rgb_host, lbx_stream stream);
 
 /* Vectored form: image i lands in rgb_hosts[i] (8h x 8w x 3 bytes each).  Synchronous. */
-lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+LBX_API lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                              uint8_t* const* rgb_hosts, lbx_stream stream);
 
 /* Asynchronous, pipelined form of lbx_reconstruct_v (what lbx_batcher's workers use).  Stages the
@@ -103,14 +113,14 @@ lbx_status lbx_reconstruct_v(lbx_decoder* dec, const uint8_t* const* blobs, cons
  * decompression and encoding in pools around GPU inference).  A third submit before the oldest
  * ticket is waited for returns LBX_E_RUNTIME.  Blob headers are validated before anything is
  * enqueued (LBX_E_FORMAT, no ticket).  rgb_hosts[i] must stay valid until the wait returns. */
-lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+LBX_API lbx_status lbx_reconstruct_submit(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                                   uint8_t* const* rgb_hosts, uint64_t* ticket);
 /* Block until the batch of `ticket` is in rgb_hosts; its status (LBX_E_FORMAT if the device unpack
  * found a malformed blob).  Each ticket is waited for exactly once. */
-lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket);
+LBX_API lbx_status lbx_reconstruct_wait(lbx_decoder* dec, uint64_t ticket);
 
 /* CUDA graphs this decoder has captured (one per batch size; caller buffers never cause one). */
-uint64_t lbx_graph_captures(lbx_decoder* dec);
+LBX_API uint64_t lbx_graph_captures(lbx_decoder* dec);
 
 /* Same pipeline for blobs resident in GPU memory (an HBM latent tier): blob i is nbytes[i] bytes at
  * device pointer blobs_dev[i] on CUDA device blob_devices[i] (-1: host memory, handled as in
@@ -119,7 +129,7 @@ uint64_t lbx_graph_captures(lbx_decoder* dec);
  * of a spilled decode, which the reference models as LatencyModel::intra_cluster_ms = 5
  * (proj/include/latentbox/sim.hpp:20, proj/src/sim.cpp:369-373, proj/src/router.cpp:99-114).  Blob
  * headers are validated by the device unpack (LBX_E_FORMAT at the wait). */
-lbx_status lbx_reconstruct_submit_dev(lbx_decoder* dec, const uint8_t* const* blobs_dev, const int* blob_devices,
+LBX_API lbx_status lbx_reconstruct_submit_dev(lbx_decoder* dec, const uint8_t* const* blobs_dev, const int* blob_devices,
                                       const size_t* nbytes, uint32_t n, uint8_t* const* rgb_hosts, uint64_t* ticket);
 
 typedef struct {
@@ -128,23 +138,23 @@ typedef struct {
   uint64_t peer_bytes;     /* their bytes */
   double peer_ms;          /* device time of the batches' peer-copy phases, summed (CUDA events) */
 } lbx_decoder_counters;
-lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out);
+LBX_API lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out);
 
 /* Same path from fp16 NCHW latents in HOST memory (no codec): H2D -> decode -> D2H.  Synchronous. */
-lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
+LBX_API lbx_status lbx_reconstruct_latents(lbx_decoder* dec, const void* latents_host, uint32_t n, uint8_t* rgb_host,
                                    lbx_stream stream);
 
 /* Host-side LBLP packer (the write path).  `latent` is one fp16 NCHW latent (c*h*w values).
  * Returns the blob size; writes it when out != NULL and cap is large enough. */
-lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, uint32_t w, uint8_t* out,
+LBX_API lbx_status lbx_pack(const uint16_t* latent, int mode, uint32_t c, uint32_t h, uint32_t w, uint8_t* out,
                     size_t cap, size_t* out_bytes);
 
 /* Device-side write path: LBLP mode-1 (lossless) pack of n fp16 NCHW latents already on the GPU
  * (latents_dev, c x h x w each, w % 32 == 0).  Blob i is written at out_dev + i * stride (stride >=
  * lbx_pack_bound(c, h, w), multiple of 4) and its size to sizes_dev[i] (uint32, device).  The bytes
  * equal lbx_pack(..., mode 1, ...).  Asynchronous on `stream` (NULL = default stream). */
-size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w);
-lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint32_t h, uint32_t w, uint8_t* out_dev,
+LBX_API size_t lbx_pack_bound(uint32_t c, uint32_t h, uint32_t w);
+LBX_API lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint32_t h, uint32_t w, uint8_t* out_dev,
                            size_t stride, uint32_t* sizes_dev, lbx_stream stream);
 
 /* Return path (the paper PNG-encodes on CPU): PNG encode of n
@@ -153,31 +163,31 @@ lbx_status lbx_pack_device(const void* latents_dev, uint32_t n, uint32_t c, uint
  * (uint32, device).  8-bit RGB, per-row adaptive filter, zlib/DEFLATE with dynamic Huffman codes
  * (stored where smaller); lossless: any PNG decoder returns rgb exactly.  w <= 8192, h <= 65535.
  * Asynchronous on `stream`. */
-size_t lbx_png_bound(uint32_t h, uint32_t w);
+LBX_API size_t lbx_png_bound(uint32_t h, uint32_t w);
 /* lbx_reconstruct with the return path on the GPU: host blobs -> unpack -> decode -> PNG encode ->
  * only the PNG bytes cross PCIe.  PNG i is written at png_host + (png_sizes[0] + ... + png_sizes[i-1])
  * and its length to png_sizes[i].  cap = bytes available at png_host; n * lbx_png_bound(8*latent_h,
  * 8*latent_w) always suffices; if the PNGs need more, LBX_E_CONFIG (sizes still returned). */
-lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
+LBX_API lbx_status lbx_reconstruct_png(lbx_decoder* dec, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
                                uint8_t* png_host, size_t cap, size_t* png_sizes, lbx_stream stream);
-lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
+LBX_API lbx_status lbx_png_encode_device(const uint8_t* rgb_dev, uint32_t n, uint32_t h, uint32_t w, uint8_t* out_dev,
                                  size_t stride, uint32_t* sizes_dev, lbx_stream stream);
 
 /* Unpack of LBLP blobs already in device memory (e.g. an HBM-resident latent tier): blob i at
  * blobs_dev + offs_dev[i] (8-byte aligned), sizes_dev[i] bytes; out_dev = n fp16 NCHW latents of
  * c x h x w.  A malformed blob sets *err_dev (device int, zero it first) to a nonzero code and leaves
  * that latent unspecified.  Bit-exact with lbx_unpack.  Asynchronous on `stream`. */
-lbx_status lbx_op_unpack(const uint8_t* blobs_dev, const unsigned long long* offs_dev, const uint32_t* sizes_dev,
+LBX_API lbx_status lbx_op_unpack(const uint8_t* blobs_dev, const unsigned long long* offs_dev, const uint32_t* sizes_dev,
                          uint32_t n, uint32_t c, uint32_t h, uint32_t w, void* out_dev, int* err_dev,
                          lbx_stream stream);
 
 /* Page-locked host memory for blobs and outputs (cudaMallocHost): copies to and from it run at full
  * PCIe rate, where pageable memory goes through a staging copy.  NULL on failure. */
-void* lbx_host_alloc(size_t bytes);
-void lbx_host_free(void* p);
+LBX_API void* lbx_host_alloc(size_t bytes);
+LBX_API void lbx_host_free(void* p);
 
 /* Thread-local description of the last error on this thread ("" if none). */
-const char* lbx_last_error(void);
+LBX_API const char* lbx_last_error(void);
 
 /* ------------------------------------------------------------------ profiling
  * Run one decode of n latents (internal buffers) eagerly with a CUDA event after every launch and
@@ -191,10 +201,10 @@ typedef struct {
   double algo_flops;
   double bytes;
 } lbx_prof_entry;
-lbx_status lbx_profile(lbx_decoder* dec, uint32_t n, lbx_prof_entry* out, int cap, int* count);
+LBX_API lbx_status lbx_profile(lbx_decoder* dec, uint32_t n, lbx_prof_entry* out, int cap, int* count);
 
 /* Kernel launches in one decode of batch n (after the first lbx_decode/reconstruct of that n), or -1. */
-int lbx_launch_count(lbx_decoder* dec, uint32_t n);
+LBX_API int lbx_launch_count(lbx_decoder* dec, uint32_t n);
 
 /* ------------------------------------------------------------------ diagnostics / op-level entry
  * Individual kernels of the path, for op-level parity tests and benchmarks.  Device pointers,
@@ -206,7 +216,7 @@ int lbx_launch_count(lbx_decoder* dec, uint32_t n);
  * gn_stats (optional, uint64 [b][32][2][2], accumulated) gets GroupNorm-32 partial sums of out as
  * exact fixed-point pairs: value = (int64)hi * 4 + lo * 2^-30 (order-independent, see gnfix.cuh).
  * cta_group/bn: 0 = auto, else force 1|2 and 128|256. */
-lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
+LBX_API lbx_status lbx_op_gemm(int mode, int M, int N, int K, const void* A, int lda, int b, int h, int w, int c,
                        const void* Bw, int ldb, void* out, int ldo, const float* bias, const void* resid, int ldr,
                        const float* row_scale, float alpha, uint64_t* gn_stats, int cta_group, int bn,
                        lbx_stream stream);
@@ -233,7 +243,7 @@ typedef struct {
   const float* gn_ss; /* optional: fused A' = SiLU(A * ss[img][c].x + ss[img][c].y) (conv3x3), float pairs */
   int b_mn_major;     /* plain GEMM: B is [K][N] with N contiguous (row stride ldb) instead of [N][K] */
 } lbx_gemm_desc;
-lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
+LBX_API lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
 /* Diagnostics.  halo_policy bits: 0 = halo staging when possible (else per-tap A staging); 1 disables
  * the two-sub-tile variant; 2 enables the fused GroupNorm A-operand transform (XF) in the decoder;
  * 4 selects the CUDA-core conv_out tail; 5 gives halo convs two A stages and the rest of smem to B;
@@ -252,26 +262,26 @@ lbx_status lbx_op_gemm_desc(const lbx_gemm_desc* d, lbx_stream stream);
  * stages every eligible GEMM's epilogue chunks in smem and TMA-stores them (default: plain GEMMs
  * only, i.e. the attention projections and scores), 26 disables the TMA-store epilogue.
  * desc_base_mode selects the UMMA descriptor base-offset convention for row-shifted halo views. */
-lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
+LBX_API lbx_status lbx_op_set_debug(int halo_policy, int desc_base_mode);
 /* Diagnostics: GEMM grids use at most gemm_sms SMs and bulk GroupNorm applies at most apply_sms
  * (0 = all), so that two kernels can share the GPU on different streams. */
-lbx_status lbx_op_set_grid_limits(int gemm_sms, int apply_sms);
+LBX_API lbx_status lbx_op_set_grid_limits(int gemm_sms, int apply_sms);
 /* Decoder tail: rgb = u8(conv3x3_{128->3}(SiLU(x * ss.x + ss.y)) + b) with x fp16 NHWC [n][H][W][128],
  * ss float pairs [n][128], w fp32 [3][3][3][128] ([out][ky][kx][in]), rgb [n][H][W][3].  impl 0 =
  * tensor cores (fp32 SiLU), 2 = tensor cores with packed-half SiLU, 1 = CUDA cores (fp32). */
-lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
+LBX_API lbx_status lbx_op_conv_out(const void* x, const float* ss, const float* w, const float* b, uint8_t* rgb, int n,
                            int H, int W, int impl, lbx_stream stream);
 /* Mid-block attention core without the L x L scores (csrc/attn_fa.cu): out [n][L][512] =
  * softmax(Q K^T / sqrt(512)) V, Q/K/V = column blocks 0/512/1024 of qkv [n][L][1536] fp16; L % 128 == 0. */
-lbx_status lbx_op_attention(const void* qkv, void* out, int n, int L, lbx_stream stream);
+LBX_API lbx_status lbx_op_attention(const void* qkv, void* out, int n, int L, lbx_stream stream);
 /* Fold a 3x3 conv weight [N][3][3][C] (fp32, host) into the 4 sub-pixel 2x2 kernels, fp16 [4][N][2][2][C]. */
-lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
+LBX_API lbx_status lbx_subpixel_weights(const float* w3x3, int N, int C, uint16_t* out);
 /* GroupNorm finalize + apply; silu 0 = identity, 1 = fp32 SiLU, 2 = packed-half SiLU; y may alias x. */
-lbx_status lbx_op_groupnorm(const void* x, void* y, const uint64_t* stats, const float* gamma, const float* beta,
+LBX_API lbx_status lbx_op_groupnorm(const void* x, void* y, const uint64_t* stats, const float* gamma, const float* beta,
                             int b, int hw, int c, int silu, float eps, lbx_stream stream);
 /* GroupNorm-32 statistics of x ([b][hw][c] fp16) into stats (uint64 [b][32][2][2] fixed point, zeroed
  * here). */
-lbx_status lbx_op_gn_stats(const void* x, uint64_t* stats, int b, int hw, int c, lbx_stream stream);
+LBX_API lbx_status lbx_op_gn_stats(const void* x, uint64_t* stats, int b, int hw, int c, lbx_stream stream);
 
 #ifdef __cplusplus
 }

@@ -7,10 +7,17 @@
 REF ?= /root/reference/proj
 JSON ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
 OUT := _ref
-SRCS := synth dual_cache tuner trace router
+SRCS := synth dual_cache tuner trace router sim
 OBJS := $(addprefix $(OUT)/,$(addsuffix .o,$(SRCS)))
 
-all: $(OUT)/libref_sim.a
+LBX := ../paper_2605_19385_b200
+
+all: $(OUT)/libref_sim.a $(OUT)/ref_binding
+
+# the reference-side binding (tools/ref_binding.cpp): reference simulator + this repo's C ABI
+$(OUT)/ref_binding: ../tools/ref_binding.cpp $(OUT)/libref_sim.a $(LBX)/liblbx.so
+	g++ -std=c++20 -O2 -I$(REF)/include -I../include $< $(OUT)/libref_sim.a -L$(LBX) -llbx \
+	  -Wl,-rpath,'$$ORIGIN/../../paper_2605_19385_b200' -lpthread -o $@
 
 $(OUT)/%.o: $(REF)/src/%.cpp
 	@mkdir -p $(OUT)

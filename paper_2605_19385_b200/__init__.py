@@ -415,6 +415,11 @@ class Completion(ctypes.Structure):
                 ("t_end_us", ctypes.c_uint64), ("worker", ctypes.c_int)]
 
 
+class BatcherStats(ctypes.Structure):
+    _fields_ = [("spills", ctypes.c_uint64), ("spill_bytes", ctypes.c_uint64), ("peer_copies", ctypes.c_uint64),
+                ("peer_ms", ctypes.c_double), ("graph_captures", ctypes.c_uint64)]
+
+
 def _batcher_lib():
     L = lib()
     if not getattr(L, "_batcher_ready", False):
@@ -427,6 +432,11 @@ def _batcher_lib():
         L.lbx_batcher_submit.restype = ctypes.c_int
         L.lbx_batcher_poll.argtypes = [vp, ctypes.POINTER(Completion), ctypes.c_int, ctypes.c_uint32]
         L.lbx_batcher_poll.restype = ctypes.c_int
+        L.lbx_batcher_submit_device.argtypes = [vp, ctypes.c_uint64, ctypes.c_int, vp, ctypes.c_size_t, ctypes.c_int,
+                                                vp]
+        L.lbx_batcher_submit_device.restype = ctypes.c_int
+        L.lbx_batcher_get_stats.argtypes = [vp, ctypes.POINTER(BatcherStats)]
+        L.lbx_batcher_get_stats.restype = ctypes.c_int
         L.lbx_batcher_pending.argtypes = [vp]
         L.lbx_batcher_pending.restype = ctypes.c_uint64
         L.lbx_now_us.restype = ctypes.c_uint64
@@ -464,6 +474,24 @@ class Batcher:
         check(_batcher_lib().lbx_batcher_submit(self._h, request_id, shape, buf.ctypes.data, buf.size,
                                                 out.ctypes.data))
         self._keep[request_id] = out  # after the C side accepted it: a rejected duplicate keeps the original
+
+    def submit_device(self, request_id: int, shape: int, blob_ptr: int, nbytes: int, blob_device: int,
+                      out: np.ndarray, keep=None):
+        """Enqueue a request whose LBLP blob is resident in GPU memory (blob_ptr on CUDA device
+        blob_device, e.g. a torch tensor's data_ptr()); `keep` (e.g. that tensor) is held until the
+        completion is polled.  A worker on another GPU fetches it with a peer copy (NVLink spill)."""
+        if not 0 <= shape < len(self._rgb_bytes):
+            raise LbxError(E_CONFIG, f"shape: no shape class {shape}")
+        _check_out(out, self._rgb_bytes[shape], "out")
+        check(_batcher_lib().lbx_batcher_submit_device(self._h, request_id, shape, blob_ptr, nbytes, blob_device,
+                                                       out.ctypes.data))
+        self._keep[request_id] = (out, keep)
+
+    def stats(self) -> dict:
+        st = BatcherStats()
+        check(_batcher_lib().lbx_batcher_get_stats(self._h, ctypes.byref(st)))
+        return {"spills": st.spills, "spill_bytes": st.spill_bytes, "peer_copies": st.peer_copies,
+                "peer_ms": st.peer_ms, "graph_captures": st.graph_captures}
 
     def poll(self, cap=256, wait_us=1000):
         arr = (Completion * cap)()

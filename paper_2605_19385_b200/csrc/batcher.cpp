@@ -43,7 +43,10 @@ uint64_t now_us() {
 
 struct Request {
   uint64_t id;
-  std::vector<uint8_t> blob;
+  std::vector<uint8_t> blob;  // host blob (copied at submit) ...
+  const uint8_t* blob_dev;    // ... or a blob resident in GPU memory (HBM latent tier)
+  size_t dev_bytes;
+  int blob_device;            // -1: host blob; else the CUDA device holding blob_dev
   uint8_t* rgb;
   uint64_t t_submit;
 };
@@ -65,6 +68,8 @@ struct lbx_batcher {
   int init_status = LBX_OK;
   int workers_ready = 0;
   int idle = 0;                            // workers with nothing in flight, waiting for work
+  uint64_t spills = 0, spill_bytes = 0;    // device-resident blobs decoded on another GPU
+  std::vector<std::vector<lbx_decoder*>> decs;  // [worker][shape], for the counters
   std::unordered_set<uint64_t> live_ids;   // submitted, not yet returned by poll
   std::vector<std::vector<std::vector<double>>> curves;  // [worker][shape] (policy 1)
 
@@ -155,6 +160,10 @@ void lbx_batcher::worker(int di) {
     d.device = device;
     d.max_batch = desc.max_batch;
     st = lbx_decoder_create(&d, &decs[s]);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      this->decs[di][s] = decs[s];
+    }
     if (st == LBX_OK) st = lbx_decoder_prepare(decs[s], desc.max_batch);  // no capture on the request path
     if (st == LBX_OK && desc.policy == 1) {
       const int ch = shapes[s].family == LBX_FAMILY_SD15 ? 4 : 16;
@@ -183,6 +192,7 @@ void lbx_batcher::worker(int di) {
   std::deque<InFlight> inflight;  // <= 2 (the decoder pipeline's depth)
   std::vector<const uint8_t*> blobs;
   std::vector<size_t> sizes;
+  std::vector<int> blob_devs;
   std::vector<uint8_t*> outs;
   auto complete = [&](std::vector<Request>& reqs, lbx_status rs, uint64_t t_start) {
     const uint64_t t_end = now_us();
@@ -237,14 +247,31 @@ void lbx_batcher::worker(int di) {
       if (rs == LBX_OK) {
         blobs.clear();
         sizes.clear();
+        blob_devs.clear();
         outs.clear();
+        bool any_dev = false;
+        uint64_t sp = 0, sp_bytes = 0;
         for (auto& r : batch) {
-          blobs.push_back(r.blob.data());
-          sizes.push_back(r.blob.size());
+          const bool on_dev = r.blob_device >= 0;
+          blobs.push_back(on_dev ? r.blob_dev : r.blob.data());
+          sizes.push_back(on_dev ? r.dev_bytes : r.blob.size());
+          blob_devs.push_back(r.blob_device);
           outs.push_back(r.rgb);
+          any_dev |= on_dev;
+          if (on_dev && r.blob_device != device) {
+            ++sp;
+            sp_bytes += r.dev_bytes;
+          }
         }
-        rs = lbx_reconstruct_submit(decs[shape], blobs.data(), sizes.data(), (uint32_t)batch.size(), outs.data(),
-                                    &ticket);
+        if (sp) {
+          std::lock_guard<std::mutex> g(mu);
+          spills += sp;
+          spill_bytes += sp_bytes;
+        }
+        rs = any_dev ? lbx_reconstruct_submit_dev(decs[shape], blobs.data(), blob_devs.data(), sizes.data(),
+                                                  (uint32_t)batch.size(), outs.data(), &ticket)
+                     : lbx_reconstruct_submit(decs[shape], blobs.data(), sizes.data(), (uint32_t)batch.size(),
+                                              outs.data(), &ticket);
       }
       if (rs == LBX_OK) inflight.push_back(InFlight{ticket, shape, std::move(batch), t_start});
       else complete(batch, rs, t_start);
@@ -255,6 +282,10 @@ void lbx_batcher::worker(int di) {
     const lbx_status rs = lbx_reconstruct_wait(decs[f.shape], f.ticket);
     complete(f.reqs, rs, f.t_start);
     inflight.pop_front();
+  }
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto*& d : this->decs[di]) d = nullptr;
   }
   for (auto* d : decs)
     if (d) lbx_decoder_destroy(d);
@@ -279,6 +310,21 @@ lbx_status lbx_batcher_create(const lbx_batcher_desc* desc, lbx_batcher** out) {
   b->shapes.assign(desc->shapes, desc->shapes + desc->n_shapes);
   b->queues.resize(desc->n_shapes);
   b->curves.assign(desc->n_devices, std::vector<std::vector<double>>(desc->n_shapes));
+  b->decs.assign(desc->n_devices, std::vector<lbx_decoder*>(desc->n_shapes, nullptr));
+  // NVLink peer access between the batcher's GPUs, for device-resident blobs decoded elsewhere
+  // (cudaMemcpyPeerAsync also works without it, through the copy engines)
+  for (int i = 0; i < desc->n_devices; ++i)
+    for (int j = 0; j < desc->n_devices; ++j) {
+      int can = 0;
+      const int a = desc->devices[i], c = desc->devices[j];
+      if (a != c && cudaDeviceCanAccessPeer(&can, a, c) == cudaSuccess && can) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(a);
+        if (cudaDeviceEnablePeerAccess(c, 0) != cudaSuccess) cudaGetLastError();  // already enabled: fine
+        cudaSetDevice(cur);
+      }
+    }
   for (int i = 0; i < desc->n_devices; ++i) b->workers.emplace_back(&lbx_batcher::worker, b, i);
   {
     std::unique_lock<std::mutex> lk(b->mu);
@@ -310,7 +356,7 @@ lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, co
                               uint8_t* rgb_out) {
   if (!b || !blob || !rgb_out || shape < 0 || shape >= (int)b->shapes.size())
     return lbx::set_last_error(LBX_E_CONFIG, "lbx_batcher_submit: bad argument");
-  Request r{request_id, std::vector<uint8_t>(blob, blob + nbytes), rgb_out, now_us()};
+  Request r{request_id, std::vector<uint8_t>(blob, blob + nbytes), nullptr, 0, -1, rgb_out, now_us()};
   {
     std::lock_guard<std::mutex> g(b->mu);
     if (b->stopping) return lbx::set_last_error(LBX_E_RUNTIME, "lbx_batcher_submit: batcher is stopping");
@@ -321,6 +367,42 @@ lbx_status lbx_batcher_submit(lbx_batcher* b, uint64_t request_id, int shape, co
     ++b->pending;
   }
   b->cv_work.notify_one();
+  return LBX_OK;
+}
+
+lbx_status lbx_batcher_submit_device(lbx_batcher* b, uint64_t request_id, int shape, const uint8_t* blob_dev,
+                                     size_t nbytes, int blob_device, uint8_t* rgb_out) {
+  if (!b || !blob_dev || !rgb_out || shape < 0 || shape >= (int)b->shapes.size() || nbytes == 0 || blob_device < 0)
+    return lbx::set_last_error(LBX_E_CONFIG, "lbx_batcher_submit_device: bad argument");
+  Request r{request_id, {}, blob_dev, nbytes, blob_device, rgb_out, now_us()};
+  {
+    std::lock_guard<std::mutex> g(b->mu);
+    if (b->stopping) return lbx::set_last_error(LBX_E_RUNTIME, "lbx_batcher_submit_device: batcher is stopping");
+    if (!b->live_ids.insert(request_id).second)
+      return lbx::set_last_error(LBX_E_CONFIG, "lbx_batcher_submit_device: request_id " + std::to_string(request_id) +
+                                                   " is already in flight");
+    b->queues[shape].push_back(std::move(r));
+    ++b->pending;
+  }
+  b->cv_work.notify_one();
+  return LBX_OK;
+}
+
+lbx_status lbx_batcher_get_stats(lbx_batcher* b, lbx_batcher_stats* out) {
+  if (!b || !out) return lbx::set_last_error(LBX_E_CONFIG, "lbx_batcher_get_stats: null argument");
+  std::lock_guard<std::mutex> g(b->mu);
+  *out = lbx_batcher_stats{};
+  out->spills = b->spills;
+  out->spill_bytes = b->spill_bytes;
+  for (auto& row : b->decs)
+    for (auto* d : row) {
+      lbx_decoder_counters c{};
+      if (d && lbx_decoder_get_counters(d, &c) == LBX_OK) {
+        out->peer_copies += c.peer_copies;
+        out->peer_ms += c.peer_ms;
+        out->graph_captures += c.graph_captures;
+      }
+    }
   return LBX_OK;
 }
 

@@ -88,9 +88,11 @@ struct Cfg {
   static constexpr int B_ROWS = BN / CG;             // B rows staged per CTA
   static constexpr int B_BYTES = B_ROWS * 64 * 2;    // one 64-wide k-block
   static constexpr int SMEM_MAX = 227 * 1024;
-  // warp 0 A-producer, 1 MMA, 2..9 epilogue, 10 B-producer (+ 11..14 A transform in XF kernels)
+  // warp 0 A-producer, 1 MMA, 2..9 epilogue, 10 B-producer.  XF kernels are laid out by aligned
+  // warpgroups so that registers can move to the epilogue (setmaxnreg): warps 0 A-producer,
+  // 1 MMA, 2 B-producer, 3 idle | 4..11 epilogue | 12..15 A transform.
   static constexpr int THREADS = 352;
-  static constexpr int THREADS_XF = 480;
+  static constexpr int THREADS_XF = 512;
   static constexpr uint32_t IDESC = ptx::idesc_f16(128 * CG, BN);
 };
 
@@ -162,7 +164,7 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&x)[32], uint32_t 
 }
 
 template <int BN, int CG, bool XF>
-__global__ void __launch_bounds__(XF ? 480 : 352, 1)
+__global__ void __launch_bounds__(XF ? 512 : 352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmO,
                    const KParams p) {
@@ -184,6 +186,9 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
   // tstore: per epilogue warp, two 2 KB staging tiles (32 rows x 64 B, SWIZZLE_64B), 1 KB aligned
   uint8_t* sOut = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sBias + 8 * (BN / 2)) + 1023) & ~uintptr_t(1023));
   constexpr int EPI_WARPS = 8;
+  constexpr uint32_t W_B = XF ? 2 : 10;        // B producer
+  constexpr uint32_t W_EPI0 = XF ? 4 : 2;      // first epilogue warp
+  constexpr uint32_t W_XF0 = 12;               // first A-transform warp (XF)
 
   const uint32_t warp = ptx::warp_id();
   const uint32_t lane = ptx::lane_id();
@@ -226,9 +231,12 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
   // here on global memory is touched, so wait for that kernel to complete and flush
   if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
+  // XF: 512 threads start at 128 registers; each role branch re-sizes its warpgroup so that the
+  // producers' registers go to the epilogue (4 x 56 + 8 x 176 + 4 x 96 warps' worth <= 64 K)
 
   if (warp == 0) {
     // ------------------------------------------------------------ A producer (TMA)
+    if constexpr (XF) ptx::setmaxnreg_dec<56>();
     if (ptx::elect_one()) {
       int st = 0;
       uint32_t ph = 0;
@@ -301,8 +309,9 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         }
       }
     }
-  } else if (warp == 10) {
+  } else if (warp == W_B) {
     // ------------------------------------------------------------ B producer (TMA, weights)
+    if constexpr (XF) ptx::setmaxnreg_dec<56>();
     if (ptx::elect_one()) {
       int st = 0;
       uint32_t ph = 0;
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     // One thread runs the whole issue loop (no per-tap elect / reconvergence).  Descriptors are
     // built once and advanced by adding (byte offset >> 4) to the address field: every smem
     // address is < 256 KB, so the 14-bit field never carries.
+    if constexpr (XF) ptx::setmaxnreg_dec<56>();
     if (leader && ptx::elect_one()) {
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
@@ -425,14 +435,17 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
-  } else if (XF && warp >= 11) {
+  } else if (XF && warp == 3) {
+    ptx::setmaxnreg_dec<56>();  // idle (keeps the warpgroups aligned)
+  } else if (XF && warp >= W_XF0) {
     // ------------------------------------------------------------ fused GroupNorm + SiLU on A
-    // Warps 11..14 rewrite each landed halo in place: y = SiLU(x * a_c + b_c) (fp32 affine, SiLU
+    // Warps 12..15 rewrite each landed halo in place: y = SiLU(x * a_c + b_c) (fp32 affine, SiLU
     // on packed halves as in act.cuh gn_act8_h2, one fp16 rounding) for pixels inside the image;
     // out-of-image positions keep TMA's zero fill (the conv pads after the activation).  Thread t
     // owns logical 16-byte chunk t & 7 (8 channels) of every 16th halo row, so its 8 (a, b) pairs
     // load once per C-block; the physical chunk is (chunk ^ row & 7) (128B swizzle).
-    const int tid = (int)(warp - 11) * 32 + (int)lane;
+    if constexpr (XF) ptx::setmaxnreg_dec<96>();
+    const int tid = (int)(warp - W_XF0) * 32 + (int)lane;
     const int cq = tid & 7;
     const int nbox = p.vsub ? 1 : p.msub;
     const int box_rows = p.vsub ? p.halo_rows + p.msub - 1 : p.halo_rows;
@@ -463,24 +476,33 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
           for (int bx = 0; bx < nbox; ++bx) {
             const uint32_t hb = ptx::smem_u32(base + bx * p.halo_sub_bytes);
             const int xs = x0 - 1 + bx * 128;
-            int hr = (tid >> 3) / 130, px = (tid >> 3) - hr * 130;
-            // two rows per iteration: independent MUFU chains per thread
-            for (int r = tid >> 3; r < rows; r += 32) {
-              int hr2 = hr, px2 = px + 16;
-              if (px2 >= 130) { px2 -= 130; ++hr2; }
-              const int r2 = r + 16;
-              const bool v1 = y0 - 1 + hr >= 0 && y0 - 1 + hr < p.H && xs + px >= 0 && xs + px < p.W;
-              const bool v2 = r2 < rows && y0 - 1 + hr2 >= 0 && y0 - 1 + hr2 < p.H && xs + px2 >= 0 && xs + px2 < p.W;
-              const uint32_t q1 = hb + r * 128 + ((cq ^ (r & 7)) << 4);
-              const uint32_t q2 = hb + r2 * 128 + ((cq ^ (r2 & 7)) << 4);
-              const uint4 u1 = v1 ? ptx::lds128(q1) : make_uint4(0, 0, 0, 0);
-              const uint4 u2 = v2 ? ptx::lds128(q2) : make_uint4(0, 0, 0, 0);
-              const uint4 w1 = gn_act8_h2<true>(u1, ca, cb);
-              const uint4 w2 = gn_act8_h2<true>(u2, ca, cb);
-              if (v1) ptx::sts128(q1, w1);
-              if (v2) ptx::sts128(q2, w2);
-              px = px2 + 16;
-              hr = hr2;
+            // validity of halo row r = (hr, px): vertical from a per-box row mask, horizontal only
+            // at the image's left / right edge (px 0 / 129); invalid rows keep TMA's zero fill
+            uint32_t vmask = 0;
+            for (int k = 0; k < box_rows; ++k)
+              if (y0 - 1 + k >= 0 && y0 - 1 + k < p.H) vmask |= 1u << k;
+            const bool ledge = xs < 0, redge = xs + 129 >= p.W;
+            int hr = 0, px = tid >> 3;  // row r = tid/8 + 16 i, as (halo row, pixel)
+            // four rows per iteration: independent LDS -> affine -> MUFU chains per thread
+            for (int r = tid >> 3; r < rows; r += 64) {
+              uint4 u[4];
+              bool v[4];
+              uint32_t q[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                int pk = px + 16 * k, hk = hr;
+                if (pk >= 130) { pk -= 130; ++hk; }
+                const int rk = r + 16 * k;
+                v[k] = rk < rows && ((vmask >> hk) & 1u) && !(ledge && pk == 0) && !(redge && pk == 129);
+                q[k] = hb + rk * 128 + ((cq ^ (rk & 7)) << 4);
+                u[k] = v[k] ? ptx::lds128(q[k]) : make_uint4(0, 0, 0, 0);
+              }
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint4 w = gn_act8_h2<true>(u[k], ca, cb);
+                if (v[k]) ptx::sts128(q[k], w);
+              }
+              px += 64;
               if (px >= 130) { px -= 130; ++hr; }
             }
           }
@@ -495,10 +517,12 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..9)
+    // ------------------------------------------------------------ epilogue (warps 2..9; XF: 4..11)
+    if constexpr (XF) ptx::setmaxnreg_inc<176>();
     // Two warps per TMEM lane quarter; warp half `hsel` takes the even/odd 32-column chunks.
     const uint32_t q = warp & 3;
-    const int hsel = (int)(warp - 2) >> 2;
+    const int ew = (int)(warp - W_EPI0);  // epilogue warp index 0..7
+    const int hsel = ew >> 2;
     const int row = q * 32 + lane;
     constexpr int NCH = BN / 32 / (EPI_WARPS / 4);  // chunks per warp per tile
     // 32-column chunk j of this warp: contiguous (the warp owns whole 128-byte row segments, so a
@@ -518,7 +542,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
     // as broadcast LDS.128 (an LDG per chunk put the L1 latency on the epilogue's critical path)
     // shared-space address: the pointer arithmetic on the dynamic smem base makes the compiler emit
     // generic LD.E/ST.E for plain dereferences (long-scoreboard stalls in ncu), so use LDS/STS
-    const uint32_t wbias = ptx::smem_u32(sBias) + (warp - 2) * (NCH * 32) * 4;
+    const uint32_t wbias = ptx::smem_u32(sBias) + ew * (NCH * 32) * 4;
     int bias_ntile = -1;
     const bool scaled = p.row_scale != nullptr || p.alpha != 1.f;
     int g_img = -1, g_ntile = -1;
@@ -547,7 +571,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         // (lane l: pixel 8k + l/4, quarter l%4), transposed through the warp's 2 KB swizzled stage
         int mt, nt, phn;
         tile_coords(p, tn, mt, nt, phn);
-        const uint32_t stage = ptx::smem_u32(sOut + (warp - 2) * 2 * 2048);
+        const uint32_t stage = ptx::smem_u32(sOut + ew * 2 * 2048);
         for (int sub = 0; sub < p.msub; ++sub) {
           const long long prow0 = tile_row0(p, mt, (int)rank, CG, sub) + q * 32;  // the warp's first pixel row
           const uint32_t tb = tmem_base + ((q * 32u) << 16) + buf * (p.msub * BN) + sub * BN;
@@ -747,7 +771,7 @@ __global__ void __launch_bounds__(XF ? 480 : 352, 1)
         if (p.tstore) {
           // stage the warp's 32 x 32 chunk (conflict-free under the 64B swizzle) and TMA-store it:
           // 16 smem wavefronts instead of 64 L1 wavefronts for two STG.256 with 32 distinct rows
-          uint8_t* buf = sOut + ((warp - 2) * 2 + (ochunk & 1)) * 2048;
+          uint8_t* buf = sOut + (ew * 2 + (ochunk & 1)) * 2048;
           if (lane == 0) ptx::bulk_wait_read<1>();  // the store that used this buffer has read it
           __syncwarp();
           const uint32_t base = ptx::smem_u32(buf) + lane * 64;

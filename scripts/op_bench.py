@@ -42,7 +42,7 @@ def main():
     b, hw, c = a.b, a.hw, a.c
     n = a.n or c
     x = (torch.randn(b, hw, hw, c, device=dev) * 0.5).half()
-    stats = torch.zeros(b, 32, 2, dtype=torch.float64, device=dev)
+    stats = lbx.gn_stats_buffer(b)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     if a.op in ("conv", "subpix", "gemm"):

@@ -34,7 +34,7 @@ def main():
         y = torch.empty_like(x)
         w = (torch.randn(c, K, device=dev) * K ** -0.5).half()
         bias = torch.randn(c, device=dev)
-        st = torch.zeros(b, 32, 2, dtype=torch.float64, device=dev)
+        st = lbx.gn_stats_buffer(b)
         gam, bet = torch.ones(c, device=dev), torch.zeros(c, device=dev)
         halves.append((x, y, w, bias, st, gam, bet))
     streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]

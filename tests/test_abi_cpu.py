@@ -32,6 +32,17 @@ def test_library_exports_every_declared_symbol(lbx):
     assert set(lbx.SYMBOLS) <= declared | {"lbx_batcher_create"}
 
 
+def test_library_exports_only_the_c_abi(lbx):
+    """Hidden visibility: the dynamic symbol table holds exactly the LBX_API functions of the headers,
+    no C++ internals (which could interpose on, or be interposed by, a host program's symbols)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", lbx.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    funcs = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert not [f for f in funcs if f.startswith("_Z")], sorted(f for f in funcs if f.startswith("_Z"))[:5]
+    assert funcs == _declared_symbols(), sorted(funcs ^ _declared_symbols())
+
+
 def test_header_compiles_as_c(tmp_path):
     src = tmp_path / "t.c"
     src.write_text('#include "lbx/reconstruct.h"\nint main(void){ lbx_decoder_desc d; (void)d; return 0; }\n')

@@ -61,3 +61,25 @@ def test_c5_full_workload_sim(c5):
     assert 0.5 < mix["image_hit"] < 0.9 and 0.1 < mix["full_miss"] < 0.35
     s = d["sim"]
     assert 0 < s["decode_p50_ms"] <= s["decode_p99_ms"] and s["decodes"] > 1_000_000
+
+
+def _ref_binding():
+    p = os.path.join(ROOT, "oracle", "_ref", "ref_binding")
+    if not os.path.exists(p):
+        pytest.skip("oracle/_ref/ref_binding not built (needs /root/reference at build time)")
+    return p
+
+
+def test_reference_binding_runs_reference_simulator():
+    """tools/ref_binding.cpp, compiled against the reference's own sources: the reference simulator
+    (lbx::run) with LatencyModel::decode_ms swapped for a given decode time; fewer ms of decode
+    means a lower tail; the outcome mix moves only through the split tuner (it observes T_decode)."""
+    import json
+    import subprocess
+    out = subprocess.run([_ref_binding(), "--decode-ms", "9.0", "--requests-per-day", "50000", "--days", "4"],
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+    stock, ours = lines[1], lines[2]
+    assert stock["decode_ms"] == 40.0 and ours["decode_ms"] == 9.0
+    assert ours["e2e_p99_ms"] <= stock["e2e_p99_ms"] and ours["stage_decode_ms"] < stock["stage_decode_ms"]
+    assert abs(ours["frac_full_miss"] - stock["frac_full_miss"]) < 0.01  # the tuner sees the new T_decode

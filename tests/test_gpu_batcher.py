@@ -192,3 +192,84 @@ def test_graph_cache_keyed_by_batch_size_only(lbx):
     assert dec.graph_captures() == base
     got = rgb_big[256 * 99:256 * 99 + rgb_bytes].cpu().numpy().reshape(ref.shape)
     assert np.array_equal(got, ref)
+
+
+def _device_blobs(lbx, blobs, device):
+    """LBLP blobs copied into one GPU buffer (an HBM latent tier): [(ptr, nbytes)], the tensor."""
+    import torch
+    offs, total = [], 0
+    for b in blobs:
+        offs.append(total)
+        total += (len(b) + 255) // 256 * 256
+    buf = torch.zeros(total, dtype=torch.uint8)
+    for o, b in zip(offs, blobs):
+        buf[o:o + len(b)] = torch.frombuffer(bytearray(b), dtype=torch.uint8)
+    dbuf = buf.to(f"cuda:{device}")
+    torch.cuda.synchronize()
+    return [(dbuf.data_ptr() + o, len(b)) for o, b in zip(offs, blobs)], dbuf
+
+
+def test_batcher_device_resident_blobs(lbx):
+    """Blobs resident in HBM (lbx_batcher_submit_device), mixed with host blobs in the same queue:
+    pixels equal a direct decode; no spill on one GPU (every worker is local to the blobs)."""
+    n = 10
+    z = weights_ref.make_latents("sd3", n, 64, 64, seed=45)
+    blobs = [lbx.pack(z[i], 1) for i in range(n)]
+    ref = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=n).reconstruct(blobs)
+    dev_blobs, keep = _device_blobs(lbx, blobs, 0)
+    b = lbx.Batcher([0, 0], [("sd3", 64, 64)], max_batch=3, max_wait_us=0)
+    outs = [np.zeros((512, 512, 3), dtype=np.uint8) for _ in range(n)]
+    for i in range(n):
+        if i % 3 == 0:
+            b.submit(i, 0, blobs[i], outs[i])
+        else:
+            b.submit_device(i, 0, dev_blobs[i][0], dev_blobs[i][1], 0, outs[i], keep=keep)
+    done = _drain(b, n)
+    assert sorted(c["id"] for c in done) == list(range(n)) and all(c["status"] == 0 for c in done)
+    for i in range(n):
+        assert np.array_equal(outs[i], ref[i]), i
+    st = b.stats()
+    assert st["spills"] == 0 and st["peer_copies"] == 0
+    b.close()
+
+
+def test_batcher_nvlink_spill_two_gpus(lbx):
+    """Blobs resident on GPU 1 decoded by workers on GPUs 0 and 1: the GPU-0 worker fetches its
+    blobs over NVLink (peer copy); pixels equal a direct decode.  Needs two GPUs."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    n = 16
+    z = weights_ref.make_latents("sd3", n, 64, 64, seed=46)
+    blobs = [lbx.pack(z[i], 1) for i in range(n)]
+    ref = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=n).reconstruct(blobs)
+    dev_blobs, keep = _device_blobs(lbx, blobs, 1)
+    b = lbx.Batcher([0, 1], [("sd3", 64, 64)], max_batch=1, max_wait_us=0)
+    outs = [np.zeros((512, 512, 3), dtype=np.uint8) for _ in range(n)]
+    for i in range(n):
+        b.submit_device(i, 0, dev_blobs[i][0], dev_blobs[i][1], 1, outs[i], keep=keep)
+    done = _drain(b, n)
+    assert sorted(c["id"] for c in done) == list(range(n)) and all(c["status"] == 0 for c in done)
+    for i in range(n):
+        assert np.array_equal(outs[i], ref[i]), i
+    st = b.stats()
+    spilled = sum(1 for c in done if c["device"] == 0)
+    assert st["spills"] == spilled == st["peer_copies"]
+    b.close()
+
+
+def test_reference_binding_with_measured_decode(lbx):
+    """tools/ref_binding (reference simulator sources + liblbx.so): the decode the reference models
+    as 40 ms is measured through lbx_reconstruct on this GPU and fed to the reference's lbx::run."""
+    import json
+    import os
+    import subprocess
+    p = os.path.join(os.path.dirname(lbx.LIB_PATH), "..", "oracle", "_ref", "ref_binding")
+    if not os.path.exists(p):
+        pytest.skip("oracle/_ref/ref_binding not built")
+    out = subprocess.run([p, "--requests-per-day", "50000", "--days", "4"], capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    print(out)
+    lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+    assert lines[0]["decode_measured"] is True
+    assert 2.0 < lines[2]["decode_ms"] < 40.0
