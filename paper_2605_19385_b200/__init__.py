@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblbx.so")
+LIB_PATH = os.environ.get("LBX_LIB") or os.path.join(_HERE, "liblbx.so")  # LBX_LIB: A/B of two builds
 
 FAMILY = {"sd15": 0, "sd3": 1, "flux": 2}
 LATENT_CHANNELS = {"sd15": 4, "sd3": 16, "flux": 16}

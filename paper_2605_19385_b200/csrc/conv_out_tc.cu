@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(kCoThreads, 1)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const float2 v = p.ss[(size_t)img * 128 + c0 + k];
-          a[k] = v.x;
-          b[k] = v.y;
+          a[k] = H2 ? 0.5f * v.x : v.x;  // H2: halved for gn_silu8_h2_half
+          b[k] = H2 ? 0.5f * v.y : v.y;
         }
       }
       for (int r = 0; r < rows_in; ++r, ++gi) {
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(kCoThreads, 1)
           for (int k = 0; k < NK; ++k) {
             const int px = p0 + 16 * k;
             if (ok[k])
-              ptx::sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_act8_h2<true>(v[k], a, b) : gn_act8<true>(v[k], a, b));
+              ptx::sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_silu8_h2_half(v[k], a, b) : gn_act8<true>(v[k], a, b));
           }
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         }

@@ -466,8 +466,8 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
           const float4* cp = reinterpret_cast<const float4*>(p.gn_ss + (size_t)img * p.cblocks * 64 + j * 64 + cq * 8);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float4 v = __ldg(cp + k);
-            ca[2 * k] = v.x; cb[2 * k] = v.y; ca[2 * k + 1] = v.z; cb[2 * k + 1] = v.w;
+            const float4 v = __ldg(cp + k);  // halved for gn_silu8_h2_half
+            ca[2 * k] = 0.5f * v.x; cb[2 * k] = 0.5f * v.y; ca[2 * k + 1] = 0.5f * v.z; cb[2 * k + 1] = 0.5f * v.w;
           }
         }
         ptx::mbar_wait(&a_full[st], ph);
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
               }
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                const uint4 w = gn_act8_h2<true>(u[k], ca, cb);
+                const uint4 w = gn_silu8_h2_half(u[k], ca, cb);
                 if (v[k]) ptx::sts128(q[k], w);
               }
               px += 64;

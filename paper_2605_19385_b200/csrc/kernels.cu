@@ -114,10 +114,10 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float2 t = site_affine(g, img, cvec * 8 + k, CV / 4);
-      a[k] = t.x;
-      b[k] = t.y;
+      a[k] = (SILU && H2) ? 0.5f * t.x : t.x;  // halved for gn_silu8_h2_half
+      b[k] = (SILU && H2) ? 0.5f * t.y : t.y;
     }
-    auto apply = [&](uint4 u) { return H2 ? gn_act8_h2<SILU>(u, a, b) : gn_act8<SILU>(u, a, b); };
+    auto apply = [&](uint4 u) { return (SILU && H2) ? gn_silu8_h2_half(u, a, b) : gn_act8<SILU>(u, a, b); };
     constexpr int U = 8;  // 16-byte loads in flight per thread (latency x bandwidth needs ~100 KB/SM)
     for (; p + (U - 1) * PSTEP < seg_end; p += U * PSTEP) {
       uint4 u[U];
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float2 t = site_affine(g, img, cvec * 8 + j, CV / 4);
-        a[j] = t.x;
-        b[j] = t.y;
+        a[j] = (SILU && H2) ? 0.5f * t.x : t.x;  // halved for gn_silu8_h2_half
+        b[j] = (SILU && H2) ? 0.5f * t.y : t.y;
       }
     }
     ptx::mbar_wait(&full[st], (uint32_t)((k / kApStages) & 1));
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
 #pragma unroll
     for (int i = 0; i < kApChunk / 16 / 256; ++i) {
       const uint4 u = q[tid + 256 * i];
-      q[tid + 256 * i] = H2 ? gn_act8_h2<SILU>(u, a, b) : gn_act8<SILU>(u, a, b);
+      q[tid + 256 * i] = (SILU && H2) ? gn_silu8_h2_half(u, a, b) : gn_act8<SILU>(u, a, b);
     }
     ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     __syncthreads();
