@@ -15,14 +15,15 @@
  *   0      4     magic "LBLP"
  *   4      1     version            = 1
  *   5      1     dtype              = 1 (IEEE fp16 latent values)
- *   6      1     mode               0 raw | 1 lossless | 2 q8
+ *   6      1     mode               0 raw | 1 lossless | 2 q8 | 3 entropy (lossless)
  *   7      1     flags              = 0
  *   8      2     C
  *   10     2     H
  *   12     2     W
  *   14     2     reserved           = 0
  *   16     4     total_bytes        size of the whole blob
- *   20     4     table_offset       mode 1: row table; mode 2: channel params; mode 0: 0
+ *   20     4     table_offset       mode 1: row table; mode 2: channel params; mode 3: plane table;
+ *                                      mode 0: 0
  *   24     4     payload_offset
  *   28     4     reserved           = 0
  *
@@ -43,6 +44,39 @@
  *   table_offset = 32: float32 scale[C], then int32 zero_point[C].  payload_offset = 32 + 8*C.
  *   payload = int8 q[C*H*W] NCHW.  Decode (fixed operation order, no FMA contraction):
  *     x = fp16_rn( fp32_rn( (float)(q - zero_point[c]) * scale[c] ) )
+ *
+ * mode 3 (entropy, lossless): the algorithm class of pcodec -- values mapped to
+ * order-preserving integers, optional delta, binned and entropy-coded, low bits raw -- laid out
+ * for one-thread-per-column GPU decode.  NOT the pcodec wire format (no pco implementation or
+ * spec exists in this build environment to pin one against).  W % 32 == 0, W <= 1024.
+ *   table_offset = 32: uint32 plane_off[C], byte offset of plane c relative to payload_offset,
+ *   multiple of 4.  payload_offset = 32 + 4*C.
+ *   Plane (H rows x W columns of channel c), all offsets below relative to the plane start:
+ *     0   uint8  delta   0: s = omap(bits); 1: s = zigzag16(omap(bits[y][x]) - omap(bits[y-1][x]))
+ *                        (mod 2^16, row -1 reads as 0) -- differences down each column
+ *     1   uint8  L       = 12 (rANS table size M = 2^L)
+ *     2   uint8  b       raw low bits per value, 0..16
+ *     3   uint8  0
+ *     4   uint16 K       bins, 1..256
+ *     6   uint16 0
+ *     8   uint32 raw_pos start of the raw low bits (multiple of 4)
+ *     12  uint32 0
+ *     16  K x {uint16 hi, uint16 freq}: bin k holds the symbols [hi << b, (hi+1) << b); hi strictly
+ *         increasing, hi < 2^(16-b); freq >= 1, sum = M; cum[k] = freq[0] + ... + freq[k-1].
+ *     then (padded to 4) uint32 state[W]: each column's initial rANS decoder state, in [2^16, 2^32)
+ *     then uint32 warp_off[W/32]: start of warp g's (columns 32g..32g+31) renormalisation words,
+ *         multiple of 4; the words run to the next warp's start (the last: to raw_pos)
+ *     then the word sequences (uint16), each padded to 4 bytes
+ *     raw_pos: W x ceil(H*b/32) uint32, column x's words at x*ceil(H*b/32)*4: value y's low b bits at
+ *         bit y*b, LSB-first across the words.
+ *   Decode: for y = 0..H-1, for each warp g, for lanes l = 0..31 in order (column x = 32g + l):
+ *     slot = st & (M-1); k = the bin with cum[k] <= slot < cum[k] + freq[k];
+ *     st = freq[k] * (st >> L) + slot - cum[k];  if st < 2^16: st = (st << 16) | next word of warp g;
+ *     s = (hi[k] << b) | low_bits(x, y);  v = delta ? v_prev(x) + unzigzag16(s) : s;  bits = omap^-1(v)
+ *   The encoder (rANS over the column, symbols in reverse) tries delta 0 and 1 and keeps the shorter
+ *   plane (ties: 0); b is the smallest value that leaves <= 256 occupied bins; freq = max(1,
+ *   floor(count * M / (H*W))), then +1 (while the sum is short) or -1 (where > 1, while over) cycling
+ *   through the bins in (count desc, hi asc) order.
  */
 #ifndef LBX_LBLP_H
 #define LBX_LBLP_H
@@ -54,7 +88,7 @@
 #define LBLP_DTYPE_F16 1
 #define LBLP_HEADER_BYTES 32
 
-enum lblp_mode { LBLP_RAW = 0, LBLP_LOSSLESS = 1, LBLP_Q8 = 2 };
+enum lblp_mode { LBLP_RAW = 0, LBLP_LOSSLESS = 1, LBLP_Q8 = 2, LBLP_ENTROPY = 3 };
 
 typedef struct lblp_header {
   char magic[4];

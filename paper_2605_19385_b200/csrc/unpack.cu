@@ -242,6 +242,111 @@ __device__ __forceinline__ void ubulk_load(void* dst, const void* src, uint32_t 
                : "memory");
 }
 
+// ---------------------------------------------------------------- mode 3 (binned rANS, lblp.h)
+// One plane per CTA: the decode warps build the slot -> bin table in shared memory (in the plane's
+// unused staging buffer), then thread t decodes columns t, t + 256, ...: per row one rANS step
+// (the warp's renormalisation words are consumed in lane order: ballot + popc), the raw low bits
+// from the column's own bit stream, the inverse delta down the column; row y's values of a warp are
+// 32 consecutive halves (coalesced stores).
+constexpr uint32_t kEntL = 12, kEntM = 1u << kEntL;
+__device__ __forceinline__ void ent_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kPlaneThreads) : "memory"); }
+
+// Returns 0 or an error code (4) -- uniform over the decode threads; on an error the caller zeroes
+// the plane.  pl / plen: the plane's bytes (global); smem: >= 4096 + 256 * 8 bytes.  s_bad: the
+// slot's error flag (per ring slot, so a fast thread resetting it for its next plane cannot race a
+// slow thread still reading it for this one: the slot is refilled only after every warp is done).
+__device__ int decode_entropy_plane(const uint8_t* pl, uint32_t plen, int H, int W, int t, int lane, uint8_t* smem,
+                                    uint16_t* dst, int& s_bad) {
+  uint8_t* slot2k = smem;                                          // [4096]
+  uint32_t* bins = reinterpret_cast<uint32_t*>(smem + kEntM);     // [256]: hi | f << 16
+  uint32_t* cums = bins + 256;                                     // [256]
+  const int delta = pl[0], Lb = pl[1], b = pl[2], K = ld_u16(pl + 4);
+  const uint32_t raw = ld_u32(pl + 8);
+  const uint32_t hdr = (16u + 4u * (uint32_t)K + 3u) & ~3u;
+  const uint32_t nwo = (uint32_t)(((uint64_t)H * b + 31) / 32);
+  bool bad = delta > 1 || Lb != (int)kEntL || b > 16 || K < 1 || K > 256 || (raw & 3u) ||
+             (uint64_t)hdr + 4ull * W + 4ull * (W / 32) > raw || (uint64_t)raw + 4ull * nwo * W > plen;
+  if (t == 0) s_bad = 0;
+  ent_bar();
+  if (!bad && t < K) {
+    const uint32_t v = ld_u32(pl + 16 + 4 * t);
+    const uint32_t hv = v & 0xFFFFu, fv = v >> 16;
+    bins[t] = v;
+    if (fv == 0 || (hv >> (16 - b))) bad = true;
+    if (t && hv <= (ld_u32(pl + 12 + 4 * t) & 0xFFFFu)) bad = true;
+  }
+  if (bad) s_bad = 1;
+  ent_bar();
+  if (s_bad) return 4;
+  if (t < K) {  // exclusive prefix of the frequencies (K <= 256: a short sequential sum per bin)
+    uint32_t c = 0;
+    for (int k = 0; k < t; ++k) c += bins[k] >> 16;
+    cums[t] = c;
+    if (t == K - 1 && c + (bins[t] >> 16) != kEntM) s_bad = 1;
+  }
+  ent_bar();
+  if (s_bad) return 4;
+  for (uint32_t sl = (uint32_t)t; sl < kEntM; sl += kPlaneThreads) {  // slot -> bin: binary search
+    int lo = 0, hi = K - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cums[mid] <= sl) lo = mid; else hi = mid - 1;
+    }
+    slot2k[sl] = (uint8_t)lo;
+  }
+  ent_bar();
+  const uint32_t* states = reinterpret_cast<const uint32_t*>(pl + hdr);
+  const uint32_t* woff = states + W;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t bmask = b ? ((1u << b) - 1u) : 0u;
+  int err = 0;
+  for (int x = t; x < W; x += kPlaneThreads) {  // warp-uniform: W % 32 == 0
+    const int g = x >> 5;
+    const uint32_t ws = woff[g], we = g + 1 < W / 32 ? woff[g + 1] : raw;
+    const bool wbad = (ws & 3u) || ws < hdr + 4u * W + 4u * (W / 32) || we > raw || ws > we;
+    const uint32_t nw = wbad ? 0u : (we - ws) / 2;
+    const uint16_t* words = reinterpret_cast<const uint16_t*>(pl + ws);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(pl + raw) + (size_t)nwo * x;
+    uint32_t st = states[x], wi = 0, prev = 0, rwi = 0;
+    uint64_t rbuf = 0;
+    uint32_t rfill = 0;
+    bool cbad = wbad;
+    for (int y = 0; y < H; ++y) {
+      const uint32_t sl = st & (kEntM - 1);
+      const int k = slot2k[sl];
+      const uint32_t bv = bins[k];
+      st = (bv >> 16) * (st >> kEntL) + sl - cums[k];
+      const bool need = st < (1u << 16);
+      const uint32_t m = __ballot_sync(0xffffffffu, need);
+      if (need) {
+        const uint32_t pos = wi + __popc(m & lt);
+        if (pos < nw) st = (st << 16) | words[pos];
+        else cbad = true;
+      }
+      wi += __popc(m);
+      uint32_t o = 0;
+      if (b) {
+        if (rfill < (uint32_t)b) {
+          rbuf |= (uint64_t)(rwi < nwo ? rw[rwi] : 0u) << rfill;
+          ++rwi;
+          rfill += 32;
+        }
+        o = (uint32_t)rbuf & bmask;
+        rbuf >>= b;
+        rfill -= b;
+      }
+      const uint32_t s = (b == 16 ? 0u : ((bv & 0xFFFFu) << b)) | o;
+      const uint32_t u = delta ? ((prev + ((s >> 1) ^ (uint32_t)(-(int)(s & 1)))) & 0xFFFFu) : s;
+      prev = u;
+      dst[(size_t)y * W + x] = omap_inv((uint16_t)u);
+    }
+    if (cbad) err = 4;
+  }
+  if (err) s_bad = 1;
+  ent_bar();
+  return s_bad ? 4 : 0;
+}
+
 struct PlaneInfo {
   int code, mode;
   uint32_t start, bytes;  // mode 1: the plane's canonical byte range (bytes = 0: rows from global)
@@ -282,6 +387,15 @@ __device__ void plane_prep(const uint8_t* base, uint32_t nbytes, bool aligned16,
         bytes = (aligned16 && r1 > r0 && (r0 & 3) == 0 && (r1 & 3) == 0 && r1 - r0 <= (uint32_t)kPlaneInBytes &&
                  (unsigned long long)payload + r1 <= nbytes) ? r1 - r0 : 0u;
       }
+    } else if (mode == 3) {
+      if ((W & 31) || W > 1024 || table != 32 || payload != 32u + 4u * (uint32_t)C || payload > nbytes) {
+        code = 4;
+      } else {  // the plane's byte range; the decode warps validate its contents
+        const uint32_t p0 = ld_u32(base + 32 + 4 * c);
+        const uint32_t p1 = c + 1 < C ? ld_u32(base + 32 + 4 * (c + 1)) : nbytes - payload;
+        if ((p0 & 3) || p1 > nbytes - payload || (unsigned long long)p0 + 16 > p1) code = 4;
+        else { start = payload + p0; bytes = p1 - p0; }
+      }
     } else {
       code = 5;
     }
@@ -306,6 +420,7 @@ __global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kerne
   uint8_t* s_in[2] = {s_dyn, s_dyn + kBuf};
   __shared__ PlaneInfo s_pi[2];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+  __shared__ int s_ent_bad[2];  // mode-3 error flag per ring slot
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long long planes = (long long)n * C;
   const int vals = H * W;
@@ -401,6 +516,12 @@ __global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kerne
           deq4(__ldg(q + i), o.x, o.y);
           d64[i] = o;
         }
+      }
+    } else if (pi.mode == 3) {
+      const int code = decode_entropy_plane(base + pi.start, pi.bytes, H, W, t, lane, s_in[b], dst, s_ent_bad[b]);
+      if (code) {
+        for (int i = t; i < vals; i += kPlaneThreads) dst[i] = 0;
+        if (t == 0) atomicExch(err, code);
       }
     } else {  // mode 1 from the staged copy
       const uint8_t* sb = s_in[b] + (pi.start - pi.lo);  // the plane's first byte

@@ -45,7 +45,7 @@ def kat():
     x[1, 1] = rng.integers(0, 65536, 64, dtype=np.uint16)
     y = rng.standard_normal((2, 4, 32)).astype(np.float16).view(np.uint16)
     for name, arr in (("mixed_2x2x64", x), ("normal_2x4x32", y)):
-        for mode in (0, 1, 2):
+        for mode in (0, 1, 2, 3):
             if mode == 2 and name == "mixed_2x2x64":
                 continue  # q8 of inf/NaN is saturating by design; KAT uses finite data
             blob = lblp.encode(arr.view(np.float16), mode)

@@ -31,7 +31,7 @@ def _latents_with_specials(seed):
     return z.view(np.float16)
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_unpack_bit_exact_vs_oracle(lbx, mode):
     z = _latents_with_specials(21)
     if mode == 2:  # q8 is lossy: specials would blow the per-channel range; use finite data
@@ -41,11 +41,11 @@ def test_unpack_bit_exact_vs_oracle(lbx, mode):
     got = _gpu_unpack(lbx, dec, blobs)
     ref = np.stack([lblp.decode(b, 16, 64, 64).view(np.uint16) for b in blobs])
     assert np.array_equal(got, ref)
-    if mode in (0, 1):
+    if mode in (0, 1, 3):
         assert np.array_equal(got, z.view(np.uint16))  # lossless round trip
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_unpack_product_packer_blobs(lbx, mode):
     """Product packer (lbx_pack) -> GPU unpack == oracle decode of the same bytes, at config-3 shape."""
     z = weights_ref.make_latents("sd3", 4, 128, 128, seed=3, smooth=True)
@@ -173,3 +173,52 @@ def test_noncanonical_row_order_decodes(lbx):
     got = lat.cpu().numpy()
     assert np.array_equal(got[0].view(np.int16), z.view(np.int16))
     assert np.array_equal(got[1].view(np.int16), z.view(np.int16))
+
+
+@pytest.mark.parametrize("fam,c,h,w,n", [("sd3", 16, 128, 128, 8), ("sd15", 4, 64, 64, 3)])
+def test_entropy_mode_decode_and_reconstruct(lbx, fam, c, h, w, n):
+    """LBLP mode 3 (binned rANS, one GPU thread per column) at the decoder shapes: GPU unpack is
+    bit-exact with the oracle and with the latents, and lbx_reconstruct from mode-3 blobs equals the
+    same decode from mode-1 blobs."""
+    z = weights_ref.make_latents(fam, n, h, w, seed=41, smooth=True)
+    z[0, 0, 0, :16] = SPECIAL.view(np.float16)
+    dec = lbx.Decoder(fam, (h, w), seed=0, max_batch=n)
+    blobs = [lbx.pack(z[i], 3) for i in range(n)]
+    got = _gpu_unpack(lbx, dec, blobs)
+    assert np.array_equal(got, np.stack([lblp.decode(b, c, h, w).view(np.uint16) for b in blobs]))
+    assert np.array_equal(got, z.view(np.uint16))
+    zf = weights_ref.make_latents(fam, n, h, w, seed=43, smooth=True)  # finite values for the decode
+    assert np.array_equal(dec.reconstruct([lbx.pack(zf[i], 3) for i in range(n)]),
+                          dec.reconstruct([lbx.pack(zf[i], 1) for i in range(n)]))
+
+
+def test_entropy_mode_malformed(lbx):
+    """Structural damage to a mode-3 blob is LBX_E_FORMAT (host validation), and the device decoder
+    flags the same damage on HBM-resident blobs (lbx_op_unpack err word) without faulting."""
+    import struct
+    import torch
+    z = weights_ref.make_latents("sd3", 1, 64, 64, seed=42)
+    good = lbx.pack(z[0], 3)
+    payload = struct.unpack_from("<I", good, 24)[0]
+    plane0 = payload + struct.unpack_from("<I", good, 32)[0]
+    bad = bytearray(good)
+    struct.pack_into("<H", bad, plane0 + 18, struct.unpack_from("<H", good, plane0 + 18)[0] + 1)  # freq sum != 4096
+    dec = lbx.Decoder("sd3", (64, 64), seed=0, max_batch=2)
+    with pytest.raises(lbx.LbxError) as e:
+        dec.reconstruct([bytes(bad)])
+    assert e.value.status == lbx.E_FORMAT
+    dev = torch.device("cuda")
+    stride = (len(good) + 255) // 256 * 256
+    buf = torch.zeros(2 * stride, dtype=torch.uint8)
+    buf[:len(good)] = torch.frombuffer(bytearray(good), dtype=torch.uint8)
+    buf[stride:stride + len(bad)] = torch.frombuffer(bad, dtype=torch.uint8)
+    bd = buf.to(dev)
+    offs = torch.tensor([0, stride], dtype=torch.int64, device=dev)
+    sizes = torch.tensor([len(good), len(bad)], dtype=torch.int32, device=dev)
+    out = torch.empty((2, 16, 64, 64), dtype=torch.float16, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    lbx.op_unpack(bd.data_ptr(), offs.data_ptr(), sizes.data_ptr(), 2, 16, 64, 64, out.data_ptr(), err.data_ptr())
+    torch.cuda.synchronize()
+    assert int(err.item()) == 4
+    assert np.array_equal(out[0].cpu().numpy().view(np.uint16), z[0].view(np.uint16))  # the good blob still decodes
+    assert dec.reconstruct([good]).shape == (1, 512, 512, 3)  # and the decoder stays usable

@@ -44,11 +44,12 @@ def test_lblp_known_answer_vectors():
         assert lblp.encode(vals.view(np.float16), c["mode"]) == blob, c["name"]
         dec = lblp.decode(blob, *c["shape"]).view(np.uint16)
         assert dec.tobytes().hex() == c["decoded_hex"], c["name"]
-        if c["mode"] in (0, 1):
+        if c["mode"] in (0, 1, 3):
             assert np.array_equal(dec, vals)
+    assert {c["mode"] for c in kat["cases"]} == {0, 1, 2, 3}
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 @pytest.mark.parametrize("shape,smooth", [((4, 64, 64), False), ((16, 128, 128), True), ((2, 3, 32), False)])
 def test_product_packer_bytes_equal_oracle_encoder(lbx, mode, shape, smooth):
     c, h, w = shape
@@ -65,10 +66,14 @@ def test_product_packer_special_values(lbx):
                         0x7E00, 0x7C01, 0xFE01, 0x3C00, 0xBC00], dtype=np.uint16)
     z = np.resize(special, (3, 4, 64)).astype(np.uint16)
     z[1] = np.random.default_rng(5).integers(0, 65536, (4, 64), dtype=np.uint16)  # arbitrary bit patterns
-    for mode in (0, 1):
+    for mode in (0, 1, 3):
         b = lbx.pack(z.view(np.float16), mode)
         assert b == lblp.encode(z.view(np.float16), mode)
         assert np.array_equal(lblp.decode(b, 3, 4, 64).view(np.uint16), z)
+    const = np.full((2, 8, 32), 0x3C00, dtype=np.uint16)  # one bin, zero-cost symbols, no renormalisation
+    b = lbx.pack(const.view(np.float16), 3)
+    assert b == lblp.encode(const.view(np.float16), 3)
+    assert np.array_equal(lblp.decode(b, 2, 8, 32).view(np.uint16), const)
 
 
 def test_packer_rejects_bad_arguments(lbx):
@@ -77,6 +82,10 @@ def test_packer_rejects_bad_arguments(lbx):
     assert e.value.status == lbx.E_CONFIG
     with pytest.raises(lbx.LbxError):
         lbx.pack(np.zeros((2, 4, 64), dtype=np.float16), 7)
+    with pytest.raises(lbx.LbxError):
+        lbx.pack(np.zeros((1, 4, 48), dtype=np.float16), 3)  # mode 3: W % 32 != 0
+    with pytest.raises(lbx.LbxError):
+        lbx.pack(np.zeros((1, 256, 128), dtype=np.float16), 3)  # mode 3: plane > 16384 values
 
 
 def test_oracle_decoder_reproduces_config1_golden():
@@ -116,3 +125,15 @@ def test_oracle_pinned_to_independent_decoder(fixture):
     rep = json.load(open(os.path.join(GOLD, "pin_cheers.json")))
     case = next(c for c in rep["cases"] if c["fixture"] == fixture)
     assert case["cheers_params"] == case["oracle_params"] and case["max_abs_float_diff"] <= 2e-5
+
+
+@pytest.mark.parametrize("smooth", [False, True])
+def test_entropy_mode_roundtrip_and_ratio(lbx, smooth):
+    """LBLP mode 3 (binned rANS, the pcodec algorithm class): lossless, and smaller than mode 1 --
+    16x128x128 N(0,1) latents at < 0.9 of raw fp16 (order-0 entropy 0.84), smooth ones < 0.8."""
+    z = weights_ref.make_latents("sd3", 1, 128, 128, seed=3, smooth=smooth)[0]
+    b = lbx.pack(z, 3)
+    assert b == lblp.encode(z, 3)
+    assert np.array_equal(lblp.decode(b, 16, 128, 128).view(np.uint16), z.view(np.uint16))
+    assert len(b) < len(lbx.pack(z, 1))
+    assert len(b) / z.nbytes < (0.80 if smooth else 0.90)
