@@ -470,7 +470,12 @@ def main():
     from paper_2605_19385_b200.dist import launch_plan, spawn_argv
 
     try:
-        plan = launch_plan(args.gpus, dict(os.environ), torch.cuda.device_count() if args.impl == "ours" else args.gpus)
+        # LBX_BENCH_SHARE_GPU=1 (diagnostics only): let N ranks share the visible GPUs so the N-rank
+        # path can be exercised on a 1-GPU box; its numbers are not an N-GPU measurement
+        visible = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+        if os.environ.get("LBX_BENCH_SHARE_GPU") == "1" and visible > 0:
+            visible = max(visible, args.gpus)
+        plan = launch_plan(args.gpus, dict(os.environ), visible)
     except ValueError as e:
         print(f"bench.py: {e}", file=sys.stderr, flush=True)
         return 2
@@ -491,10 +496,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = os.environ.get("LBX_BENCH_SHARE_GPU") == "1" and world > torch.cuda.device_count()
+    if shared:  # diagnostics: ranks share GPUs (NCCL needs one GPU per rank: gloo instead)
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     if args.config == 0:
         args.config = 2 if world == 1 else 4  # N > 1: BASELINE configs[3], sharded whole requests
@@ -671,9 +682,10 @@ def main():
     # through one batcher driving all N GPUs of the box at 25x per GPU.
     latency = None
     barrier()
-    spill = leg_peer_spill(torch, world) if rank == 0 else None
+    spill = leg_peer_spill(torch, world) if rank == 0 and not shared else None
     if rank == 0 and not args.no_latency:
-        latency = c5_latency(local, scale=25 * world, devices=world)
+        ndev = min(world, torch.cuda.device_count())
+        latency = c5_latency(local, scale=25 * ndev, devices=ndev)
     barrier()
 
     if rank == 0:
@@ -685,7 +697,9 @@ def main():
             "config": {"workload": name, "family": fam, "latent": [c, 128, 128], "batch_per_gpu": batch,
                        "global_batch": batch * world, "output": "1024x1024x3 uint8",
                        "l2": "no flush: per-step working set ~40 GB of activations >> 126 MB L2",
-                       "parallelism": f"dp{world} (whole-request sharding, no collective)"},
+                       "parallelism": f"dp{world} (whole-request sharding, no collective)"
+                                      + (" [LBX_BENCH_SHARE_GPU: ranks shared GPUs -- diagnostics, not an N-GPU number]"
+                                         if shared else "")},
             "per_rank_img_s": [round(v, 2) for v in per_rank],
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,

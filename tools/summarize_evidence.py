@@ -52,8 +52,8 @@ def launches(tag):
         g[1] += us
     tot = sum(v[1] for v in agg.values())
     n = sum(v[0] for v in agg.values())
-    lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none: every launch of bench.py --batch 4 "
-             "--steps 1 --warmup 1 (2 decodes + profile)",
+    lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none: every launch of a short bench run "
+             "(scripts/gpu_round.sh: config 2, batch 32, --steps 1 --warmup 1: 2 decodes + the eager profile)",
              "# cold-cache, serialised: compare SHARES with the step profile, not absolutes",
              f"# launches {n}, total {tot / 1e3:.1f} ms", "share\tlaunches\ttotal_us\tkernel"]
     for k, (c, us) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
@@ -101,7 +101,8 @@ def main(tag):
     json.dump(b, open(os.path.join(P, f"{tag}_bench.json"), "w"), indent=1)
     step_profile(tag)
     launches(tag)
-    ncu_dom(tag)
+    if os.path.exists(os.path.join(G, f"dom_{tag}.ncu-rep")):
+        ncu_dom(tag)
     print("wrote profiles/ for", tag)
 
 
