@@ -349,6 +349,7 @@ __device__ int decode_entropy_plane(const uint8_t* pl, uint32_t plen, int H, int
 
 struct PlaneInfo {
   int code, mode;
+  uint32_t plen;          // mode 3: the plane's length (its bytes start at `start`)
   uint32_t start, bytes;  // mode 1: the plane's canonical byte range (bytes = 0: rows from global)
   uint32_t payload, nbytes;
   uint32_t lo;            // staged copy of [lo, start + bytes) at the buffer's base (lo = start & ~15)
@@ -359,7 +360,7 @@ struct PlaneInfo {
 __device__ void plane_prep(const uint8_t* base, uint32_t nbytes, bool aligned16, int c, int C, int H, int W,
                            PlaneInfo& pi, uint8_t* buf, uint64_t* bar) {
   int code = 0, mode = -1;
-  uint32_t start = 0, bytes = 0, table = 0, payload = 0;
+  uint32_t start = 0, bytes = 0, table = 0, payload = 0, plen = 0;
   if (nbytes < 32 || base[0] != 'L' || base[1] != 'B' || base[2] != 'L' || base[3] != 'P' || base[4] != 1 ||
       base[5] != 1)
     code = 2;
@@ -394,16 +395,21 @@ __device__ void plane_prep(const uint8_t* base, uint32_t nbytes, bool aligned16,
         const uint32_t p0 = ld_u32(base + 32 + 4 * c);
         const uint32_t p1 = c + 1 < C ? ld_u32(base + 32 + 4 * (c + 1)) : nbytes - payload;
         if ((p0 & 3) || p1 > nbytes - payload || (unsigned long long)p0 + 16 > p1) code = 4;
-        else { start = payload + p0; bytes = p1 - p0; }
+        else {
+          start = payload + p0;
+          plen = p1 - p0;  // staged into shared memory like a mode-1 plane when it fits
+          bytes = (aligned16 && plen <= (uint32_t)kPlaneInBytes) ? plen : 0u;
+        }
       }
     } else {
       code = 5;
     }
   }
   pi.code = code; pi.mode = mode; pi.start = start; pi.bytes = bytes; pi.payload = payload; pi.nbytes = nbytes;
+  pi.plen = plen;
   pi.use_bar = 0;
   pi.lo = start & ~15u;
-  if (!code && mode == 1 && bytes) {
+  if (!code && (mode == 1 || mode == 3) && bytes) {
     const uint32_t end = start + bytes, hi = end & ~15u;  // [lo, hi) by TMA (the caller), [hi, end) here
     for (uint32_t o = hi > pi.lo ? hi : pi.lo; o < end; o += 4)
       *reinterpret_cast<uint32_t*>(buf + (o - pi.lo)) = ld_u32(base + o);
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kerne
   __shared__ PlaneInfo s_pi[2];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
   __shared__ int s_ent_bad[2];  // mode-3 error flag per ring slot
+  __shared__ __align__(16) uint8_t s_ent_tab[kEntM + 256 * 8];  // mode-3 slot -> bin table, bins, cums
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const long long planes = (long long)n * C;
   const int vals = H * W;
@@ -444,7 +451,7 @@ __global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kerne
         plane_prep(base, sizes[bi], (offs[bi] & 15) == 0, c, C, H, W, pi, s_in[b], nullptr);
         // plane_prep issued nothing (null barrier): issue the staging copy here with its bytes
         uint32_t tx = 0;
-        if (!pi.code && pi.mode == 1 && pi.bytes) {
+        if (!pi.code && (pi.mode == 1 || pi.mode == 3) && pi.bytes) {
           const uint32_t end = pi.start + pi.bytes, hi = end & ~15u;
           if (hi > pi.lo) tx = hi - pi.lo;
         }
@@ -518,7 +525,8 @@ __global__ void __launch_bounds__(kPlaneThreads + 32, 3) lblp_unpack_plane_kerne
         }
       }
     } else if (pi.mode == 3) {
-      const int code = decode_entropy_plane(base + pi.start, pi.bytes, H, W, t, lane, s_in[b], dst, s_ent_bad[b]);
+      const uint8_t* pl = pi.bytes ? s_in[b] + (pi.start - pi.lo) : base + pi.start;  // staged or global
+      const int code = decode_entropy_plane(pl, pi.plen, H, W, t, lane, s_ent_tab, dst, s_ent_bad[b]);
       if (code) {
         for (int i = t; i < vals; i += kPlaneThreads) dst[i] = 0;
         if (t == 0) atomicExch(err, code);
