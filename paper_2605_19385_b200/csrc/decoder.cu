@@ -209,7 +209,8 @@ class Decoder {
   lbx_status graph_for(int n, cudaStream_t s, cudaGraphExec_t* out);
   lbx_status validate_blobs(const uint8_t* const* blobs, const size_t* nbytes, uint32_t n, size_t* total);
   lbx_status stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
-                         cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs = nullptr);
+                         cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs = nullptr,
+                         cudaEvent_t after_copies = nullptr);
   lbx_status grow_staging(Staging& st, size_t total);
   lbx_status alloc_slot(Slot& sl);
   static void free_staging(Staging& st) {
@@ -635,7 +636,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       // written).  Without the preload (debug bit 10) it is added in the epilogue at >= 256
       // channels and folded as extra K at 128.  A 1x1 shortcut is always folded.
       const bool epi_resid =
-          R.cin == R.cout && !resid_fold_always() && (resid_preload() || R.cout >= 256);
+          R.cin == R.cout && !resid_fold_always() && (resid_preload() || R.cout >= 256 || resid_epilogue_all());
       if (epi_resid) {
         g.resid = X_; g.ldr = R.cout;
       } else {
@@ -816,7 +817,8 @@ lbx_status Decoder::grow_staging(Staging& st, size_t total) {
 // to the executing node at LatencyModel::intra_cluster_ms, proj/include/latentbox/sim.hpp:20,
 // proj/src/sim.cpp:369-373); their headers are validated by the device unpack (err_dev).
 lbx_status Decoder::stage_blobs(Staging& st, const uint8_t* const* blobs, const size_t* nbytes, uint32_t n,
-                                cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs) {
+                                cudaStream_t s, __half* lat_out, int* err_dev, const int* blob_devs,
+                                cudaEvent_t after_copies) {
   size_t total = 0;
   if (!blob_devs) {
     lbx_status vs = validate_blobs(blobs, nbytes, n, &total);
@@ -862,6 +864,7 @@ lbx_status Decoder::stage_blobs(Staging& st, const uint8_t* const* blobs, const 
       }
     }
   }
+  if (after_copies) LBX_CUDA_TRY(cudaEventRecord(after_copies, s));
   LBX_CUDA_TRY(cudaMemcpyAsync(st.offs_dev, st.table_host, (size_t)max_batch * 12, cudaMemcpyHostToDevice, s));
   LBX_CUDA_TRY(cudaEventRecord(st.copied, s));
   launch_lblp_unpack(st.dev, st.offs_dev, st.sizes_dev, (int)n, cl, h, w, lat_out, err_dev, s);
@@ -1059,8 +1062,10 @@ static lbx_status submit_impl(lbx_decoder* dec, const uint8_t* const* blobs, con
   if (blob_devs)
     for (uint32_t i = 0; i < n; ++i) sl.timed_peer |= blob_devs[i] >= 0 && blob_devs[i] != d.desc.device;
   if (sl.timed_peer) LBX_CUDA_TRY(cudaEventRecord(sl.peer0, d.in_stream));
-  if ((st = d.stage_blobs(sl.st, blobs, nbytes, n, d.in_stream, sl.lat, sl.err, blob_devs)) != LBX_OK) return st;
-  if (sl.timed_peer) LBX_CUDA_TRY(cudaEventRecord(sl.peer1, d.in_stream));
+  // peer1 is recorded right after the blob copies (before the table upload and the unpack)
+  if ((st = d.stage_blobs(sl.st, blobs, nbytes, n, d.in_stream, sl.lat, sl.err, blob_devs,
+                          sl.timed_peer ? sl.peer1 : nullptr)) != LBX_OK)
+    return st;
   LBX_CUDA_TRY(cudaEventRecord(sl.unpacked, d.in_stream));
   LBX_CUDA_TRY(cudaStreamWaitEvent(d.stream, sl.unpacked, 0));
   LBX_CUDA_TRY(cudaMemcpyAsync(d.lat, sl.lat, d.lat_elems(n) * 2, cudaMemcpyDeviceToDevice, d.stream));

@@ -896,6 +896,7 @@ static int g_stage_policy = 0;     // 1: two A halo stages, the rest of smem to 
 static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box (bit 6 clears)
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
+static int g_eadd_all = 0;         // bit 29: identity residuals added in the epilogue at every width
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
@@ -926,7 +927,8 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vsub_policy = ((halo_policy >> 6) & 1) ? 0 : 1;
   g_fold_always = (halo_policy >> 7) & 1;
   g_vt_legacy = (halo_policy >> 9) & 1;
-  g_rpf_policy = ((halo_policy >> 10) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
+  g_rpf_policy = ((halo_policy >> 10) & 1) || ((halo_policy >> 29) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
+  g_eadd_all = (halo_policy >> 29) & 1;
   g_rpf_pf = (halo_policy >> 21) & 1;
   g_sched_policy = (halo_policy >> 22) & 1;
   g_pdl_policy = (halo_policy >> 23) & 1;
@@ -1071,6 +1073,7 @@ bool gemm_tc_prepare() {  // per device (a multi-GPU batcher drives several from
 bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
 bool resid_preload() { return g_rpf_policy != 0; }
+bool resid_epilogue_all() { return g_eadd_all != 0; }
 bool pdl_enabled() { return g_pdl_policy != 0; }
 void gemm_tc_set_max_sms(int n) { g_gemm_max_sms = n; }
 

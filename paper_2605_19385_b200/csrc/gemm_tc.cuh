@@ -67,6 +67,7 @@ bool resid_fold_always();
 bool v_transpose_legacy();
 // Debug bit 10 clears: conv residuals preloaded into the TMEM accumulator (default on).
 bool resid_preload();
+bool resid_epilogue_all();  // debug bit 29: identity residuals added in the epilogue at every width
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).
 bool gemm_tc_prepare();
