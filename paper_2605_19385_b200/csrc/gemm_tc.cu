@@ -34,6 +34,18 @@
 
 namespace lbx {
 
+// Division by a launch-invariant divisor without the ~20-instruction IDIV sequence: q = n / d for
+// 0 <= n < 2^31 as (umulhi(n, m) + n) >> s with s = ceil(log2 d), m = 2^32 (2^s - d) / d + 1.
+struct FastDiv {
+  uint32_t m = 1, s = 0;
+  FastDiv() = default;
+  explicit FastDiv(uint32_t d) {
+    while ((1u << s) < d) ++s;
+    m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  }
+};
+__device__ __forceinline__ int fdiv(int n, FastDiv f) { return (int)((__umulhi((uint32_t)n, f.m) + (uint32_t)n) >> f.s); }
+
 struct KParams {
   int mode;
   int M, N, K;
@@ -77,6 +89,12 @@ struct KParams {
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
   const float2* gn_ss; // fused GroupNorm+SiLU on A (XF kernels): per (image, channel) (scale, shift)
   int k_main;          // K of the main segment (B columns of the extra segment start here)
+  // invariant divisors of the tile / row arithmetic
+  FastDiv fd_ntiles;   // t / n_tiles
+  FastDiv fd_segs;     // vsub: 128*CG-pixel segments per image row (W / (128 CG))
+  FastDiv fd_per_img;  // vsub: tiles per image ((H / msub) * segs)
+  FastDiv fd_rpi;      // m / rows_per_img (GroupNorm image index)
+  int segs, per_img;
 };
 
 constexpr int kHaloW = 130;      // 128 output pixels + 1-pixel halo on each side
@@ -100,8 +118,8 @@ __device__ __forceinline__ int g_store_mode_dev(const KParams& p) { return p.sto
 __device__ __forceinline__ int g_rpf_l2pf_dev(const KParams& p) { return p.rpf_pf; }
 
 __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile, int& n_tile, int& phase) {
-  n_tile = t % p.n_tiles;
-  int r = t / p.n_tiles;
+  int r = fdiv(t, p.fd_ntiles);
+  n_tile = t - r * p.n_tiles;
   if (p.mode == GEMM_SUBPIX) {
     phase = r & 3;
     m_tile = r >> 2;
@@ -117,12 +135,10 @@ __device__ __forceinline__ void tile_coords(const KParams& p, int t, int& m_tile
 // so both sub-tiles' taps read one (halo_rows + 1)-row halo box.
 __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank, int CG, int sub) {
   if (!p.vsub) return m_tile * (128 * p.msub * CG) + rank * (128 * p.msub) + sub * 128;
-  const int segs = p.W / (128 * CG);
-  const int per_img = (p.H / p.msub) * segs;
-  const int img = m_tile / per_img;
-  const int r = m_tile - img * per_img;
-  const int yp = r / segs;
-  const int x0 = (r - yp * segs) * 128 * CG + rank * 128;
+  const int img = fdiv(m_tile, p.fd_per_img);
+  const int r = m_tile - img * p.per_img;
+  const int yp = fdiv(r, p.fd_segs);
+  const int x0 = (r - yp * p.segs) * 128 * CG + rank * 128;
   return (img * p.H + yp * p.msub + sub) * p.W + x0;
 }
 
@@ -610,8 +626,9 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       } else if (tn < t_end) {
         int mt, nt, phn;
         tile_coords(p, tn, mt, nt, phn);
+        const long long mrow0 = tile_row0(p, mt, (int)rank, CG, 0) + row;
         for (int sub = 0; sub < p.msub; ++sub) {
-          const long long mrow = tile_row0(p, mt, (int)rank, CG, sub) + row;
+          const long long mrow = mrow0 + sub * (p.vsub ? p.W : 128);
           const __half* rb = p.resid + mrow * p.ldr + nt * BN + cbase * 32;
           const uint32_t tb = tmem_base + ((q * 32u) << 16) + buf * (p.msub * BN) + sub * BN;
 #pragma unroll
@@ -676,10 +693,12 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         bias_ntile = n_tile;
       }
       if (p.rpf) prefetch_resid(t + 2 * t_step);
+      const int mrow0 = tile_row0(p, m_tile, (int)rank, CG, 0) + row;  // sub-tile s: + s * sub_stride
+      const int sub_stride = p.vsub ? p.W : 128;
       ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       for (int sub = 0; sub < (p.epi_skip == 1 ? 0 : p.msub); ++sub) {
-      const int m = tile_row0(p, m_tile, (int)rank, CG, sub) + row;
+      const int m = mrow0 + sub * sub_stride;
       long long orow = m;
       if (p.mode == GEMM_SUBPIX) {
         const int hw = p.H * p.W;
@@ -690,7 +709,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       }
       const float rs = scaled ? p.alpha * (p.row_scale ? p.row_scale[m] : 1.f) : 1.f;
       if (p.gn_stats) {
-        const int img = m / p.rows_per_img;  // warp-uniform: 32-row slices never straddle images
+        const int img = fdiv(m, p.fd_rpi);  // warp-uniform: 32-row slices never straddle images
         if (img != g_img || n_tile != g_ntile) {
           flush();
           g_img = img;
@@ -1151,7 +1170,15 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.vsub = (kp.msub == 2 && g_vsub_policy && a.H % 2 == 0 && a.W % (128 * cg) == 0) ? 1 : 0;
   kp.tmem_cols = 2 * bn * kp.msub;
   kp.m_tiles = a.M / (128 * cg * kp.msub);
+  if (kp.vsub) {
+    kp.segs = a.W / (128 * cg);
+    kp.per_img = (a.H / kp.msub) * kp.segs;
+    kp.fd_segs = FastDiv((uint32_t)kp.segs);
+    kp.fd_per_img = FastDiv((uint32_t)kp.per_img);
+  }
   kp.n_tiles = a.N / bn;
+  kp.fd_ntiles = FastDiv((uint32_t)kp.n_tiles);
+  kp.fd_rpi = FastDiv((uint32_t)(a.rows_per_img > 0 ? a.rows_per_img : 1));
   kp.tiles = kp.m_tiles * kp.n_tiles * (a.mode == GEMM_SUBPIX ? 4 : 1);
   if (a.gn_ss) {  // fused GroupNorm + SiLU on the A operand: conv3x3 halo staging only
     if (a.mode != GEMM_CONV3X3 || !kp.halo) return cudaErrorInvalidValue;
