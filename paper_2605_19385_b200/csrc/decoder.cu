@@ -636,7 +636,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       // written).  Without the preload (debug bit 10) it is added in the epilogue at >= 256
       // channels and folded as extra K at 128.  A 1x1 shortcut is always folded.
       const bool epi_resid =
-          R.cin == R.cout && !resid_fold_always() && (resid_preload() || R.cout >= 256 || resid_epilogue_all());
+          R.cin == R.cout && !resid_fold_always() && !(resid_rbuf() && R.cout <= 128) &&
+          (resid_preload() || R.cout >= 256 || resid_epilogue_all());
       if (epi_resid) {
         g.resid = X_; g.ldr = R.cout;
       } else {

@@ -89,6 +89,10 @@ struct KParams {
   int n_extra;         // extra plain k-blocks from the second A operand (K2 / 64)
   const float2* gn_ss; // fused GroupNorm+SiLU on A (XF kernels): per (image, channel) (scale, shift)
   int k_main;          // K of the main segment (B columns of the extra segment start here)
+  int rbuf;            // 1: the extra K segment is staged k-block by k-block in its own buffer (msub x
+                       // 16 KB), each k-block's MMAs interleaved between halo taps (rbuf_at), so its
+                       // loads hide behind the taps instead of taking short A-ring stages
+  int r_bytes;         // smem bytes of that buffer (0 without rbuf)
   // invariant divisors of the tile / row arithmetic
   FastDiv fd_ntiles;   // t / n_tiles
   FastDiv fd_segs;     // vsub: 128*CG-pixel segments per image row (W / (128 CG))
@@ -179,6 +183,10 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&x)[32], uint32_t 
   return x[0];
 }
 
+// rbuf: global tap index (halo stage j, tap tp -> j * taps + tp) before which extra k-block e of the
+// tile is consumed -- spread evenly so every k-block's load hides behind whole taps of MMAs
+__device__ __forceinline__ int rbuf_at(int e, int n_extra, int total_taps) { return (e * total_taps) / n_extra; }
+
 template <int BN, int CG, bool XF>
 __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -189,14 +197,17 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + p.a_stages * p.a_stage_bytes;
-  uint64_t* a_full = reinterpret_cast<uint64_t*>(sB + p.b_stages * C::B_BYTES);
+  uint8_t* sR = sB + p.b_stages * C::B_BYTES;  // rbuf: one extra-segment k-block of every sub-tile
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(sR + p.r_bytes);
   uint64_t* a_empty = a_full + kMaxStages;
   uint64_t* b_full = a_empty + kMaxStages;
   uint64_t* b_empty = b_full + kMaxStages;
   uint64_t* tfull = b_empty + kMaxStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* a_xform = tempty + 2;  // XF: halo transformed (GroupNorm + SiLU applied) and fenced
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_xform + kMaxStages);
+  uint64_t* r_full = a_xform + kMaxStages;  // rbuf: k-block landed / consumed
+  uint64_t* r_empty = r_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(r_empty + 1);
   // 8 epilogue warps x (BN / 2) floats, 16-byte aligned for LDS.128
   float* sBias = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));
   // tstore: per epilogue warp, two 2 KB staging tiles (32 rows x 64 B, SWIZZLE_64B), 1 KB aligned
@@ -237,6 +248,8 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       ptx::mbar_init(&tfull[i], 1);
       ptx::mbar_init(&tempty[i], EPI_WARPS * CG);
     }
+    ptx::mbar_init(r_full, 1);
+    ptx::mbar_init(r_empty, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<CG>(tmem_slot, p.tmem_cols);
@@ -255,12 +268,26 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     if constexpr (XF) ptx::setmaxnreg_dec<56>();
     if (ptx::elect_one()) {
       int st = 0;
-      uint32_t ph = 0;
+      uint32_t ph = 0, rph = 0;
+      const int tot_taps = n_a * per_a;
       for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int rows_cta = 128 * p.msub;
         const int m0 = tile_row0(p, m_tile, rank, CG, 0);  // this CTA's first A row
+        // rbuf: extra k-block e of every sub-tile into the dedicated buffer, once its previous
+        // k-block has been consumed
+        auto r_load = [&](int e) {
+          ptx::mbar_wait(r_empty, rph ^ 1);
+          if (leader) ptx::mbar_arrive_expect_tx(r_full, CG * rows_cta * 64 * 2);
+          for (int sub = 0; sub < p.msub; ++sub) {
+            const int ms = p.vsub ? tile_row0(p, m_tile, rank, CG, sub) : m0 + sub * 128;
+            if constexpr (CG == 1) ptx::tma_load_2d(&tmA2, r_full, sR + sub * 16384, e * 64, ms);
+            else ptx::tma_load_2d_pair(&tmA2, r_full, sR + sub * 16384, e * 64, ms);
+          }
+          rph ^= 1;
+        };
+        int e_next = 0;
         int img = 0, y0 = 0, x0 = 0;
         if (p.mode != GEMM_PLAIN) {
           const int hw = p.H * p.W;
@@ -270,6 +297,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
           x0 = rem - y0 * p.W;
         }
         for (int j = 0; j < n_a; ++j) {
+          if (p.rbuf && e_next < p.n_extra && rbuf_at(e_next, p.n_extra, tot_taps) == j * per_a) r_load(e_next++);
           ptx::mbar_wait(&a_empty[st], ph ^ 1);
           uint8_t* dst = sA + st * p.a_stage_bytes;
           // XF: each CTA's transform warps wait for their own halo, so A lands on the local barrier
@@ -310,8 +338,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst, c0, c1, c2, c3);
           }
           if (++st == p.a_stages) { st = 0; ph ^= 1; }
+          if (p.rbuf)  // the k-blocks consumed between this stage's later taps
+            while (e_next < p.n_extra && rbuf_at(e_next, p.n_extra, tot_taps) < (j + 1) * per_a) r_load(e_next++);
         }
-        for (int e = 0; e < p.n_extra; ++e) {  // second operand: plain [M][K2] rows of this tile
+        for (int e = 0; e < (p.rbuf ? 0 : p.n_extra); ++e) {  // second operand: plain [M][K2] rows of this tile
           ptx::mbar_wait(&a_empty[st], ph ^ 1);
           uint8_t* dst = sA + st * p.a_stage_bytes;
           if (XF) ptx::mbar_arrive_expect_tx(&a_full[st], rows_cta * 64 * 2);
@@ -338,8 +368,18 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         const int b_row = (p.mode == GEMM_SUBPIX ? phs * p.N : 0) + n_tile * BN + rank * C::B_ROWS +
                           (p.b_mn ? 0 : bimg * p.batch_b);
         const int k_img = p.b_mn ? bimg * p.batch_b : 0;
+        int e_next = 0;
         for (int j = 0; j < n_a; ++j) {
           for (int tp = 0; tp < per_a; ++tp) {
+            if (p.rbuf && e_next < p.n_extra && rbuf_at(e_next, p.n_extra, n_a * per_a) == j * per_a + tp) {
+              ptx::mbar_wait(&b_empty[st], ph ^ 1);  // the extra k-block's B rows, in MMA order
+              if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
+              uint8_t* dst = sB + st * C::B_BYTES;
+              if constexpr (CG == 1) ptx::tma_load_2d(&tmB, &b_full[st], dst, p.k_main + e_next * 64, b_row);
+              else ptx::tma_load_2d_pair(&tmB, &b_full[st], dst, p.k_main + e_next * 64, b_row);
+              if (++st == p.b_stages) { st = 0; ph ^= 1; }
+              ++e_next;
+            }
             ptx::mbar_wait(&b_empty[st], ph ^ 1);
             if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
             const int k0 = p.halo ? tp * (p.cblocks * 64) + j * 64 : j * 64;  // K = (tap, channel)
@@ -357,7 +397,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             if (++st == p.b_stages) { st = 0; ph ^= 1; }
           }
         }
-        for (int e = 0; e < p.n_extra; ++e) {
+        for (int e = 0; e < (p.rbuf ? 0 : p.n_extra); ++e) {
           ptx::mbar_wait(&b_empty[st], ph ^ 1);
           if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
           uint8_t* dst = sB + st * C::B_BYTES;
@@ -375,7 +415,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     if constexpr (XF) ptx::setmaxnreg_dec<56>();
     if (leader && ptx::elect_one()) {
       int as = 0, bs = 0;
-      uint32_t aph = 0, bph = 0;
+      uint32_t aph = 0, bph = 0, rph = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint64_t a_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sA));
@@ -388,6 +428,9 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       const uint32_t a_stage16 = (uint32_t)p.a_stage_bytes >> 4, sub16 = (uint32_t)p.halo_sub_bytes >> 4;
       const int msub = p.msub;
       const bool conv = p.mode == GEMM_CONV3X3, halo = p.halo != 0, dbm = p.desc_base_mode != 0;
+      const uint64_t r_desc0 = ptx::sdesc_k_sw128(ptx::smem_u32(sR));
+      const uint32_t rb = (p.rbuf && p.n_extra) ? 1u : 0u;  // the tile's first MMA is an extra k-block's
+      const int tot_taps = n_a * per_a;
       for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
@@ -395,13 +438,37 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         ptx::mbar_wait_cluster(&tempty[acc], p.rpf ? acc_phase : acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * (msub * BN);
-        const uint32_t acc0 = p.rpf ? 1u : 0u;  // accumulate onto the preloaded residual
+        const uint32_t acc0 = (p.rpf ? 1u : 0u) | rb;  // accumulate onto the preloaded residual / k-block 0
+        int e_next = 0;
         for (int j = 0; j < n_a; ++j) {
-          if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
-          else ptx::mbar_wait(&a_full[as], aph);
-          const uint64_t a_stage = a_desc0 + (uint64_t)(as * a_stage16);
+          uint64_t a_stage = 0;
           int r0 = halo && !conv ? (phs & 1) : 0;  // the tap's 128 A rows start r0 rows into the halo
           for (int tp = 0; tp < per_a; ++tp) {
+            if (rb && e_next < p.n_extra && rbuf_at(e_next, p.n_extra, tot_taps) == j * per_a + tp) {
+              ptx::mbar_wait(r_full, rph);  // extra k-block e_next (its B rows are next in the ring)
+              ptx::mbar_wait(&b_full[bs], bph);
+              ptx::tc_fence_after();
+              const uint64_t b_desc = b_desc0 + (uint64_t)(bs * (C::B_BYTES >> 4));
+#pragma unroll
+              for (int sub = 0; sub < 2; ++sub) {
+                if (sub < msub) {
+                  const uint64_t a_desc = r_desc0 + (uint64_t)(sub * (16384 >> 4));
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)
+                    ptx::mma_f16_ss<CG>(d_tmem + sub * BN, a_desc + 2 * k, b_desc + b_k16 * k, idesc, (e_next | k) != 0);
+                }
+              }
+              ptx::mma_commit<CG>(&b_empty[bs]);
+              ptx::mma_commit<CG>(r_empty);
+              if (++bs == p.b_stages) { bs = 0; bph ^= 1; }
+              rph ^= 1;
+              ++e_next;
+            }
+            if (tp == 0) {
+              if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
+              else ptx::mbar_wait(&a_full[as], aph);
+              a_stage = a_desc0 + (uint64_t)(as * a_stage16);
+            }
             ptx::mbar_wait(&b_full[bs], bph);
             ptx::tc_fence_after();
             const uint64_t b_desc = b_desc0 + (uint64_t)(bs * (C::B_BYTES >> 4));
@@ -423,10 +490,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             }
           }
           ptx::mma_commit<CG>(&a_empty[as]);
-          if (j == n_a - 1 && p.n_extra == 0) ptx::mma_commit<CG>(&tfull[acc]);
+          if (j == n_a - 1 && (p.n_extra == 0 || p.rbuf)) ptx::mma_commit<CG>(&tfull[acc]);
           if (++as == p.a_stages) { as = 0; aph ^= 1; }
         }
-        for (int e = 0; e < p.n_extra; ++e) {
+        for (int e = 0; e < (p.rbuf ? 0 : p.n_extra); ++e) {
           if (XF) ptx::mbar_wait_cluster(&a_xform[as], aph);
           else ptx::mbar_wait(&a_full[as], aph);
           ptx::mbar_wait(&b_full[bs], bph);
@@ -916,6 +983,8 @@ static int g_vsub_policy = 1;      // 1: vertical sub-tiles sharing one halo box
 static int g_fold_always = 0;      // 1: fold identity residuals into K at every width (bit 7)
 static int g_vt_legacy = 0;        // 1: attention V transposed by a kernel instead of MN-major B (bit 9)
 static int g_eadd_all = 0;         // bit 29: identity residuals added in the epilogue at every width
+static int g_rbuf_policy = 0;      // bit 24: extra K segments (1x1 shortcut, folded identity residual)
+                                   // staged through their own buffer between halo taps (rbuf)
 static int g_rpf_policy = 1;       // preload conv residuals into the TMEM accumulator: 1 for 128-wide
                                    // outputs (default; 256-wide: the epilogue read measured 10% faster
                                    // on c256), 0 never (bit 10), 2 at every width (bit 20)
@@ -948,6 +1017,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_vt_legacy = (halo_policy >> 9) & 1;
   g_rpf_policy = ((halo_policy >> 10) & 1) || ((halo_policy >> 29) & 1) ? 0 : ((halo_policy >> 20) & 1) ? 2 : 1;
   g_eadd_all = (halo_policy >> 29) & 1;
+  g_rbuf_policy = (halo_policy >> 24) & 1;
   g_rpf_pf = (halo_policy >> 21) & 1;
   g_sched_policy = (halo_policy >> 22) & 1;
   g_pdl_policy = (halo_policy >> 23) & 1;
@@ -963,7 +1033,7 @@ template <int BN, int CG, bool XF>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
   // ---- operand staging plan (tstore: 32 KB of the budget go to the output staging tiles)
-  const int budget = kSmemBudget - ((kp.tstore || kp.rres) ? 33 * 1024 : 0);
+  const int budget = kSmemBudget - ((kp.tstore || kp.rres) ? 33 * 1024 : 0) - kp.r_bytes;
   if (kp.halo) {
     if (kp.vsub) {  // one box of halo_rows + msub - 1 rows; sub-tile s starts 130 s rows in
       kp.halo_sub_bytes = 130 * 128;
@@ -976,7 +1046,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     }
     // policy 1: a halo stage feeds >= 36 MMAs, so two are enough and the rest of the budget goes to
     // B; policy 0 (default): three A stages when the B tile is small and there is one sub-tile
-    if (g_stage_policy || ((kp.tstore || kp.rres) && Cf::B_BYTES >= 16384)) kp.a_stages = 2;
+    if (g_stage_policy || kp.rbuf || ((kp.tstore || kp.rres) && Cf::B_BYTES >= 16384)) kp.a_stages = 2;
     else kp.a_stages = (Cf::B_BYTES >= 32768 || kp.msub > 1) ? 2 : 3;
     kp.b_stages = (budget - kp.a_stages * kp.a_stage_bytes) / Cf::B_BYTES;
   } else {
@@ -986,7 +1056,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
   if (kp.a_stages > kMaxStages) kp.a_stages = kMaxStages;
   if (kp.b_stages > kMaxStages) kp.b_stages = kMaxStages;
   if (kp.a_stages < 2 || kp.b_stages < 2) return cudaErrorInvalidValue;
-  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + (5 * kMaxStages + 4) * 8 + 16 +
+  const int smem = 1024 + kp.a_stages * kp.a_stage_bytes + kp.b_stages * Cf::B_BYTES + kp.r_bytes + (5 * kMaxStages + 6) * 8 + 16 +
                    16 + 8 * (BN / 2) * 4 + ((kp.tstore || kp.rres) ? 1024 + 8 * 2 * 2048 : 0);
   if (smem > Cf::SMEM_MAX) return cudaErrorInvalidValue;
 
@@ -1093,6 +1163,7 @@ bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
 bool resid_preload() { return g_rpf_policy != 0; }
 bool resid_epilogue_all() { return g_eadd_all != 0; }
+bool resid_rbuf() { return g_rbuf_policy != 0; }
 bool pdl_enabled() { return g_pdl_policy != 0; }
 void gemm_tc_set_max_sms(int n) { g_gemm_max_sms = n; }
 
@@ -1180,6 +1251,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.fd_ntiles = FastDiv((uint32_t)kp.n_tiles);
   kp.fd_rpi = FastDiv((uint32_t)(a.rows_per_img > 0 ? a.rows_per_img : 1));
   kp.tiles = kp.m_tiles * kp.n_tiles * (a.mode == GEMM_SUBPIX ? 4 : 1);
+  // rbuf: conv halo mode with an extra segment of at most one k-block per tap (not with XF)
+  kp.rbuf = (g_rbuf_policy && kp.n_extra && kp.halo && a.mode == GEMM_CONV3X3 && !a.gn_ss &&
+             kp.n_extra <= kp.cblocks * kp.taps) ? 1 : 0;
+  kp.r_bytes = kp.rbuf ? kp.msub * 16384 : 0;
   if (a.gn_ss) {  // fused GroupNorm + SiLU on the A operand: conv3x3 halo staging only
     if (a.mode != GEMM_CONV3X3 || !kp.halo) return cudaErrorInvalidValue;
     kp.gn_ss = a.gn_ss;

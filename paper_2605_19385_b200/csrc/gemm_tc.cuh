@@ -67,6 +67,8 @@ bool resid_fold_always();
 bool v_transpose_legacy();
 // Debug bit 10 clears: conv residuals preloaded into the TMEM accumulator (default on).
 bool resid_preload();
+bool resid_rbuf();          // debug bit 24: extra K segments through their own buffer (rbuf); the
+                            // 128-wide identity residual is then folded into K instead of preloaded
 bool resid_epilogue_all();  // debug bit 29: identity residuals added in the epilogue at every width
 
 // Resolve the TMA encoder and set kernel attributes up front (never during stream capture).

@@ -211,11 +211,22 @@ def test_gn_stats_and_apply(lbx, c, silu, inplace):
     _close(y, ref, rel=4e-3 if silu == 2 else 2e-3, abs_=2e-3)
 
 
+@pytest.mark.parametrize("rbuf", [False, True])
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("b,h,w,c,cin", [(2, 16, 256, 128, 128), (1, 16, 256, 128, 256), (1, 64, 64, 256, 512),
-                                         (3, 8, 512, 128, 128)])
-def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin):
-    """conv3x3(H) + X.W2^T as an extra K segment (identity -> residual, W_sc -> 1x1 shortcut)."""
+                                         (3, 8, 512, 128, 128), (1, 8, 512, 256, 512)])
+def test_conv3x3_with_folded_residual(lbx, cg, b, h, w, c, cin, rbuf):
+    """conv3x3(H) + X.W2^T as an extra K segment (identity -> residual, W_sc -> 1x1 shortcut); with
+    rbuf (debug bit 24) the segment's k-blocks go through their own buffer between halo taps."""
+    if rbuf:
+        lbx.check(lbx.lib().lbx_op_set_debug(1 | (1 << 24), 0))
+    try:
+        _folded_residual_case(lbx, cg, b, h, w, c, cin)
+    finally:
+        lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+
+
+def _folded_residual_case(lbx, cg, b, h, w, c, cin):
     n = c
     hin = _rand(b, h, w, c, seed=21)
     x = _rand(b, h, w, cin, seed=22)
