@@ -10,8 +10,10 @@ requests are sharded across GPUs (weak scaling: fixed batch per GPU), no data-pa
 timing is barrier + CUDA events, max over ranks.
 
   value      device-timed images/s, latents already resident in HBM (lbx_decode, CUDA graph)
-  e2e        images/s through lbx_reconstruct with HOST buffers: packed LBLP blobs H2D, unpack,
-             decode, RGB D2H into pinned host memory, every step inside the timed region
+  e2e        images/s through the C ABI with HOST buffers (lbx_reconstruct_submit / _wait, two
+             batches in flight): packed LBLP blobs H2D, unpack, decode, RGB D2H into pinned host
+             memory, every step's copies inside the timed region; e2e.sync = one lbx_reconstruct
+             call per step
   roofline   dominant kernel (largest share of step time in an eager per-launch profile, CUDA
              events on the launching stream), algorithmic FLOPs / launch time vs MEASURED_PEAKS
   cpu_baseline  the oracle (torch fp32, all host cores) decoding a bounded sample on rank 0
@@ -370,14 +372,17 @@ def leg_config34(lbx, torch, dev, stream, steps, root):
     for mode, name in ((1, "config4"), (2, "config3")):
         blobs = [lbx.pack(z[i], mode) for i in range(batch)]
         dec.reconstruct(blobs, out, stream=sp)
-        e2e_ms = timed_events(stream, lambda: dec.reconstruct(blobs, out, stream=sp), k) / k
+        sync_ms = timed_events(stream, lambda: dec.reconstruct(blobs, out, stream=sp), k) / k
+        e2e_ms, _ = pipelined_ms(torch, dec, blobs, k)
         res[name] = {"e2e_img_s": round(batch * 1e3 / e2e_ms, 2), "e2e_ms_per_step": round(e2e_ms, 2),
+                     "e2e_sync_img_s": round(batch * 1e3 / sync_ms, 2),
                      "h2d_bytes_per_step": int(sum(len(b) for b in blobs)), "d2h_bytes_per_step": int(out.nbytes),
                      "blobs": blobs}
     clocks = clk.stop()
     c4 = {"workload": "config4: sd3 16x128x128 -> 1024^2, batch 64 per GPU", "steps": k,
           "device_img_s": round(batch * 1e3 / ms, 2), "device_ms_per_step": round(ms, 2),
-          "e2e_img_s": res["config4"]["e2e_img_s"], "e2e_path": "lbx_reconstruct, LBLP mode-1 (lossless) blobs",
+          "e2e_img_s": res["config4"]["e2e_img_s"], "e2e_sync_img_s": res["config4"]["e2e_sync_img_s"],
+          "e2e_path": "lbx_reconstruct_submit/_wait (two batches in flight; sync = lbx_reconstruct), LBLP mode-1 (lossless) blobs",
           "h2d_bytes_per_step": res["config4"]["h2d_bytes_per_step"],
           "d2h_bytes_per_step": res["config4"]["d2h_bytes_per_step"], "clocks": clocks}
     q8 = res["config3"].pop("blobs")
@@ -385,6 +390,27 @@ def leg_config34(lbx, torch, dev, stream, steps, root):
               "GPU unpack + dequantize -> decode -> RGB D2H, batch 64", steps=k,
               packed_bytes_per_latent=round(statistics.mean(len(b) for b in q8)), clocks=clocks)
     return c4, c3, q8, dec
+
+
+def pipelined_ms(torch, dec, blobs, steps, warmup=2):
+    """ms per step through the asynchronous pipeline (lbx_reconstruct_submit / _wait, two batches in
+    flight -- the paper's fetch/decode/encode overlap): batch k+1's H2D + unpack and batch k-1's RGB
+    D2H overlap batch k's decode graph.  Every step's copies are inside the timed region: host clock
+    from the first submit to the return of the last wait.  Returns (ms, the last step's output)."""
+    n = len(blobs)
+    outs = [torch.empty((n, 8 * dec.h, 8 * dec.w, 3), dtype=torch.uint8, pin_memory=True).numpy() for _ in range(2)]
+    views = [[o[i] for i in range(n)] for o in outs]
+    for w in range(max(2, warmup)):
+        dec.wait(dec.submit(blobs, views[w % 2]))
+    t0 = time.perf_counter()
+    tickets = []
+    for s in range(steps):
+        if len(tickets) == 2:
+            dec.wait(tickets.pop(0))
+        tickets.append(dec.submit(blobs, views[s % 2]))
+    for t in tickets:
+        dec.wait(t)
+    return (time.perf_counter() - t0) * 1e3 / steps, outs[(steps - 1) % 2]
 
 
 def leg_batcher_service(lbx, torch, dev, stream, seconds=4.0):
@@ -569,11 +595,25 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-        e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
-        e2e = {"value": world * batch * args.steps / (e2e_ms / 1e3), "unit": "img/s",
-               "h2d_bytes_per_step": int(sum(len(b) for b in blobs) + 12 * batch),
-               "d2h_bytes_per_step": int(out.nbytes), "path": f"lbx_reconstruct: LBLP mode-{mode} blobs (host) -> "
-               "H2D -> GPU unpack -> decode graph -> RGB D2H (pinned)"}
+        sync_ms = reduce_max(e0.elapsed_time(e1), dev)
+        # the same steps through the asynchronous pipeline (lbx_reconstruct_submit / _wait, two batches
+        # in flight, the paper's fetch/decode/encode overlap): batch k+1's H2D + unpack and batch k-1's
+        # RGB D2H overlap batch k's decode graph.  Every step's copies are inside the timed region:
+        # host clock from the first submit to the return of the last wait, max over ranks.
+        barrier()
+        torch.cuda.synchronize(dev)
+        pipe_step_ms, last = pipelined_ms(torch, dec, blobs, args.steps, args.warmup)
+        pipe_ms = reduce_max(pipe_step_ms * args.steps, dev)
+        barrier()
+        h2d = int(sum(len(b) for b in blobs) + 12 * batch)
+        e2e = {"value": world * batch * args.steps / (pipe_ms / 1e3), "unit": "img/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out.nbytes),
+               "path": f"lbx_reconstruct_submit/_wait: LBLP mode-{mode} blobs (host) -> H2D -> GPU unpack -> "
+               "decode graph -> RGB D2H (pinned), two batches in flight, host clock",
+               "sync": {"value": world * batch * args.steps / (sync_ms / 1e3), "unit": "img/s",
+                        "path": "lbx_reconstruct (synchronous, one batch at a time), CUDA events"}}
+        if not np.array_equal(last, out):
+            raise SystemExit("bench: pipelined reconstruct output differs from lbx_reconstruct's")
         # the return path with the PNG encode on the GPU (lbx_reconstruct_png): fewer steps, same clocking
         pout = torch.empty(batch * lbx.png_bound(1024, 1024), dtype=torch.uint8, pin_memory=True).numpy()
         dec.reconstruct_png(blobs, pout, stream=sp)
@@ -603,8 +643,11 @@ def main():
     tensor_ms = sum(g["ms"] for g in groups.values() if g["flops"] > 0)
     if dom["flops"] > 0:
         achieved = dom["algo"] / (dom["ms"] / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "peak_sustained": peak_sus, "frac_sustained": achieved / peak_sus,
+        # the kernel is timed inside a whole decode step (seconds of back-to-back work at the power
+        # cap), so its peak is the SUSTAINED measured figure; the burst one is reported beside it
+        roof = {"bound": "tensor", "kernel": dom_name, "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
+                "frac": achieved / peak_sus, "peak_kind": "sustained (kernel timed inside a long decode step)",
+                "peak_burst": peak, "frac_burst": achieved / peak,
                 "peak_source": src, "launches": dom["n"], "ms_per_launch": dom["ms"] / dom["n"],
                 "share_of_step": dom["ms"] / total_ms, "traffic": None}
     else:

@@ -13,8 +13,8 @@ for shp in "1024 128" "256 512"; do
       -o gpurun_out/$tag python scripts/op_bench.py conv --b 8 --hw $1 --c $2 --stats $f --iters 1 > /dev/null 2>&1
     echo "=== $tag (op_bench conv --b 8 --hw $1 --c $2 --stats $f)" >> $OUT
     python tools/ncu_summary.py gpurun_out/$tag.ncu-rep | tail -n +2 >> $OUT
-    python tools/ncu_lines.py gpurun_out/$tag.ncu-rep --top 12 --range producers:254-455 --range xf_transform:457-535 \
-      --range epilogue:536-905 >> $OUT
+    python tools/ncu_lines.py gpurun_out/$tag.ncu-rep --top 12 --range producers:267-522 --range xf_transform:524-602 \
+      --range epilogue:603-912 >> $OUT
     python tools/ncu_waits.py gpurun_out/$tag.ncu-rep >> $OUT
     rm -f gpurun_out/$tag.ncu-rep
   done
