@@ -18,7 +18,11 @@
 // whole ring prefetches (the first version kept three rows resident for 72 MMAs per output row
 // and ran latency-bound at ~2.5 TB/s).
 //
-// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 epilogue, 6..13 transform.
+// Warps: 0 TMA producer, 1 TMEM allocator + MMA issuer, 2..5 epilogue, 6.. transform in
+// KCO_GROUPS groups of eight that take input rows round-robin.  One group was the kernel's serial
+// stage (~1.1 us per row against ~0.8 us for the row's HBM share): batch 32 at 1024^2 went
+// 4.31 TB/s (one group) -> 4.72 (two) -> 5.43 (three, 3 chunks in flight per thread) = 0.83 of
+// the measured HBM copy rate (scripts/gpu_tail2.sh).
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -32,7 +36,15 @@ namespace lbx {
 
 namespace {
 
-constexpr int kCoThreads = 448;
+constexpr int kCoXfGroups = KCO_GROUPS;                   // transform groups (alternate input rows)
+constexpr int kCoThreads = 192 + kCoXfGroups * 256;
+#ifndef KCO_GROUPS
+#define KCO_GROUPS 3
+#endif
+#ifndef KCO_NK
+#define KCO_NK 3
+#endif
+constexpr int kCoNK = KCO_NK;                     // transform chunks in flight per thread
 constexpr int kCoSlots = 6;                       // input-row ring depth
 constexpr int kCoBoxBytes = 64 * 130 * 2;         // one TMA box: 64 channels x 130 pixels
 constexpr int kCoCbPitch = 17408;                 // 1024-aligned pitch of one 64-channel block
@@ -215,10 +227,14 @@ __global__ void __launch_bounds__(kCoThreads, 1)
       gi = base + rows_in;
     }
   } else {
-    // ------------------------------------------------------------------ transform (warps 6..13)
-    // thread t owns logical chunk lc = t & 7 (8 channels) of channel block cb = (t >> 3) & 1 for
-    // pixels (t >> 4) + 16 k; the physical 16-byte chunk is lc ^ (px & 7) (128B swizzle).
-    const int t = (int)threadIdx.x - 6 * 32;
+    // ------------------------------------------------------------------ transform (warps 6..21)
+    // group g = (warp - 6) / 8 takes the input rows with gi % kCoXfGroups == g (kCoSlots is a
+    // multiple of the group count, so a group keeps to its own slots); within a group thread t owns
+    // logical chunk lc = t & 7 (8 channels) of channel block cb = (t >> 3) & 1 for pixels
+    // (t >> 4) + 16 k; the physical 16-byte chunk is lc ^ (px & 7) (128B swizzle).
+    static_assert(kCoSlots % kCoXfGroups == 0, "slots per transform group");
+    const uint32_t grp = (warp - 6) >> 3;
+    const int t = ((int)threadIdx.x - 6 * 32) & 255;
     const int lc = t & 7, cb = (t >> 3) & 1, p0 = t >> 4;
     const int c0 = cb * 64 + lc * 8;
     uint32_t gi = 0;
@@ -237,29 +253,32 @@ __global__ void __launch_bounds__(kCoThreads, 1)
         }
       }
       for (int r = 0; r < rows_in; ++r, ++gi) {
+        if (gi % kCoXfGroups != grp) continue;
         const int s = gi % kCoSlots;
         ptx::mbar_wait(&slot_full[s], (gi / kCoSlots) & 1);
         const int y = y0 - 1 + r;
         if (y >= 0 && y < p.H) {
           const uint32_t blk = ptx::smem_u32(sRow + s * kCoSlotBytes + cb * kCoCbPitch);  // shared-space
                                                                                        // address: LDS/STS, not generic LD/ST
-          // all of this thread's chunks of the row (pixels p0 + 16k, k < 9) are loaded before any
-          // is transformed: nine independent LDS -> math -> STS chains instead of one at a time
-          constexpr int NK = 9;
-          uint4 v[NK];
-          bool ok[NK];
+          // this thread's chunks of the row (pixels p0 + 16k, k < 9) in passes of kCoNK: each pass
+          // loads all its chunks before transforming any (independent LDS -> math -> STS chains)
 #pragma unroll
-          for (int k = 0; k < NK; ++k) {
-            const int px = p0 + 16 * k;
-            const int gx = x0 - 1 + px;
-            ok[k] = px < 130 && gx >= 0 && gx < p.W;  // padding stays zero
-            if (ok[k]) v[k] = ptx::lds128(blk + px * 128 + ((lc ^ (px & 7)) << 4));
-          }
+          for (int k0 = 0; k0 < 9; k0 += kCoNK) {
+            uint4 v[kCoNK];
+            bool ok[kCoNK];
 #pragma unroll
-          for (int k = 0; k < NK; ++k) {
-            const int px = p0 + 16 * k;
-            if (ok[k])
-              ptx::sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_silu8_h2_half(v[k], a, b) : gn_act8<true>(v[k], a, b));
+            for (int k = 0; k < kCoNK; ++k) {
+              const int px = p0 + 16 * (k0 + k);
+              const int gx = x0 - 1 + px;
+              ok[k] = k0 + k < 9 && px < 130 && gx >= 0 && gx < p.W;  // padding stays zero
+              if (ok[k]) v[k] = ptx::lds128(blk + px * 128 + ((lc ^ (px & 7)) << 4));
+            }
+#pragma unroll
+            for (int k = 0; k < kCoNK; ++k) {
+              const int px = p0 + 16 * (k0 + k);
+              if (ok[k])
+                ptx::sts128(blk + px * 128 + ((lc ^ (px & 7)) << 4), H2 ? gn_silu8_h2_half(v[k], a, b) : gn_act8<true>(v[k], a, b));
+            }
           }
           ptx::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
         }

@@ -5,6 +5,7 @@ per-op timing).  Not part of the product; device buffers come from torch (plumbi
   python scripts/op_bench.py conv --b 4 --hw 1024 --c 128 --n 128 --resid --stats
   python scripts/op_bench.py subpix --b 4 --hw 512 --c 256
   python scripts/op_bench.py gn --b 4 --hw 1024 --c 128
+  python scripts/op_bench.py tail --b 32 --hw 1024      # GroupNorm+SiLU+conv_out+u8 (GB/s of 256 B/px in + 3 out)
 """
 import argparse
 import os
@@ -18,7 +19,7 @@ import paper_2605_19385_b200 as lbx  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("op", choices=["conv", "subpix", "gemm", "gn"])
+    ap.add_argument("op", choices=["conv", "subpix", "gemm", "gn", "tail"])
     ap.add_argument("--b", type=int, default=4)
     ap.add_argument("--hw", type=int, default=1024)
     ap.add_argument("--c", type=int, default=128)
@@ -76,6 +77,18 @@ def main():
                         bias=0 if a.nobias else bias.data_ptr(), resid=resid.data_ptr() if resid is not None else 0, ldr=n,
                         gn_stats=stats.data_ptr() if a.stats else 0, cta_group=a.cg, bn=a.bn,
                         gn_ss=gss.data_ptr() if gss is not None else 0)
+    elif a.op == "tail":
+        c = 128
+        x = (torch.randn(b, hw, hw, c, device=dev) * 0.5).half()
+        ss = torch.stack([torch.rand(b, c, device=dev) + 0.5, torch.randn(b, c, device=dev) * 0.5], dim=-1).contiguous()
+        wt = torch.randn(3, 3, 3, c, device=dev) * (9 * c) ** -0.5
+        bt = torch.randn(3, device=dev) * 0.2
+        rgb = torch.empty(b, hw, hw, 3, dtype=torch.uint8, device=dev)
+        flops = float(b * hw * hw * (2 * c + 3))  # bytes
+
+        def run():
+            lbx.op_conv_out(x.data_ptr(), ss.data_ptr(), wt.data_ptr(), bt.data_ptr(), rgb.data_ptr(), b, hw, hw,
+                            impl=2)
     else:
         gamma = torch.ones(c, device=dev)
         beta = torch.zeros(c, device=dev)
@@ -94,7 +107,7 @@ def main():
     if a.sustain > 0:
         import subprocess
         import time
-        unit_scale = 1e9 if a.op == "gn" else 1e12
+        unit_scale = 1e9 if a.op in ("gn", "tail") else 1e12
         smi = subprocess.Popen(["nvidia-smi", "--query-gpu=power.draw,clocks.sm", "--format=csv,noheader,nounits",
                                 "-lms", "100"], stdout=subprocess.PIPE, text=True)
         t0 = time.time()
@@ -115,7 +128,7 @@ def main():
         clk = sorted(x[1] for x in half)[len(half) // 2] if half else 0
         ms = ev0.elapsed_time(ev1) / reps
         rate = flops / (ms / 1e3) / unit_scale
-        unit = "GB/s" if a.op == "gn" else "TFLOP/s(algo)"
+        unit = "GB/s" if a.op in ("gn", "tail") else "TFLOP/s(algo)"
         print(f"SUSTAINED {a.op} b{b} hw{hw} c{c} n{n}: {ms:.3f} ms  {rate:.1f} {unit}  power {pw:.0f} W  sm {clk:.0f} MHz  "
               f"{pw / rate:.3f} W per {unit}")
         return
@@ -125,8 +138,8 @@ def main():
     ev1.record()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / a.iters
-    unit = "GB/s" if a.op == "gn" else "TFLOP/s(algo)"
-    scale = 1e9 if a.op == "gn" else 1e12
+    unit = "GB/s" if a.op in ("gn", "tail") else "TFLOP/s(algo)"
+    scale = 1e9 if a.op in ("gn", "tail") else 1e12
     print(f"{a.op} b{b} hw{hw} c{c} n{n}: {ms:.3f} ms  {flops / (ms / 1e3) / scale:.1f} {unit}")
 
 
