@@ -6,6 +6,34 @@
 
 namespace lbx {
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2 / FMUL2): two IEEE fp32 operations per instruction, each
+// rounded once, so bit-identical to the scalar forms with half the issue slots.
+__device__ __forceinline__ uint64_t f2_pack(float2 a) {
+  uint64_t u;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(u) : "f"(a.x), "f"(a.y));
+  return u;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t u) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(u));
+  return r;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+  return f2_unpack(d);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(d);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(d);
+}
+
 // SiLU with one MUFU op per element: ex2 on the SFU, the reciprocal of (1 + e) on the FMA pipe
 // (bit-trick seed, 3 Newton steps -> fp32-accurate).  The SFU (16 ops/clk/SM) is what bounded the
 // GroupNorm-apply pass at ~3.5 TB/s with ex2 + rcp; the FMA pipe has 8x its throughput.
@@ -43,8 +71,9 @@ __device__ __forceinline__ uint4 gn_act8(uint4 u, const float (&a)[8], const flo
   uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-    float y0 = fmaf(f.x, a[2 * j], b[2 * j]), y1 = fmaf(f.y, a[2 * j + 1], b[2 * j + 1]);
+    const float2 y = ffma2(__half22float2(*reinterpret_cast<const __half2*>(&w[j])), make_float2(a[2 * j], a[2 * j + 1]),
+                           make_float2(b[2 * j], b[2 * j + 1]));
+    float y0 = y.x, y1 = y.y;
     if (SILU) { y0 = silu_f(y0); y1 = silu_f(y1); }
     const __half2 h = __floats2half2_rn(y0, y1);
     w[j] = *reinterpret_cast<const uint32_t*>(&h);
@@ -66,8 +95,8 @@ __device__ __forceinline__ uint4 gn_act8_h2(uint4 u, const float (&a)[8], const 
   uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-    __half2 y = __floats2half2_rn(fmaf(f.x, a[2 * j], b[2 * j]), fmaf(f.y, a[2 * j + 1], b[2 * j + 1]));
+    __half2 y = __float22half2_rn(ffma2(__half22float2(*reinterpret_cast<const __half2*>(&w[j])),
+                                        make_float2(a[2 * j], a[2 * j + 1]), make_float2(b[2 * j], b[2 * j + 1])));
     if (SILU) {
       const __half2 h = __hmul2(y, __float2half2_rn(0.5f));
       const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
@@ -87,8 +116,8 @@ __device__ __forceinline__ uint4 gn_silu8_h2_half(uint4 u, const float (&ah)[8],
   uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
-    const __half2 h = __floats2half2_rn(fmaf(f.x, ah[2 * j], bh[2 * j]), fmaf(f.y, ah[2 * j + 1], bh[2 * j + 1]));
+    const __half2 h = __float22half2_rn(ffma2(__half22float2(*reinterpret_cast<const __half2*>(&w[j])),
+                                              make_float2(ah[2 * j], ah[2 * j + 1]), make_float2(bh[2 * j], bh[2 * j + 1])));
     const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
     const uint32_t tb = tanh_f16x2(hb);
     const __half2 y = __hfma2(h, *reinterpret_cast<const __half2*>(&tb), h);

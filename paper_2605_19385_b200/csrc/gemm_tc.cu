@@ -150,19 +150,22 @@ __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank,
 // then the group sums of squares of this lane's 32 fp32 outputs -- added to the lane's running
 // accumulators a[0..NV).  The cross-lane reduction happens once per flush (warp_flush_stats), not per
 // chunk: it was two thirds of the epilogue's instructions.
+// Even and odd elements are summed as packed pairs (FADD2 / FFMA2) and the pair folded at the end.
 template <int NV>
 __device__ __forceinline__ void lane_group_stats(const float (&xs)[32], float* a) {
   constexpr int G = NV / 2, E = 32 / G;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    float s = 0.f, s2 = 0.f;
+    float2 s = make_float2(xs[g * E], xs[g * E + 1]);
+    float2 s2 = fmul2(s, s);
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      s += xs[g * E + i];
-      s2 = fmaf(xs[g * E + i], xs[g * E + i], s2);
+    for (int i = 2; i < E; i += 2) {
+      const float2 x = make_float2(xs[g * E + i], xs[g * E + i + 1]);
+      s = fadd2(s, x);
+      s2 = ffma2(x, x, s2);
     }
-    a[g] += s;
-    a[G + g] += s2;
+    a[g] += s.x + s.y;
+    a[G + g] += s2.x + s2.y;
   }
 }
 
@@ -813,7 +816,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
         if (scaled) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= rs;
+          for (int i = 0; i < 16; ++i) {
+            const float2 t = fmul2(make_float2(v[2 * i], v[2 * i + 1]), make_float2(rs, rs));
+            v[2 * i] = t.x; v[2 * i + 1] = t.y;
+          }
         }
         if (p.bias) {
 #pragma unroll
@@ -822,7 +828,9 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                          : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
                          : "r"(wbias + (j * 32 + 4 * i) * 4));
-            v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+            const float2 t0 = fadd2(make_float2(v[4 * i], v[4 * i + 1]), make_float2(b.x, b.y));
+            const float2 t1 = fadd2(make_float2(v[4 * i + 2], v[4 * i + 3]), make_float2(b.z, b.w));
+            v[4 * i] = t0.x; v[4 * i + 1] = t0.y; v[4 * i + 2] = t1.x; v[4 * i + 3] = t1.y;
           }
         }
         if (eresid) {
@@ -832,9 +840,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             const uint32_t w4[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w4[k]));
-              v[i * 8 + 2 * k] += f.x;
-              v[i * 8 + 2 * k + 1] += f.y;
+              const float2 t = fadd2(make_float2(v[i * 8 + 2 * k], v[i * 8 + 2 * k + 1]),
+                                     __half22float2(*reinterpret_cast<const __half2*>(&w4[k])));
+              v[i * 8 + 2 * k] = t.x;
+              v[i * 8 + 2 * k + 1] = t.y;
             }
           }
           if (j + PF < NCH) {
