@@ -36,14 +36,14 @@ namespace lbx {
 
 namespace {
 
-constexpr int kCoXfGroups = KCO_GROUPS;                   // transform groups (alternate input rows)
-constexpr int kCoThreads = 192 + kCoXfGroups * 256;
 #ifndef KCO_GROUPS
 #define KCO_GROUPS 3
 #endif
 #ifndef KCO_NK
 #define KCO_NK 3
 #endif
+constexpr int kCoXfGroups = KCO_GROUPS;                   // transform groups (alternate input rows)
+constexpr int kCoThreads = 192 + kCoXfGroups * 256;
 constexpr int kCoNK = KCO_NK;                     // transform chunks in flight per thread
 constexpr int kCoSlots = 6;                       // input-row ring depth
 constexpr int kCoBoxBytes = 64 * 130 * 2;         // one TMA box: 64 channels x 130 pixels
