@@ -261,6 +261,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if args.config == 0:  # the same workload as our arm: config 2 at N = 1, config 4 at N > 1
+        args.config = 2 if args.gpus == 1 else 4
     fam, c, batch, name = workload(args)
     threads = os.cpu_count() or 1
     # bounded: each step decodes one 1024^2 image; warm-up capped at 1 step (no JIT/caches to warm)
