@@ -581,6 +581,29 @@ def main():
     value = world * batch * args.steps / (ms_max / 1e3)
     launches = dec.launch_count(batch)
 
+    # ---------------------------------------------------------------- strong scaling (N > 1)
+    # BASELINE config 4 as written: ONE batch of 64 sharded across the N GPUs (64 / N whole requests
+    # per rank), device-timed like `value` (max over ranks); `value` keeps 64 per GPU (weak scaling)
+    strong = None
+    if world > 1 and args.config == 4 and not args.batch:
+        gb = 64
+        f0, f1 = shard_range(gb, rank, world)
+        nb = f1 - f0
+        for _ in range(max(1, args.warmup)):
+            dec.decode_ptr(lat.data_ptr(), nb, rgb.data_ptr(), sp)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dec.decode_ptr(lat.data_ptr(), nb, rgb.data_ptr(), sp)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        sms = reduce_max(e0.elapsed_time(e1), dev)
+        strong = {"global_batch": gb, "per_gpu": nb, "value": gb * args.steps / (sms / 1e3), "unit": "img/s",
+                  "ms_per_step": sms / args.steps, "scaling": "strong",
+                  "note": "BASELINE configs[3]: one batch of 64 sharded across the N GPUs (whole requests)"}
+
     # ---------------------------------------------------------------- end to end (host buffers)
     e2e = None
     if not args.no_e2e:
@@ -745,7 +768,7 @@ def main():
                        "parallelism": f"dp{world} (whole-request sharding, no collective)"
                                       + (" [LBX_BENCH_SHARE_GPU: ranks shared GPUs -- diagnostics, not an N-GPU number]"
                                          if shared else "")},
-            "per_rank_img_s": [round(v, 2) for v in per_rank],
+            "per_rank_img_s": [round(v, 2) for v in per_rank], "strong_scaling": strong,
             "e2e": e2e, "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches * args.steps if launches > 0 else None,
             "configs": configs, "batcher_service": batcher, "nvlink_spill": spill,
