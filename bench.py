@@ -585,8 +585,8 @@ def main():
     # BASELINE config 4 as written: ONE batch of 64 sharded across the N GPUs (64 / N whole requests
     # per rank), device-timed like `value` (max over ranks); `value` keeps 64 per GPU (weak scaling)
     strong = None
-    if world > 1 and args.config == 4 and not args.batch:
-        gb = 64
+    if world > 1 and args.config == 4:
+        gb = batch  # 64 (BASELINE configs[3]) unless --batch overrides it
         f0, f1 = shard_range(gb, rank, world)
         nb = f1 - f0
         for _ in range(max(1, args.warmup)):
