@@ -97,6 +97,9 @@ class Decoder {
   void* arena = nullptr;
   __half *X = nullptr, *A = nullptr, *Hb = nullptr, *S = nullptr, *Vt = nullptr, *lat = nullptr;
   float* rowscale = nullptr;
+  float* rowmax = nullptr;    // fused-exp attention: sampled row maxima, 2 per row of a group
+  float* rowpart = nullptr;   // fused-exp attention: row partial sums, 2 per (row, 256-key tile)
+  int* attn_flag = nullptr;   // fused-exp attention: per-group overflow flags (fallback runs if set)
   unsigned long long* stats = nullptr;  // GroupNorm sites, gnfix.cuh layout
   float2* ss = nullptr;
   uint8_t* rgb = nullptr;
@@ -418,7 +421,8 @@ lbx_status Decoder::alloc_arena() {
     return o;
   };
   const size_t oX = slot(x_el * 2), oA = slot(x_el * 2), oH = slot(h_el * 2), oS = slot(s_el * 2),
-               oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oSt = slot((size_t)kMaxSites * nb * 32 * kGnStatWords * 8),
+               oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oRm = slot(hw * 8 * (size_t)s_imgs),
+               oRp = slot(hw * (size_t)s_imgs * (hw / 256 + 1) * 8), oFl = slot(4 * (size_t)(nb + 1)), oSt = slot((size_t)kMaxSites * nb * 32 * kGnStatWords * 8),
                oSs = slot(nb * 512 * 8), oLat = slot(nb * cl * hw * 2), oRgb = slot(nb * hw * 64 * 3),
                oErr = slot(64);
   LBX_CUDA_TRY(cudaMalloc(&arena, off));
@@ -429,6 +433,9 @@ lbx_status Decoder::alloc_arena() {
   S = (__half*)(b + oS);
   Vt = (__half*)(b + oVt);
   rowscale = (float*)(b + oR);
+  rowmax = (float*)(b + oRm);
+  rowpart = (float*)(b + oRp);
+  attn_flag = (int*)(b + oFl);
   stats = (unsigned long long*)(b + oSt);
   ss = (float2*)(b + oSs);
   lat = (__half*)(b + oLat);
@@ -547,6 +554,9 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       double algo = ga.mode == GEMM_SUBPIX ? 2.0 * 4.0 * ga.M * (double)ga.N * 9.0 * ga.C : fl_main;
       // folded extra K: a 1x1 shortcut (K2 != N) is real algorithmic work; an identity residual is not
       if (ga.K2 && ga.K2 != ga.N) algo += 2.0 * ga.M * (double)ga.N * ga.K2;
+      if (ga.rowred == 1) algo = 0;  // the sampled row maxima are extra work, not the algorithm's
+      double fl_ex = fl;
+      if (ga.run_if) fl_ex = algo = 0;  // the fallback runs only when flagged (normally an early exit)
       char nm[160];
       if (ga.mode == GEMM_PLAIN)
         snprintf(nm, sizeof nm, "%s gemm M%d N%d K%d", what, ga.M, ga.N, ga.K);
@@ -556,7 +566,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       const double by = 2.0 * ((double)ga.M * ga.K / (ga.mode == GEMM_PLAIN ? 1 : (ga.mode == GEMM_CONV3X3 ? 9 : 4)) +
                                (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1) +
                                (double)ga.M * ga.N * (ga.mode == GEMM_SUBPIX ? 4 : 1) * (ga.resid ? 2 : 1));
-      mark(nm, fl, algo, by);
+      mark(nm, fl_ex, algo, ga.run_if ? 0.0 : by);
     }
     return e;
   };
@@ -668,6 +678,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     // groups of up to s_imgs images: one scores GEMM, one softmax and one P.V launch per group
     // (batched plain GEMMs; the P.V of a single image is only 128 pair-tiles, < 2 waves)
     const int gsz = v_transpose_legacy() ? 1 : s_imgs;
+    const bool fused_exp = attn_fused_exp() && L % 256 == 0 && L >= 256;
+    if (fused_exp) LBX_STEP(cudaMemsetAsync(attn_flag, 0, sizeof(int) * (size_t)((n + gsz - 1) / gsz), s), "memset attn flags");
     for (int i0 = 0; i0 < n; i0 += gsz) {
       const int g = std::min(gsz, n - i0);
       const __half* base = Hb + (size_t)i0 * L * 1536;
@@ -679,8 +691,34 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       sq.out = S; sq.ldo = L;
       sq.alpha = 1.0f / std::sqrt(512.0f);
       if (g > 1) { sq.batch_m = L; sq.batch_b = L; sq.b_rows_total = g * L; }
-      if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
-      LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s), "attn.softmax", 4.0 * g * L * (double)L);
+      if (fused_exp) {
+        // softmax folded into the score GEMM: r_m = max of S over 256 keys sampled at stride L/256
+        // (a small GEMM whose epilogue keeps only row maxima), then E = exp(S - r_m) straight from
+        // the fp32 accumulator with per-row partial sums, then row_scale = 1 / sum.  An E that may
+        // overflow fp16 (a score ~11 above r_m) flags the group, and the exact two-pass softmax
+        // below -- launched always, running only when flagged -- recomputes S and P.
+        int* flag = attn_flag + i0 / gsz;
+        GemmArgs mx = sq;
+        mx.N = 256;
+        mx.Bw = base + 512; mx.ldb = 1536 * (L / 256);  // every (L/256)-th key row of each image
+        if (g > 1) { mx.batch_b = 256; mx.b_rows_total = g * 256; }
+        mx.out = S; mx.ldo = 256;                        // not written (rowred 1)
+        mx.rowred = 1; mx.row_part = rowmax;
+        if ((st = gemm(mx, "attn.score_sample")) != LBX_OK) return st;
+        GemmArgs ex = sq;
+        ex.rowred = 2; ex.row_max = rowmax; ex.row_part = rowpart; ex.exp_flag = flag;
+        ex.exp_force = attn_force_fallback() ? 1 : 0;  // tests: every group takes the fallback
+        if ((st = gemm(ex, "attn.scores+exp")) != LBX_OK) return st;
+        LBX_LAUNCH(launch_attn_rowsum(rowpart, 2 * (L / 256), rowscale, g * L, s), "attn.rowsum",
+                   8.0 * g * L * (L / 256) + 4.0 * g * L);
+        GemmArgs fb = sq;
+        fb.run_if = flag;
+        if ((st = gemm(fb, "attn.scores(fallback)")) != LBX_OK) return st;
+        LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s, flag), "attn.softmax(fallback)", 0.0);
+      } else {
+        if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
+        LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s), "attn.softmax", 4.0 * g * L * (double)L);
+      }
       GemmArgs pv;
       pv.mode = GEMM_PLAIN;
       pv.M = g * L; pv.N = 512; pv.K = L;

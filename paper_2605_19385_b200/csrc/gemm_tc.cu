@@ -80,6 +80,15 @@ struct KParams {
   int pdl;             // 1: launched as a programmatic dependent (wait before any global access)
   int rres;            // 1: residual preload through per-warp smem staging (line-covering loads)
   int epi_skip;        // diagnostics (debug bit 12): the epilogue only hands buffers back (wrong results)
+  int rowred;          // attention row reductions (GemmArgs::rowred)
+  const float* row_max;
+  float* row_part;
+  int* exp_flag;
+  int exp_force;       // tests: flag every group (the exact-softmax fallback always runs)
+  const int* run_if;   // skip the launch unless *run_if != 0
+  int ld_skip;         // diagnostics (bits 27 / 28): after a CTA's first tile the B / A producer only
+                       // arrives on the full barrier (no TMA; stale operands, wrong results) -- the
+                       // energy and time of the operand traffic
   int store_mode;      // epilogue global stores: 0 STG.128, 1 STG.256, 2 streaming STG.128
   int tstore;          // 1: epilogue stages each 32x32 chunk in smem and TMA-stores it (tmO)
   int cmap;            // epilogue column chunks per warp: 1 contiguous (hsel*NCH + j), 0 interleaved
@@ -236,6 +245,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
   const int n_a = p.halo ? p.cblocks : p.num_kb;
   const int per_a = p.halo ? p.taps : 1;
 
+  if (p.run_if) {  // uniform across the grid: every CTA reads the same flag before any barrier
+    if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (*reinterpret_cast<const volatile int*>(p.run_if) == 0) return;
+  }
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
     ptx::tma_prefetch(&tmB);
@@ -302,6 +315,11 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         for (int j = 0; j < n_a; ++j) {
           if (p.rbuf && e_next < p.n_extra && rbuf_at(e_next, p.n_extra, tot_taps) == j * per_a) r_load(e_next++);
           ptx::mbar_wait(&a_empty[st], ph ^ 1);
+          if ((p.ld_skip & 2) && t != t_first && !XF) {  // diagnostics: no A traffic
+            if (leader) ptx::mbar_arrive(&a_full[st]);
+            if (++st == p.a_stages) { st = 0; ph ^= 1; }
+            continue;
+          }
           uint8_t* dst = sA + st * p.a_stage_bytes;
           // XF: each CTA's transform warps wait for their own halo, so A lands on the local barrier
           if (XF) ptx::mbar_arrive_expect_tx(&a_full[st], p.a_tx_bytes);
@@ -384,6 +402,11 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
               ++e_next;
             }
             ptx::mbar_wait(&b_empty[st], ph ^ 1);
+            if ((p.ld_skip & 1) && t != t_first) {  // diagnostics: no B traffic
+              if (leader) ptx::mbar_arrive(&b_full[st]);
+              if (++st == p.b_stages) { st = 0; ph ^= 1; }
+              continue;
+            }
             if (leader) ptx::mbar_arrive_expect_tx(&b_full[st], CG * C::B_BYTES);
             const int k0 = p.halo ? tp * (p.cblocks * 64) + j * 64 : j * 64;  // K = (tap, channel)
             uint8_t* dst = sB + st * C::B_BYTES;
@@ -787,6 +810,16 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         }
       }
 
+      // attention row reductions: this lane's row, this warp's column half of the tile
+      float racc = p.rowred == 1 ? -INFINITY : 0.f;
+      bool rbig = false;  // rowred 2: a chunk's E sum reached the fp16 range limit (possible overflow)
+      float2 esc = make_float2(0.f, 0.f), eoff = esc;  // E = 2^(acc * esc - eoff): alpha log2(e), r_m log2(e)
+      if (p.rowred == 2) {
+        const float rref = fmaxf(__ldg(p.row_max + 2 * (size_t)m), __ldg(p.row_max + 2 * (size_t)m + 1));
+        esc = make_float2(p.alpha * 1.4426950408889634f, p.alpha * 1.4426950408889634f);
+        eoff = make_float2(-rref * 1.4426950408889634f, -rref * 1.4426950408889634f);
+      }
+
       // residual prefetch ring, two chunks deep, issued before waiting for the accumulator
       constexpr int PF = NCH < 2 ? NCH : 2;
       uint4 rr[PF][4];
@@ -814,12 +847,29 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (scaled) {
+        if (p.rowred == 2) {  // E = exp(alpha acc - r_m): one FFMA2 per pair, the exponential in fp32
+          float2 cs = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 u = ffma2(make_float2(v[2 * i], v[2 * i + 1]), esc, eoff);
+            v[2 * i] = ptx::ex2_approx(u.x);
+            v[2 * i + 1] = ptx::ex2_approx(u.y);
+            cs = fadd2(cs, make_float2(v[2 * i], v[2 * i + 1]));
+          }
+          const float csum = cs.x + cs.y;
+          racc += csum;
+          rbig |= !(csum < 65504.f);  // some E of the chunk may not fit fp16 (or NaN): flag the group
+        } else if (scaled) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const float2 t = fmul2(make_float2(v[2 * i], v[2 * i + 1]), make_float2(rs, rs));
             v[2 * i] = t.x; v[2 * i + 1] = t.y;
           }
+        }
+        if (p.rowred == 1) {  // row maximum only, nothing stored
+#pragma unroll
+          for (int i = 0; i < 32; ++i) racc = fmaxf(racc, v[i]);
+          continue;
         }
         if (p.bias) {
 #pragma unroll
@@ -901,6 +951,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             lane_group_stats<4>(v, sacc + j * 4);
           }
         }
+      }
+      if (p.rowred) {
+        p.row_part[(size_t)m * (2 * p.n_tiles) + n_tile * 2 + hsel] = racc;
+        if (p.rowred == 2 && (rbig || p.exp_force)) atomicOr(p.exp_flag, 1);
       }
       }  // sub-tiles
       if (p.rpf) {
@@ -1007,6 +1061,9 @@ static int g_sched_policy = 0;     // 1: contiguous tile blocks per cluster for 
 static int g_rpf_pf = 0;           // 1: L2 prefetch ahead of the residual preload (bit 21 sets;
                                    // measured neutral under the power cap)
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
+static int g_attn_exp = 1;          // attention softmax fused into the score GEMM (bit 3 clears)
+static int g_attn_fallback = 0;     // bit 11: force the fused path's exact-softmax fallback (tests)
+static int g_ld_skip = 0;          // diagnostics only (bits 27 / 28): skip B / A operand loads
 static int g_cmap_policy = 1;      // 1: contiguous epilogue column chunks per warp (bit 19 clears)
 static int g_tstore_policy = 2;    // TMA-store epilogue: 2 (default) plain GEMMs only -- the attention
                                    // GEMMs gain 13-26% (scores 9.5 -> 8.3 ms per step) -- 1 every
@@ -1033,6 +1090,9 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_rres_policy = (halo_policy >> 25) & 1;
   g_tstore_policy = ((halo_policy >> 26) & 1) ? 0 : ((halo_policy >> 18) & 1) ? 1 : 2;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
+  g_attn_exp = ((halo_policy >> 3) & 1) ? 0 : 1;
+  g_attn_fallback = (halo_policy >> 11) & 1;
+  g_ld_skip = ((halo_policy >> 27) & 1) | (((halo_policy >> 28) & 1) << 1);
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
   g_epi_skip = ((halo_policy >> 12) & 1) ? 1 : ((halo_policy >> 13) & 1) ? 2 : ((halo_policy >> 14) & 1) ? 3
                                                                      : ((halo_policy >> 15) & 1) ? 4 : 0;
@@ -1170,6 +1230,8 @@ bool gemm_tc_prepare() {  // per device (a multi-GPU batcher drives several from
 
 bool resid_fold_always() { return g_fold_always != 0; }
 bool v_transpose_legacy() { return g_vt_legacy != 0; }
+bool attn_fused_exp() { return g_attn_exp != 0; }
+bool attn_force_fallback() { return g_attn_fallback != 0; }
 bool resid_preload() { return g_rpf_policy != 0; }
 bool resid_epilogue_all() { return g_eadd_all != 0; }
 bool resid_rbuf() { return g_rbuf_policy != 0; }
@@ -1221,6 +1283,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.out = a.out; kp.ldo = a.ldo; kp.bias = a.bias; kp.resid = a.resid; kp.ldr = a.ldr;
   // residual preload into TMEM: conv mode, unscaled outputs (the preload would be scaled too)
   kp.epi_skip = g_epi_skip;
+  kp.ld_skip = g_ld_skip;
   kp.store_mode = g_store_mode;
   kp.cmap = g_cmap_policy;
   if (kp.store_mode == 1 && ((reinterpret_cast<uintptr_t>(a.out) & 31) || (a.ldo % 16))) kp.store_mode = 0;
@@ -1235,6 +1298,14 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.pdl = g_pdl_policy;
   kp.rres = (kp.rpf && g_rres_policy && !kp.tstore && a.ldr % 8 == 0) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
+  kp.run_if = a.run_if;
+  if (a.rowred) {  // plain GEMM, 256-wide tiles (two column halves per tile), nothing else in the epilogue
+    if (a.mode != GEMM_PLAIN || a.bias || a.resid || a.gn_stats || a.row_scale || !a.row_part ||
+        (a.rowred == 2 && (!a.row_max || !a.exp_flag)) || a.rowred > 2 || a.N % 256 || force_bn == 128)
+      return cudaErrorInvalidValue;
+    kp.rowred = a.rowred; kp.row_max = a.row_max; kp.row_part = a.row_part; kp.exp_flag = a.exp_flag;
+    kp.exp_force = a.exp_force;
+  }
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
                      a.rows_per_img <= 0))

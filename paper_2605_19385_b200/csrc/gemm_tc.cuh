@@ -50,6 +50,20 @@ struct GemmArgs {
   unsigned long long* gn_stats = nullptr;  // [img][32][2][2] fixed point (gnfix.cuh); zeroed by the caller
   int gn_cpg = 0;                 // channels per group = N / 32
   int rows_per_img = 0;           // M rows per image (GN image index = m / rows_per_img)
+  // attention row reductions (plain GEMM with alpha, no bias / residual / GroupNorm), per output
+  // row m and (n tile, epilogue column half) h -> row_part[m * 2 * n_tiles + h]:
+  //   rowred 1: the maximum of the scaled values; nothing is stored
+  //   rowred 2: E = exp(v - r_m) is stored (fp16), r_m = max(row_max[2m], row_max[2m + 1]) (a
+  //             rowred-1 pass over a sample of the keys); row_part gets the fp32 sums of E.  A
+  //             32-column chunk whose sum reaches 65504 (an E may overflow fp16) sets *exp_flag,
+  //             and the caller reruns the exact softmax for the group (exp_force: always).
+  int rowred = 0;
+  const float* row_max = nullptr;
+  float* row_part = nullptr;
+  int* exp_flag = nullptr;
+  int exp_force = 0;
+  // if set, the launch does nothing unless *run_if != 0 (the exact-softmax fallback of a group)
+  const int* run_if = nullptr;
 };
 
 // Launch on `stream`.  Returns cudaSuccess or the launch error.  Chooses tile / CTA-pair config.
@@ -65,6 +79,10 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode);
 bool resid_fold_always();
 // Debug bit 9: transpose V with a kernel for P.V (default: V read in place as an MN-major B).
 bool v_transpose_legacy();
+// Attention softmax fused into the score GEMM (exp in the epilogue against a sampled row maximum,
+// exact-softmax fallback on overflow); debug bit 3 clears.  Bit 11 forces the fallback (tests).
+bool attn_fused_exp();
+bool attn_force_fallback();
 // Debug bit 10 clears: conv residuals preloaded into the TMEM accumulator (default on).
 bool resid_preload();
 bool resid_rbuf();          // debug bit 24: extra K segments through their own buffer (rbuf); the

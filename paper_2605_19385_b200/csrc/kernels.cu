@@ -348,9 +348,13 @@ void launch_gn_stats(const __half* x, unsigned long long* stats, int n, int hw, 
 // ----------------------------------------------------------------------------- softmax
 // One 256-thread block per row; the row (<= 16384 fp16 = 32 KiB) is held in registers.
 template <int VPT>  // 16-byte vectors per thread
-__global__ void __launch_bounds__(256) softmax_rows_kernel(__half* S, float* row_scale, int cols) {
+__global__ void __launch_bounds__(256) softmax_rows_kernel(__half* S, float* row_scale, int rows, int cols,
+                                                           const int* run_if) {
+  if (run_if && *reinterpret_cast<const volatile int*>(run_if) == 0) return;
   __shared__ float red[8];
-  __half* row = S + (size_t)blockIdx.x * cols;
+  for (int rix = blockIdx.x; rix < rows; rix += gridDim.x) {  // grid = rows, or one wave when guarded
+  __syncthreads();  // red[] of the previous row is consumed
+  __half* row = S + (size_t)rix * cols;
   const int nvec = cols / 8;
   uint4 u[VPT];
   float mx = -INFINITY;
@@ -400,15 +404,37 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(__half* S, float* row
   if (threadIdx.x == 0) {
     float t = 0.f;
     for (int i = 0; i < 8; ++i) t += red[i];
-    row_scale[blockIdx.x] = 1.0f / t;
+    row_scale[rix] = 1.0f / t;
+  }
   }
 }
 
-void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s) {
+void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s, const int* run_if) {
   const int nvec = cols / 8;
-  if (nvec <= 256 * 2) softmax_rows_kernel<2><<<rows, 256, 0, s>>>(S, row_scale, cols);
-  else if (nvec <= 256 * 4) softmax_rows_kernel<4><<<rows, 256, 0, s>>>(S, row_scale, cols);
-  else softmax_rows_kernel<8><<<rows, 256, 0, s>>>(S, row_scale, cols);
+  // guarded (fallback) launches are one wave of row-looping blocks, so the usual early exit is cheap
+  const int grid = run_if ? std::min(rows, num_sms() * 8) : rows;
+  if (nvec <= 256 * 2) softmax_rows_kernel<2><<<grid, 256, 0, s>>>(S, row_scale, rows, cols, run_if);
+  else if (nvec <= 256 * 4) softmax_rows_kernel<4><<<grid, 256, 0, s>>>(S, row_scale, rows, cols, run_if);
+  else softmax_rows_kernel<8><<<grid, 256, 0, s>>>(S, row_scale, rows, cols, run_if);
+}
+
+// Row sums of the fused-exp score GEMM (GemmArgs::rowred 2): row_scale[r] = 1 / (sum of the row's
+// nparts partial sums).  One warp per row; lane l adds parts l, l + 32, ... in order and the lanes
+// combine through a fixed butterfly, so the result does not depend on the batch or the grid.
+__global__ void __launch_bounds__(256) attn_rowsum_kernel(const float* __restrict__ part, int nparts,
+                                                          float* __restrict__ row_scale, int rows) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* pr = part + (size_t)r * nparts;
+  float t = 0.f;
+  for (int i = lane; i < nparts; i += 32) t += pr[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) row_scale[r] = 1.0f / t;
+}
+
+void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s) {
+  attn_rowsum_kernel<<<(rows + 7) / 8, 256, 0, s>>>(part, nparts, row_scale, rows);
 }
 
 // ----------------------------------------------------------------------------- transpose

@@ -94,6 +94,31 @@ def test_batch_invariance(lbx):
         assert np.array_equal(single[0], batch[i]), i
 
 
+def test_attention_softmax_paths(lbx):
+    """The softmax fused into the score GEMM (default: exp against a sampled row maximum) against
+    the exact two-pass softmax (debug bit 3), and the fused path's overflow fallback (bit 11 forces
+    it for every group): the fallback output is bit-identical to the two-pass path, the fused one
+    within 1 LSB of it, and both meet the oracle bar.  Two images per attention group (sd3, batch 2)
+    and one (sd15) cover the batched and the single-image score GEMMs."""
+    import vae_ref
+    import weights_ref
+    cases = [("sd15", 1, 1), ("sd3", 2, 5)]
+    try:
+        for fam, n, seed in cases:
+            z = weights_ref.make_latents(fam, n, 64, 64, seed=seed)
+            ref = vae_ref.decode(z, weights_ref.make_weights(fam, 0), fam)
+            outs = {}
+            for name, bits in (("fused", 1), ("two_pass", 1 | (1 << 3)), ("fallback", 1 | (1 << 11))):
+                lbx.check(lbx.lib().lbx_op_set_debug(bits, 0))
+                outs[name] = lbx.Decoder(fam, (64, 64), seed=0, max_batch=n).reconstruct_latents(z)
+                _check(_stats(outs[name], ref), f"{fam} batch {n} attention {name}")
+            assert np.array_equal(outs["fallback"], outs["two_pass"])
+            d = np.abs(outs["fused"].astype(np.int16) - outs["two_pass"].astype(np.int16))
+            assert d.max() <= 1, d.max()
+    finally:
+        lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+
+
 def test_decode_device_pointers_and_graph_reuse(lbx):
     """lbx_decode on device buffers; repeated calls (graph replay) are bit-identical."""
     import torch
