@@ -695,9 +695,11 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
         // softmax folded into the score GEMM: r_m = max of S over 256 keys sampled at stride L/256
         // (a small GEMM whose epilogue keeps only row maxima), then E = exp(S - r_m) straight from
         // the fp32 accumulator with per-row partial sums, then row_scale = 1 / sum.  An E that may
-        // overflow fp16 (a score ~11 above r_m) flags the group, and the exact two-pass softmax
-        // below -- launched always, running only when flagged -- recomputes S and P.
+        // overflow fp16 (a score ~11 above r_m) flags the group; the fallback below -- launched
+        // always, running only when flagged -- takes the exact row maximum over all keys (the same
+        // GEMM with N = L) and recomputes E against it, so every E <= 1.
         int* flag = attn_flag + i0 / gsz;
+        const int nparts = 2 * (L / 256);
         GemmArgs mx = sq;
         mx.N = 256;
         mx.Bw = base + 512; mx.ldb = 1536 * (L / 256);  // every (L/256)-th key row of each image
@@ -709,12 +711,16 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
         ex.rowred = 2; ex.row_max = rowmax; ex.row_part = rowpart; ex.exp_flag = flag;
         ex.exp_force = attn_force_fallback() ? 1 : 0;  // tests: every group takes the fallback
         if ((st = gemm(ex, "attn.scores+exp")) != LBX_OK) return st;
-        LBX_LAUNCH(launch_attn_rowsum(rowpart, 2 * (L / 256), rowscale, g * L, s), "attn.rowsum",
-                   8.0 * g * L * (L / 256) + 4.0 * g * L);
-        GemmArgs fb = sq;
-        fb.run_if = flag;
-        if ((st = gemm(fb, "attn.scores(fallback)")) != LBX_OK) return st;
-        LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s, flag), "attn.softmax(fallback)", 0.0);
+        LBX_LAUNCH(launch_attn_rowsum(rowpart, nparts, rowscale, g * L, s), "attn.rowsum",
+                   4.0 * g * L * nparts + 4.0 * g * L);
+        GemmArgs fmx = sq;  // fallback: exact row maxima over all keys (nothing stored)
+        fmx.rowred = 1; fmx.row_part = rowpart; fmx.run_if = flag;
+        if ((st = gemm(fmx, "attn.score_max(fallback)")) != LBX_OK) return st;
+        LBX_LAUNCH(launch_attn_rowmax(rowpart, nparts, rowmax, g * L, s, flag), "attn.rowmax(fallback)", 0.0);
+        GemmArgs fex = ex;
+        fex.exp_force = 0; fex.run_if = flag;
+        if ((st = gemm(fex, "attn.scores+exp(fallback)")) != LBX_OK) return st;
+        LBX_LAUNCH(launch_attn_rowsum(rowpart, nparts, rowscale, g * L, s, flag), "attn.rowsum(fallback)", 0.0);
       } else {
         if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
         LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s), "attn.softmax", 4.0 * g * L * (double)L);

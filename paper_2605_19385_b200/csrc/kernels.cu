@@ -421,20 +421,42 @@ void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaSt
 // Row sums of the fused-exp score GEMM (GemmArgs::rowred 2): row_scale[r] = 1 / (sum of the row's
 // nparts partial sums).  One warp per row; lane l adds parts l, l + 32, ... in order and the lanes
 // combine through a fixed butterfly, so the result does not depend on the batch or the grid.
-__global__ void __launch_bounds__(256) attn_rowsum_kernel(const float* __restrict__ part, int nparts,
-                                                          float* __restrict__ row_scale, int rows) {
-  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (r >= rows) return;
-  const float* pr = part + (size_t)r * nparts;
-  float t = 0.f;
-  for (int i = lane; i < nparts; i += 32) t += pr[i];
+// MAX = true: out[2r] = max of the row's parts, out[2r + 1] = -inf (the exact row maximum of the
+// fallback, in the sampled-maximum layout the score GEMM reads).  Guarded launches (run_if) are one
+// wave of row-looping warps that exit at once unless the group was flagged.
+template <bool MAX>
+__global__ void __launch_bounds__(256) attn_rowred_kernel(const float* __restrict__ part, int nparts,
+                                                          float* __restrict__ out, int rows, const int* run_if) {
+  if (run_if && *reinterpret_cast<const volatile int*>(run_if) == 0) return;
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += gridDim.x * 8) {
+    const float* pr = part + (size_t)r * nparts;
+    float t = MAX ? -INFINITY : 0.f;
+    for (int i = lane; i < nparts; i += 32) t = MAX ? fmaxf(t, pr[i]) : t + pr[i];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  if (lane == 0) row_scale[r] = 1.0f / t;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float u = __shfl_xor_sync(0xffffffffu, t, o);
+      t = MAX ? fmaxf(t, u) : t + u;
+    }
+    if (lane == 0) {
+      if (MAX) {
+        out[2 * (size_t)r] = t;
+        out[2 * (size_t)r + 1] = -INFINITY;
+      } else {
+        out[r] = 1.0f / t;
+      }
+    }
+  }
 }
 
-void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s) {
-  attn_rowsum_kernel<<<(rows + 7) / 8, 256, 0, s>>>(part, nparts, row_scale, rows);
+void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s, const int* run_if) {
+  const int grid = run_if ? std::min((rows + 7) / 8, num_sms() * 8) : (rows + 7) / 8;
+  attn_rowred_kernel<false><<<grid, 256, 0, s>>>(part, nparts, row_scale, rows, run_if);
+}
+
+void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s, const int* run_if) {
+  const int grid = run_if ? std::min((rows + 7) / 8, num_sms() * 8) : (rows + 7) / 8;
+  attn_rowred_kernel<true><<<grid, 256, 0, s>>>(part, nparts, row_max2, rows, run_if);
 }
 
 // ----------------------------------------------------------------------------- transpose

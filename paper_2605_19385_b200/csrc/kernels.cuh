@@ -35,8 +35,13 @@ void launch_gn_apply(const __half* x, __half* y, const GnSrc& g, long long rows,
 // Row softmax numerator in place: P = exp(S - rowmax(S)) (fp16), row_scale = 1 / sum(P) (fp32).
 // With run_if set the launch does nothing unless *run_if != 0 (the fused-exp path's fallback).
 void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s, const int* run_if = nullptr);
-// row_scale[r] = 1 / sum(part[r][0 .. nparts)) in a fixed order (fused-exp attention scores).
-void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s);
+// Fused-exp attention scores: row_scale[r] = 1 / sum(part[r][0 .. nparts)) in a fixed order, and
+// (fallback) row_max2[2r] = max(part[r][..]), row_max2[2r + 1] = -inf.  With run_if set the launch
+// does nothing unless *run_if != 0.
+void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s,
+                        const int* run_if = nullptr);
+void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s,
+                        const int* run_if = nullptr);
 
 // out[c][r] = in[r][c] for an R x Cc block with input row stride ldi and output row stride ldo.
 void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, int Cc, cudaStream_t s);

@@ -95,11 +95,11 @@ def test_batch_invariance(lbx):
 
 
 def test_attention_softmax_paths(lbx):
-    """The softmax fused into the score GEMM (default: exp against a sampled row maximum) against
-    the exact two-pass softmax (debug bit 3), and the fused path's overflow fallback (bit 11 forces
-    it for every group): the fallback output is bit-identical to the two-pass path, the fused one
-    within 1 LSB of it, and both meet the oracle bar.  Two images per attention group (sd3, batch 2)
-    and one (sd15) cover the batched and the single-image score GEMMs."""
+    """The softmax fused into the score GEMM (default: exp against a sampled row maximum), its
+    overflow fallback (exact row maximum over all keys, then the same fused exp; debug bit 11 forces
+    it for every group) and the exact two-pass softmax (debug bit 3): each meets the oracle bar and
+    they agree within 1 LSB.  Two images per attention group (sd3, batch 2) and one (sd15) cover the
+    batched and the single-image score GEMMs."""
     import vae_ref
     import weights_ref
     cases = [("sd15", 1, 1), ("sd3", 2, 5)]
@@ -112,11 +112,45 @@ def test_attention_softmax_paths(lbx):
                 lbx.check(lbx.lib().lbx_op_set_debug(bits, 0))
                 outs[name] = lbx.Decoder(fam, (64, 64), seed=0, max_batch=n).reconstruct_latents(z)
                 _check(_stats(outs[name], ref), f"{fam} batch {n} attention {name}")
-            assert np.array_equal(outs["fallback"], outs["two_pass"])
-            d = np.abs(outs["fused"].astype(np.int16) - outs["two_pass"].astype(np.int16))
-            assert d.max() <= 1, d.max()
+            for other in ("two_pass", "fallback"):
+                d = np.abs(outs["fused"].astype(np.int16) - outs[other].astype(np.int16))
+                assert d.max() <= 1, (other, d.max())
     finally:
         lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+
+
+def _peaked_attention_params(fam, seed, gain):
+    """Canonical fp32 parameter blob with the attention's to_q / to_k weights and biases scaled by
+    `gain` (a power of two, so the fp16 weights stay exact): scores gain^2 times wider."""
+    import weights_ref
+    w = weights_ref.make_weights(fam, seed)
+    for t in ("to_q", "to_k"):
+        for kind in ("weight", "bias"):
+            w[f"decoder.mid_block.attentions.0.{t}.{kind}"] = w[f"decoder.mid_block.attentions.0.{t}.{kind}"] * gain
+    cl, _, _, pq = weights_ref.FAMILIES[fam]
+    blob = np.concatenate([w[name].ravel() for name, _, _, _ in weights_ref.param_specs(cl, pq)]).astype(np.float32)
+    return w, blob
+
+
+def test_attention_overflow_fallback_peaked_scores(lbx):
+    """Scores 64x wider than the seeded weights give (std ~22 instead of 0.34): the maximum over the
+    256 sampled keys misses the row maximum by far more than fp16's exp range, so the fused path
+    must detect the overflow itself and take the fallback.  Its output equals the forced fallback
+    bit for bit and meets the oracle bar on the same weights."""
+    import vae_ref
+    import weights_ref
+    w, blob = _peaked_attention_params("sd15", 0, 8.0)
+    z = weights_ref.make_latents("sd15", 1, 64, 64, seed=1)
+    ref = vae_ref.decode(z, w, "sd15")
+    try:
+        lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+        natural = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1).reconstruct_latents(z)
+        lbx.check(lbx.lib().lbx_op_set_debug(1 | (1 << 11), 0))
+        forced = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1).reconstruct_latents(z)
+    finally:
+        lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
+    assert np.array_equal(natural, forced)
+    _check(_stats(natural, ref), "sd15 peaked attention (fallback taken)")
 
 
 def test_decode_device_pointers_and_graph_reuse(lbx):
