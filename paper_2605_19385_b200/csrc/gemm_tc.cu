@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -85,6 +86,7 @@ struct KParams {
   float* row_part;
   int* exp_flag;
   int exp_force;       // tests: flag every group (the exact-softmax fallback always runs)
+  int exp_h2;          // rowred 2: fp16 exponent, two E per MUFU op (ex2.approx.f16x2)
   const int* run_if;   // skip the launch unless *run_if != 0
   int ld_skip;         // diagnostics (bits 27 / 28): after a CTA's first tile the B / A producer only
                        // arrives on the full barrier (no TMA; stale operands, wrong results) -- the
@@ -847,6 +849,43 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        if (p.rowred == 2 && p.exp_h2) {
+          // E = exp(alpha acc - r_m): the exponent u = log2(e) (alpha acc - r_m) in fp32 (one FFMA2
+          // per pair), rounded to fp16 -- its error is relative to |S - r_m|, not to |S| -- then two
+          // E per MUFU op (ex2.approx.f16x2), already the fp16 values P.V multiplies; their fp32 sum
+          float2 cs = make_float2(0.f, 0.f);
+          uint32_t e2[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 u = ffma2(make_float2(v[2 * i], v[2 * i + 1]), esc, eoff);
+            const __half2 uh = __floats2half2_rn(u.x, u.y);
+            e2[i] = ptx::ex2_approx_h2(*reinterpret_cast<const uint32_t*>(&uh));
+            cs = fadd2(cs, __half22float2(*reinterpret_cast<const __half2*>(&e2[i])));
+          }
+          const float csum = cs.x + cs.y;
+          racc += csum;
+          rbig |= !(csum < 65504.f);  // an E of the chunk may be inf (or NaN): flag the group
+          uint4* op = reinterpret_cast<uint4*>(p.out + orow * p.ldo + n);
+          uint4 pk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) pk[i] = make_uint4(e2[4 * i], e2[4 * i + 1], e2[4 * i + 2], e2[4 * i + 3]);
+          if (p.tstore) {
+            uint8_t* buf = sOut + (ew * 2 + (ochunk & 1)) * 2048;
+            if (lane == 0) ptx::bulk_wait_read<1>();
+            __syncwarp();
+            const uint32_t base = ptx::smem_u32(buf) + lane * 64;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ptx::sts128(base + ((i ^ ((lane >> 1) & 3)) << 4), pk[i]);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::tma_store_2d(&tmO, buf, n, (int)(orow - lane));
+            ++ochunk;
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) op[i] = pk[i];
+          }
+          continue;
+        }
         if (p.rowred == 2) {  // E = exp(alpha acc - r_m): one FFMA2 per pair, the exponential in fp32
           float2 cs = make_float2(0.f, 0.f);
 #pragma unroll
@@ -1090,7 +1129,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_rres_policy = (halo_policy >> 25) & 1;
   g_tstore_policy = ((halo_policy >> 26) & 1) ? 0 : ((halo_policy >> 18) & 1) ? 1 : 2;
   g_cmap_policy = ((halo_policy >> 19) & 1) ? 0 : 1;
-  g_attn_exp = ((halo_policy >> 3) & 1) ? 0 : 1;
+  g_attn_exp = ((halo_policy >> 3) & 1) ? 0 : ((halo_policy >> 30) & 1) ? 2 : 1;  // bit 30: f16x2 exp
   g_attn_fallback = (halo_policy >> 11) & 1;
   g_ld_skip = ((halo_policy >> 27) & 1) | (((halo_policy >> 28) & 1) << 1);
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
@@ -1240,6 +1279,9 @@ void gemm_tc_set_max_sms(int n) { g_gemm_max_sms = n; }
 
 bool gemm_tc_can_fuse_gn(const GemmArgs& a) {
   // halo staging (128-pixel row segments); four extra warps transform each landed halo
+  // LBX_FUSE_C (diagnostics): with bit 2, fuse only the convs with this many input channels
+  static const int fuse_c = std::getenv("LBX_FUSE_C") ? std::atoi(std::getenv("LBX_FUSE_C")) : 0;
+  if (fuse_c && a.C != fuse_c) return false;
   return g_fuse_policy && g_halo_policy && a.mode == GEMM_CONV3X3 && a.W >= 128 && a.W % 128 == 0 &&
          a.N % 128 == 0 && a.C % 64 == 0 && a.M % 256 == 0;
 }
@@ -1305,6 +1347,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
       return cudaErrorInvalidValue;
     kp.rowred = a.rowred; kp.row_max = a.row_max; kp.row_part = a.row_part; kp.exp_flag = a.exp_flag;
     kp.exp_force = a.exp_force;
+    kp.exp_h2 = g_attn_exp == 2 ? 1 : 0;
   }
   kp.gn_stats = a.gn_stats; kp.gn_cpg = a.gn_cpg; kp.rows_per_img = a.rows_per_img;
   if (a.gn_stats && (!(a.gn_cpg == 4 || a.gn_cpg == 8 || a.gn_cpg == 16) || a.N != 32 * a.gn_cpg ||
