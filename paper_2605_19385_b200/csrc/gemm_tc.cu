@@ -201,7 +201,9 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&x)[32], uint32_t 
 // tile is consumed -- spread evenly so every k-block's load hides behind whole taps of MMAs
 __device__ __forceinline__ int rbuf_at(int e, int n_extra, int total_taps) { return (e * total_taps) / n_extra; }
 
-template <int BN, int CG, bool XF>
+// RR: the attention row-reduction epilogue (GemmArgs::rowred) is compiled in -- a separate
+// instantiation, so the conv epilogue carries none of its branches or registers
+template <int BN, int CG, bool XF, bool RR = false>
 __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmO,
@@ -813,10 +815,10 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       }
 
       // attention row reductions: this lane's row, this warp's column half of the tile
-      float racc = p.rowred == 1 ? -INFINITY : 0.f;
+      float racc = RR && p.rowred == 1 ? -INFINITY : 0.f;
       bool rbig = false;  // rowred 2: a chunk's E sum reached the fp16 range limit (possible overflow)
       float2 esc = make_float2(0.f, 0.f), eoff = esc;  // E = 2^(acc * esc - eoff): alpha log2(e), r_m log2(e)
-      if (p.rowred == 2) {
+      if (RR && p.rowred == 2) {
         const float rref = fmaxf(__ldg(p.row_max + 2 * (size_t)m), __ldg(p.row_max + 2 * (size_t)m + 1));
         esc = make_float2(p.alpha * 1.4426950408889634f, p.alpha * 1.4426950408889634f);
         eoff = make_float2(-rref * 1.4426950408889634f, -rref * 1.4426950408889634f);
@@ -849,7 +851,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        if (p.rowred == 2 && p.exp_h2) {
+        if (RR && p.rowred == 2 && p.exp_h2) {
           // E = exp(alpha acc - r_m): the exponent u = log2(e) (alpha acc - r_m) in fp32 (one FFMA2
           // per pair), rounded to fp16 -- its error is relative to |S - r_m|, not to |S| -- then two
           // E per MUFU op (ex2.approx.f16x2), already the fp16 values P.V multiplies; their fp32 sum
@@ -886,7 +888,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
           }
           continue;
         }
-        if (p.rowred == 2) {  // E = exp(alpha acc - r_m): one FFMA2 per pair, the exponential in fp32
+        if (RR && p.rowred == 2) {  // E = exp(alpha acc - r_m): one FFMA2 per pair, the exponential in fp32
           float2 cs = make_float2(0.f, 0.f);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -905,7 +907,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
             v[2 * i] = t.x; v[2 * i + 1] = t.y;
           }
         }
-        if (p.rowred == 1) {  // row maximum only, nothing stored
+        if (RR && p.rowred == 1) {  // row maximum only, nothing stored
 #pragma unroll
           for (int i = 0; i < 32; ++i) racc = fmaxf(racc, v[i]);
           continue;
@@ -991,7 +993,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
           }
         }
       }
-      if (p.rowred) {
+      if (RR && p.rowred) {
         p.row_part[(size_t)m * (2 * p.n_tiles) + n_tile * 2 + hsel] = racc;
         if (p.rowred == 2 && (rbig || p.exp_force)) atomicOr(p.exp_flag, 1);
       }
@@ -1137,7 +1139,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
                                                                      : ((halo_policy >> 15) & 1) ? 4 : 0;
 }
 
-template <int BN, int CG, bool XF>
+template <int BN, int CG, bool XF, bool RR = false>
 static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream) {
   using Cf = Cfg<BN, CG>;
   // ---- operand staging plan (tstore: 32 KB of the budget go to the output staging tiles)
@@ -1209,7 +1211,7 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
     cuuint32_t box[2] = {64, (cuuint32_t)Cf::B_ROWS};
     if (!make_map(&tmB, a.Bw, 2, dims, strides, box)) return cudaErrorInvalidValue;
   }
-  auto kern = gemm_tc_kernel<BN, CG, XF>;
+  auto kern = gemm_tc_kernel<BN, CG, XF, RR>;
   const int sms = num_sms();
   int clusters = (g_gemm_max_sms > 0 && g_gemm_max_sms < sms ? g_gemm_max_sms : sms) / CG;
   if (kp.gn_stats && !kp.sched) {
@@ -1246,7 +1248,9 @@ static cudaError_t launch_cfg(const GemmArgs& a, KParams kp, cudaStream_t stream
 template <int BN, int CG>
 static bool set_attr() {
   return ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, CG, false>), Cfg<BN, CG>::SMEM_MAX) &&
-         ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, CG, true>), Cfg<BN, CG>::SMEM_MAX);
+         ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<BN, CG, true>), Cfg<BN, CG>::SMEM_MAX) &&
+         (BN != 256 || ensure_smem_attr(reinterpret_cast<const void*>(gemm_tc_kernel<256, CG, false, true>),
+                                        Cfg<256, CG>::SMEM_MAX));
 }
 
 bool ensure_smem_attr(const void* func, int bytes) {
@@ -1385,6 +1389,10 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
     if (bn == 128 && cg == 2) return launch_cfg<128, 2, true>(a, kp, stream);
     if (bn == 256 && cg == 1) return launch_cfg<256, 1, true>(a, kp, stream);
     return launch_cfg<128, 1, true>(a, kp, stream);
+  }
+  if (kp.rowred) {  // bn == 256 (checked above)
+    if (cg == 2) return launch_cfg<256, 2, false, true>(a, kp, stream);
+    return launch_cfg<256, 1, false, true>(a, kp, stream);
   }
   if (bn == 256 && cg == 2) return launch_cfg<256, 2, false>(a, kp, stream);
   if (bn == 128 && cg == 2) return launch_cfg<128, 2, false>(a, kp, stream);
