@@ -1104,7 +1104,8 @@ static int g_rpf_pf = 0;           // 1: L2 prefetch ahead of the residual prelo
 static int g_epi_skip = 0;         // diagnostics only (bit 12): skip the epilogue's work
 static int g_attn_exp = 1;          // attention softmax fused into the score GEMM (bit 3 clears)
 static int g_attn_fallback = 0;     // bit 11: force the fused path's exact-softmax fallback (tests)
-static int g_ld_skip = 0;          // diagnostics only (bits 27 / 28): skip B / A operand loads
+static int g_ld_skip = 0;
+static int g_small_bn = 1;          // 128-wide tiles for small grids (LBX_SMALL_BN=0 disables; A/B)          // diagnostics only (bits 27 / 28): skip B / A operand loads
 static int g_cmap_policy = 1;      // 1: contiguous epilogue column chunks per warp (bit 19 clears)
 static int g_tstore_policy = 2;    // TMA-store epilogue: 2 (default) plain GEMMs only -- the attention
                                    // GEMMs gain 13-26% (scores 9.5 -> 8.3 ms per step) -- 1 every
@@ -1268,6 +1269,11 @@ bool ensure_smem_attr(const void* func, int bytes) {
 
 bool gemm_tc_prepare() {  // per device (a multi-GPU batcher drives several from one process)
   num_sms();
+  static const bool env_read = [] {
+    if (const char* e = std::getenv("LBX_SMALL_BN")) g_small_bn = std::atoi(e);
+    return true;
+  }();
+  (void)env_read;
   return tma_available() && set_attr<256, 2>() && set_attr<128, 2>() && set_attr<256, 1>() && set_attr<128, 1>();
 }
 
@@ -1362,6 +1368,16 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   int bn = force_bn ? force_bn : (a.N % 256 == 0 ? 256 : 128);
   if (a.N % bn) return cudaErrorInvalidValue;
   int cg = force_cg ? force_cg : ((a.M % 256 == 0) ? 2 : 1);
+  if (!force_bn && bn == 256 && !a.rowred && g_small_bn) {
+    // small grids (the 64x64 layers and the attention of a 512^2 decode): when 256-wide tiles
+    // would leave clusters idle, 128-wide ones double the tiles.  With GroupNorm statistics the
+    // rule looks at one image's tiles, so the choice -- and with it which values a lane sums in
+    // fp32 -- does not depend on the batch (decodes stay bit-identical across batch sizes); plain
+    // GEMM outputs do not depend on the tile width at all (same K order per element).
+    const long long rows = a.gn_stats ? (long long)a.rows_per_img : (long long)a.M;
+    const long long t256 = rows / (128 * cg) * (a.N / 256) * (a.mode == GEMM_SUBPIX ? 4 : 1);
+    if (t256 < num_sms() / cg) bn = 128;
+  }
   if (a.M % (128 * cg)) return cudaErrorInvalidValue;
   kp.msub = (kp.halo && g_msub_policy && bn == 128 && cg == 2 && a.mode == GEMM_CONV3X3 && a.W % 256 == 0 &&
              a.M % (512 * cg) == 0) ? 2 : 1;
