@@ -35,7 +35,8 @@ def sources():
 def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall,-fvisibility=hidden",
                    "--expt-relaxed-constexpr",
-                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if os.environ.get("LBX_PTXAS_V") else "-O3"]
+                   "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if os.environ.get("LBX_PTXAS_V") else "-O3"] + \
+        os.environ.get("LBX_EXTRA_NVCC_FLAGS", "").split()  # experiments only (A/B builds)
 
 
 def _compile(src: str) -> str:

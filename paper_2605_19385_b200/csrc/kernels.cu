@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(256) gn_apply_kernel(const __half* x, __half* 
 // A chunk never straddles an image (every image is a multiple of 32 KB), and thread t always
 // owns channel octet t mod CV (256 is a multiple of CV), so its 8 affine pairs change only with
 // the image.
-constexpr int kApChunk = 32768, kApStages = 4;
+#ifndef LBX_AP_STAGES
+#define LBX_AP_STAGES 4
+#endif
+constexpr int kApChunk = 32768, kApStages = LBX_AP_STAGES;
 
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
