@@ -31,7 +31,7 @@ SYMBOLS = [
     "lbx_op_conv_out", "lbx_pack_bound", "lbx_pack_device", "lbx_op_attention",
     "lbx_png_bound", "lbx_png_encode_device", "lbx_reconstruct_png", "lbx_op_unpack", "lbx_op_set_grid_limits",
     "lbx_host_alloc", "lbx_host_free", "lbx_reconstruct_v", "lbx_reconstruct_submit", "lbx_reconstruct_wait",
-    "lbx_graph_captures",
+    "lbx_graph_captures", "lbx_decoder_get_counters",
 ]
 
 
@@ -46,6 +46,11 @@ class LbxError(RuntimeError):
 class ProfEntry(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 96), ("ms", ctypes.c_double), ("flops", ctypes.c_double),
                 ("algo_flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+class DecoderCounters(ctypes.Structure):
+    _fields_ = [("graph_captures", ctypes.c_uint64), ("peer_copies", ctypes.c_uint64), ("peer_bytes", ctypes.c_uint64),
+                ("peer_ms", ctypes.c_double), ("attn_fallbacks", ctypes.c_uint64)]
 
 
 class GemmDesc(ctypes.Structure):
@@ -125,6 +130,7 @@ def lib() -> ctypes.CDLL:
     L.lbx_reconstruct_v.argtypes = [vp, vp, vp, u32, vp, vp]
     L.lbx_reconstruct_submit.argtypes = [vp, vp, vp, u32, vp, ctypes.POINTER(ctypes.c_uint64)]
     L.lbx_reconstruct_wait.argtypes = [vp, ctypes.c_uint64]
+    L.lbx_decoder_get_counters.argtypes = [vp, ctypes.POINTER(DecoderCounters)]
     L.lbx_graph_captures.argtypes = [vp]
     L.lbx_graph_captures.restype = ctypes.c_uint64
     for name in SYMBOLS:
@@ -231,6 +237,12 @@ class Decoder:
     def graph_captures(self) -> int:
         """CUDA graphs captured so far (one per batch size)."""
         return int(lib().lbx_graph_captures(self._h))
+
+    def counters(self) -> dict:
+        """lbx_decoder_get_counters: graph captures, NVLink peer copies, attention fallbacks."""
+        c = DecoderCounters()
+        check(lib().lbx_decoder_get_counters(self._h, ctypes.byref(c)))
+        return {name: getattr(c, name) for name, _ in DecoderCounters._fields_}
 
     def prepare(self, n_max: int) -> None:
         check(lib().lbx_decoder_prepare(self._h, n_max))

@@ -100,6 +100,7 @@ class Decoder {
   float* rowmax = nullptr;    // fused-exp attention: sampled row maxima, 2 per row of a group
   float* rowpart = nullptr;   // fused-exp attention: row partial sums, 2 per (row, 256-key tile)
   int* attn_flag = nullptr;   // fused-exp attention: per-group overflow flags (fallback runs if set)
+  unsigned long long* attn_fallbacks = nullptr;  // flagged groups so far (never reset; counters API)
   unsigned long long* stats = nullptr;  // GroupNorm sites, gnfix.cuh layout
   float2* ss = nullptr;
   uint8_t* rgb = nullptr;
@@ -422,7 +423,7 @@ lbx_status Decoder::alloc_arena() {
   };
   const size_t oX = slot(x_el * 2), oA = slot(x_el * 2), oH = slot(h_el * 2), oS = slot(s_el * 2),
                oVt = slot(vt_el * 2), oR = slot(hw * 4 * (size_t)s_imgs), oRm = slot(hw * 8 * (size_t)s_imgs),
-               oRp = slot(hw * (size_t)s_imgs * (hw / 256 + 1) * 8), oFl = slot(4 * (size_t)(nb + 1)), oSt = slot((size_t)kMaxSites * nb * 32 * kGnStatWords * 8),
+               oRp = slot(hw * (size_t)s_imgs * (hw / 256 + 1) * 8), oFl = slot(4 * (size_t)(nb + 1)), oCnt = slot(8), oSt = slot((size_t)kMaxSites * nb * 32 * kGnStatWords * 8),
                oSs = slot(nb * 512 * 8), oLat = slot(nb * cl * hw * 2), oRgb = slot(nb * hw * 64 * 3),
                oErr = slot(64);
   LBX_CUDA_TRY(cudaMalloc(&arena, off));
@@ -436,6 +437,8 @@ lbx_status Decoder::alloc_arena() {
   rowmax = (float*)(b + oRm);
   rowpart = (float*)(b + oRp);
   attn_flag = (int*)(b + oFl);
+  attn_fallbacks = (unsigned long long*)(b + oCnt);
+  LBX_CUDA_TRY(cudaMemset(attn_fallbacks, 0, 8));
   stats = (unsigned long long*)(b + oSt);
   ss = (float2*)(b + oSs);
   lat = (__half*)(b + oLat);
@@ -740,6 +743,8 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       pv.row_scale = rowscale;
       if ((st = gemm(pv, "attn.pv")) != LBX_OK) return st;
     }
+    if (fused_exp)
+      LBX_LAUNCH(launch_attn_count(attn_flag, (n + gsz - 1) / gsz, attn_fallbacks, s), "attn.count", 0.0);
     GemmArgs o;
     o.mode = GEMM_PLAIN;
     o.M = n * L; o.N = 512; o.K = 512;
@@ -1149,6 +1154,11 @@ lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out)
   out->peer_copies = dec->d.peer_copies;
   out->peer_bytes = dec->d.peer_bytes;
   out->peer_ms = dec->d.peer_ms;
+  out->attn_fallbacks = 0;
+  if (dec->d.attn_fallbacks) {
+    LBX_CUDA_TRY(cudaSetDevice(dec->d.desc.device));
+    LBX_CUDA_TRY(cudaMemcpy(&out->attn_fallbacks, dec->d.attn_fallbacks, 8, cudaMemcpyDeviceToHost));
+  }
   return LBX_OK;
 }
 

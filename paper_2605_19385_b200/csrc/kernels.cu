@@ -457,6 +457,17 @@ void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int row
   attn_rowred_kernel<false><<<grid, 256, 0, s>>>(part, nparts, row_scale, rows, run_if);
 }
 
+// counter += number of flagged attention groups (the decoder's lbx_decoder_counters.attn_fallbacks)
+__global__ void attn_count_kernel(const int* __restrict__ flags, int groups, unsigned long long* counter) {
+  unsigned long long c = 0;
+  for (int i = 0; i < groups; ++i) c += flags[i] != 0;
+  if (c) atomicAdd(counter, c);
+}
+
+void launch_attn_count(const int* flags, int groups, unsigned long long* counter, cudaStream_t s) {
+  attn_count_kernel<<<1, 1, 0, s>>>(flags, groups, counter);
+}
+
 void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s, const int* run_if) {
   const int grid = run_if ? std::min((rows + 7) / 8, num_sms() * 8) : (rows + 7) / 8;
   attn_rowred_kernel<true><<<grid, 256, 0, s>>>(part, nparts, row_max2, rows, run_if);

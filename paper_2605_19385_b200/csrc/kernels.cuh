@@ -42,6 +42,7 @@ void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int row
                         const int* run_if = nullptr);
 void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s,
                         const int* run_if = nullptr);
+void launch_attn_count(const int* flags, int groups, unsigned long long* counter, cudaStream_t s);
 
 // out[c][r] = in[r][c] for an R x Cc block with input row stride ldi and output row stride ldo.
 void launch_transpose(const __half* in, int ldi, __half* out, int ldo, int R, int Cc, cudaStream_t s);

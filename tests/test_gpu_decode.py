@@ -144,7 +144,12 @@ def test_attention_overflow_fallback_peaked_scores(lbx):
     ref = vae_ref.decode(z, w, "sd15")
     try:
         lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
-        natural = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1).reconstruct_latents(z)
+        dec = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1)
+        natural = dec.reconstruct_latents(z)
+        assert dec.counters()["attn_fallbacks"] >= 1  # the one attention group was flagged
+        plain = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=1)
+        plain.reconstruct_latents(z)
+        assert plain.counters()["attn_fallbacks"] == 0
         lbx.check(lbx.lib().lbx_op_set_debug(1 | (1 << 11), 0))
         forced = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1).reconstruct_latents(z)
     finally:
