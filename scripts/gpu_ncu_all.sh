@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 N=$(timeout -s KILL 300 python scripts/ncu_kernels.py --batch 8 | grep "launches per decode" | awk '{print $4}')
 echo "launches per decode: $N"
 timeout -s KILL 2400 ncu --set full --clock-control none -s $N \
-  -k regex:'gemm_tc|gn_apply|softmax|conv_out|latent_prep|gn_finalize|lblp|png_' \
+  -k regex:'gemm_tc|gn_apply|softmax|attn_|conv_out|latent_prep|gn_finalize|lblp|png_' \
   -o gpurun_out/ncu_all_$TAG python scripts/ncu_kernels.py --batch 8 > gpurun_out/ncu_all_$TAG.log 2>&1
 tail -n 3 gpurun_out/ncu_all_$TAG.log
 ls -la gpurun_out/ncu_all_$TAG.ncu-rep
