@@ -403,6 +403,16 @@ lbx_status Decoder::upload_weights(const std::vector<float>& p) {
   return LBX_OK;
 }
 
+// Images per conv launch: 8 (a batch-32 decode measured 285.7 against 292.1 ms per step with one
+// launch per conv, bit-identical; 4 measured the same as 8).  LBX_CONV_CHUNK overrides (0: one launch).
+static int conv_chunk_images() {
+  static const int v = [] {
+    const char* e = std::getenv("LBX_CONV_CHUNK");
+    return e ? std::max(0, std::atoi(e)) : 8;
+  }();
+  return v;
+}
+
 // --------------------------------------------------------------------------- arena
 lbx_status Decoder::alloc_arena() {
   const size_t hw = (size_t)h * w;
@@ -548,8 +558,33 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   LBX_STEP(cudaMemsetAsync(stats, 0, (size_t)kMaxSites * site_stride * 8, s), "memset stats");
 
   auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
-    ++launches;
-    lbx_status e = chk(gemm_tc_launch(ga, s), what);
+    lbx_status e = LBX_OK;
+    const int chunk = conv_chunk_images();
+    if (ga.mode != GEMM_PLAIN && chunk > 0 && ga.B_img > chunk) {
+      // a long conv launch as several launches of `chunk` whole images: the persistent clusters
+      // drift apart over hundreds of tiles, and vertically adjacent tiles -- which share halo rows --
+      // then run too far apart for the rows to survive in L2.  Each launch starts
+      // the clusters in step again.  Image tiles map to clusters exactly as in one launch, so the
+      // GroupNorm partial sums (and the decode) are bit-identical.
+      const size_t hw = (size_t)ga.H * ga.W, ohw = ga.mode == GEMM_SUBPIX ? 4 * hw : hw;
+      for (int i0 = 0; i0 < ga.B_img && e == LBX_OK; i0 += chunk) {
+        GemmArgs c = ga;
+        const int cnt = std::min(chunk, ga.B_img - i0);
+        c.B_img = cnt;
+        c.M = (int)(cnt * hw);
+        c.A = ga.A + i0 * hw * ga.C;
+        if (ga.A2) c.A2 = ga.A2 + i0 * hw * ga.lda2;
+        c.out = ga.out + i0 * ohw * ga.ldo;
+        if (ga.resid) c.resid = ga.resid + i0 * hw * ga.ldr;
+        if (ga.gn_stats) c.gn_stats = ga.gn_stats + (size_t)i0 * 32 * kGnStatWords;
+        if (ga.gn_ss) c.gn_ss = ga.gn_ss + (size_t)i0 * ga.C;
+        ++launches;
+        e = chk(gemm_tc_launch(c, s), what);
+      }
+    } else {
+      ++launches;
+      e = chk(gemm_tc_launch(ga, s), what);
+    }
     if (e == LBX_OK && prof) {
       const double fl_main = 2.0 * ga.M * (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1);  // 4 phases
       const double fl = fl_main + 2.0 * ga.M * (double)ga.N * ga.K2;  // executed, incl. the folded K

@@ -76,6 +76,7 @@ struct KParams {
   int vsub;            // 1: the sub-tiles are vertically adjacent image rows sharing one halo box
   int b_mn;            // 1: B is MN-major in memory ([K][N], N contiguous), staged as 64-wide N atoms
   int rpf;             // 1: the residual is preloaded into the TMEM accumulator by the epilogue warps
+  int a_hint;          // 1: conv A boxes loaded with an L2 evict_last policy (LBX_A_HINT, A/B)
   int rpf_pf;          // 1: L2-prefetch the next preload's rows before waiting for the accumulator
   int sched;           // 1: each cluster takes a contiguous block of tiles (conv modes), 0: round-robin
   int pdl;             // 1: launched as a programmatic dependent (wait before any global access)
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       int st = 0;
       uint32_t ph = 0, rph = 0;
       const int tot_taps = n_a * per_a;
+      const uint64_t a_pol = p.a_hint ? ptx::l2_policy_evict_last() : 0ull;
       for (int t = t_first; t < t_end; t += t_step) {
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
@@ -358,6 +360,9 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
           if (p.mode == GEMM_PLAIN) {
             if constexpr (CG == 1) ptx::tma_load_2d(&tmA, &a_full[st], dst, c0, c1);
             else ptx::tma_load_2d_pair(&tmA, &a_full[st], dst, c0, c1);
+          } else if (p.a_hint) {  // halo rows: keep them in L2 for the vertically adjacent tiles
+            if constexpr (CG == 1 || XF) ptx::tma_load_4d_hint(&tmA, &a_full[st], dst, c0, c1, c2, c3, a_pol);
+            else ptx::tma_load_4d_pair_hint(&tmA, &a_full[st], dst, c0, c1, c2, c3, a_pol);
           } else {
             if constexpr (CG == 1 || XF) ptx::tma_load_4d(&tmA, &a_full[st], dst, c0, c1, c2, c3);
             else ptx::tma_load_4d_pair(&tmA, &a_full[st], dst, c0, c1, c2, c3);
@@ -1346,6 +1351,8 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.rpf = (a.resid && a.mode == GEMM_CONV3X3 && !a.row_scale && a.alpha == 1.f && !a.gn_ss && g_rpf_policy &&
             (g_rpf_policy == 2 || a.N <= 128)) ? 1 : 0;
   kp.rpf_pf = g_rpf_pf;
+  static const int a_hint = std::getenv("LBX_A_HINT") ? std::atoi(std::getenv("LBX_A_HINT")) : 0;
+  kp.a_hint = (a_hint && a.mode != GEMM_PLAIN) ? 1 : 0;
   kp.sched = (g_sched_policy && a.mode != GEMM_PLAIN) ? 1 : 0;
   kp.pdl = g_pdl_policy;
   kp.rres = (kp.rpf && g_rres_policy && !kp.tstore && a.ldr % 8 == 0) ? 1 : 0;
