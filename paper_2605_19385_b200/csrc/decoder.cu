@@ -557,34 +557,10 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
   if (prof) mark("start", 0, 0, 0);
   LBX_STEP(cudaMemsetAsync(stats, 0, (size_t)kMaxSites * site_stride * 8, s), "memset stats");
 
-  auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
-    lbx_status e = LBX_OK;
-    const int chunk = conv_chunk_images();
-    if (ga.mode != GEMM_PLAIN && chunk > 0 && ga.B_img > chunk) {
-      // a long conv launch as several launches of `chunk` whole images: the persistent clusters
-      // drift apart over hundreds of tiles, and vertically adjacent tiles -- which share halo rows --
-      // then run too far apart for the rows to survive in L2.  Each launch starts
-      // the clusters in step again.  Image tiles map to clusters exactly as in one launch, so the
-      // GroupNorm partial sums (and the decode) are bit-identical.
-      const size_t hw = (size_t)ga.H * ga.W, ohw = ga.mode == GEMM_SUBPIX ? 4 * hw : hw;
-      for (int i0 = 0; i0 < ga.B_img && e == LBX_OK; i0 += chunk) {
-        GemmArgs c = ga;
-        const int cnt = std::min(chunk, ga.B_img - i0);
-        c.B_img = cnt;
-        c.M = (int)(cnt * hw);
-        c.A = ga.A + i0 * hw * ga.C;
-        if (ga.A2) c.A2 = ga.A2 + i0 * hw * ga.lda2;
-        c.out = ga.out + i0 * ohw * ga.ldo;
-        if (ga.resid) c.resid = ga.resid + i0 * hw * ga.ldr;
-        if (ga.gn_stats) c.gn_stats = ga.gn_stats + (size_t)i0 * 32 * kGnStatWords;
-        if (ga.gn_ss) c.gn_ss = ga.gn_ss + (size_t)i0 * ga.C;
-        ++launches;
-        e = chk(gemm_tc_launch(c, s), what);
-      }
-    } else {
-      ++launches;
-      e = chk(gemm_tc_launch(ga, s), what);
-    }
+  // one kernel launch, and (profiling) its entry: executed / algorithmic FLOPs and bytes of this launch
+  auto launch1 = [&](const GemmArgs& ga, const char* what) -> lbx_status {
+    ++launches;
+    const lbx_status e = chk(gemm_tc_launch(ga, s), what);
     if (e == LBX_OK && prof) {
       const double fl_main = 2.0 * ga.M * (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1);  // 4 phases
       const double fl = fl_main + 2.0 * ga.M * (double)ga.N * ga.K2;  // executed, incl. the folded K
@@ -598,13 +574,38 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       char nm[160];
       if (ga.mode == GEMM_PLAIN)
         snprintf(nm, sizeof nm, "%s gemm M%d N%d K%d", what, ga.M, ga.N, ga.K);
-      else
+      else  // named per layer (not per chunk): the launches of one conv group together
         snprintf(nm, sizeof nm, "%s %s c%d->%d @%dx%d", what, ga.mode == GEMM_CONV3X3 ? "conv3x3" : "subpix2x2",
                  ga.C, ga.N, ga.mode == GEMM_SUBPIX ? 2 * ga.H : ga.H, ga.mode == GEMM_SUBPIX ? 2 * ga.W : ga.W);
       const double by = 2.0 * ((double)ga.M * ga.K / (ga.mode == GEMM_PLAIN ? 1 : (ga.mode == GEMM_CONV3X3 ? 9 : 4)) +
                                (double)ga.N * ga.K * (ga.mode == GEMM_SUBPIX ? 4 : 1) +
                                (double)ga.M * ga.N * (ga.mode == GEMM_SUBPIX ? 4 : 1) * (ga.resid ? 2 : 1));
       mark(nm, fl_ex, algo, ga.run_if ? 0.0 : by);
+    }
+    return e;
+  };
+  auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
+    const int chunk = conv_chunk_images();
+    if (ga.mode == GEMM_PLAIN || chunk <= 0 || ga.B_img <= chunk) return launch1(ga, what);
+    // a long conv launch as several launches of `chunk` whole images: the persistent clusters
+    // drift apart over hundreds of tiles, and vertically adjacent tiles -- which share halo rows --
+    // then run too far apart for the rows to survive in L2.  Each launch starts the
+    // clusters in step again.  Image tiles map to clusters exactly as in one launch, so the
+    // GroupNorm partial sums (and the decode) are bit-identical.
+    const size_t hw = (size_t)ga.H * ga.W, ohw = ga.mode == GEMM_SUBPIX ? 4 * hw : hw;
+    lbx_status e = LBX_OK;
+    for (int i0 = 0; i0 < ga.B_img && e == LBX_OK; i0 += chunk) {
+      GemmArgs c = ga;
+      const int cnt = std::min(chunk, ga.B_img - i0);
+      c.B_img = cnt;
+      c.M = (int)(cnt * hw);
+      c.A = ga.A + i0 * hw * ga.C;
+      if (ga.A2) c.A2 = ga.A2 + i0 * hw * ga.lda2;
+      c.out = ga.out + i0 * ohw * ga.ldo;
+      if (ga.resid) c.resid = ga.resid + i0 * hw * ga.ldr;
+      if (ga.gn_stats) c.gn_stats = ga.gn_stats + (size_t)i0 * 32 * kGnStatWords;
+      if (ga.gn_ss) c.gn_ss = ga.gn_ss + (size_t)i0 * ga.C;
+      e = launch1(c, what);
     }
     return e;
   };
