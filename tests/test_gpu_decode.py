@@ -158,6 +158,21 @@ def test_attention_overflow_fallback_peaked_scores(lbx):
     _check(_stats(natural, ref), "sd15 peaked attention (fallback taken)")
 
 
+def test_chunked_conv_launches_batch_invariance(lbx):
+    """The decoder launches each conv 8 images at a time: a batch of 11 runs as an
+    8-image and a 3-image launch per conv.  Images on both sides of the split, including the ragged
+    last chunk, decode bit-identically to the same latents alone, and stay within the oracle bar."""
+    import vae_ref
+    import weights_ref
+    z = weights_ref.make_latents("sd15", 11, 64, 64, seed=17)
+    dec = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=11)
+    batch = dec.reconstruct_latents(z)
+    for i in (0, 7, 8, 10):
+        assert np.array_equal(dec.reconstruct_latents(z[i:i + 1])[0], batch[i]), i
+    ref = vae_ref.decode(z[8:9], weights_ref.make_weights("sd15", 0), "sd15")
+    _check(_stats(batch[8:9], ref), "batch 11 (8 + 3 image launches), image 8")
+
+
 def test_decode_device_pointers_and_graph_reuse(lbx):
     """lbx_decode on device buffers; repeated calls (graph replay) are bit-identical."""
     import torch
