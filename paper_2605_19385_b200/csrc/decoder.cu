@@ -403,14 +403,26 @@ lbx_status Decoder::upload_weights(const std::vector<float>& p) {
   return LBX_OK;
 }
 
-// Images per conv launch: 8 (a batch-32 decode measured 285.7 against 292.1 ms per step with one
-// launch per conv, bit-identical; 4 measured the same as 8).  LBX_CONV_CHUNK overrides (0: one launch).
-static int conv_chunk_images() {
+// Images per conv launch.  LBX_CONV_CHUNK = k > 0 fixes k images (0: one launch per conv); by
+// default (-1) each launch gets about LBX_CONV_CHUNK_ELEMS output elements (2^28: 8 images of a
+// c512 @256^2 conv, 2 of a c128 @1024^2 conv, the whole batch of the small 128^2 layers).  A fixed 8
+// measured 285.7 against 292.1 ms per batch-32 step with one launch per conv, bit-identical; the
+// 2^28-element rule 278.0 against 279.8 for the fixed 8 (2^27 and 2^29 in between).
+static int conv_chunk_fixed() {
   static const int v = [] {
     const char* e = std::getenv("LBX_CONV_CHUNK");
-    return e ? std::max(0, std::atoi(e)) : 8;
+    return e ? std::atoi(e) : -1;
   }();
   return v;
+}
+static int conv_chunk_images(size_t out_elems_per_image) {
+  const int fixed = conv_chunk_fixed();
+  if (fixed >= 0) return fixed;
+  static const double target = [] {
+    const char* e = std::getenv("LBX_CONV_CHUNK_ELEMS");
+    return e ? std::atof(e) : 268435456.0;
+  }();
+  return std::max(1, (int)(target / (double)std::max<size_t>(1, out_elems_per_image)));
 }
 
 // --------------------------------------------------------------------------- arena
@@ -585,8 +597,9 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     return e;
   };
   auto gemm = [&](GemmArgs ga, const char* what) -> lbx_status {
-    const int chunk = conv_chunk_images();
-    if (ga.mode == GEMM_PLAIN || chunk <= 0 || ga.B_img <= chunk) return launch1(ga, what);
+    if (ga.mode == GEMM_PLAIN) return launch1(ga, what);
+    const int chunk = conv_chunk_images((size_t)ga.H * ga.W * ga.N * (ga.mode == GEMM_SUBPIX ? 4 : 1));
+    if (chunk <= 0 || ga.B_img <= chunk) return launch1(ga, what);
     // a long conv launch as several launches of `chunk` whole images: the persistent clusters
     // drift apart over hundreds of tiles, and vertically adjacent tiles -- which share halo rows --
     // then run too far apart for the rows to survive in L2.  Each launch starts the
