@@ -73,7 +73,7 @@ def ncu_dom(tag):
             "smsp__issue_active.avg.pct_of_peak_sustained_active"]
     vals = {}
     out = [f"# ncu --set full --clock-control none of the dominant kernel (conv3x3 c128->128 + residual + GN "
-           f"statistics, 8 images at 1024^2 = one of the decoder's 8-image conv launches): scripts/op_bench.py conv --b 8 --hw 1024 --c 128 --resid --stats (residual preloaded into TMEM, as in the decoder)"]
+           f"statistics, 2 images at 1024^2 = one of the decoder's launches of this conv, 2^28 output elements): scripts/op_bench.py conv --b 2 --hw 1024 --c 128 --resid --stats (residual preloaded into TMEM, as in the decoder)"]
     for i, name in enumerate(h):
         if name in want:
             vals[name] = (v[i], u[i])
@@ -90,10 +90,10 @@ def ncu_dom(tag):
         return f * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}[unit]
     traffic = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
     tj = {"resnet.conv2+residual conv3x3 c128->128 @1024x1024": traffic,
-          "_source": f"profiles/{tag}_ncu_dominant.txt: ncu --set full of scripts/op_bench.py conv --b 8 --hw 1024 "
-                     "--c 128 --resid --stats (the decoder's dominant launch: convs run as 8-image launches); "
-                     "dram__bytes_read.sum + dram__bytes_write.sum per launch; algorithmic = 3 x 2.15 GB "
-                     "(input, residual, output)"}
+          "_source": f"profiles/{tag}_ncu_dominant.txt: ncu --set full of scripts/op_bench.py conv --b 2 --hw 1024 "
+                     "--c 128 --resid --stats (the decoder's dominant launch: this conv runs 2 images per "
+                     "launch); dram__bytes_read.sum + dram__bytes_write.sum per launch; algorithmic = "
+                     "3 x 0.537 GB (input, residual, output)"}
     json.dump(tj, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
 
