@@ -173,6 +173,22 @@ def test_chunked_conv_launches_batch_invariance(lbx):
     _check(_stats(batch[8:9], ref), "batch 11 (8 + 3 image launches), image 8")
 
 
+@pytest.mark.parametrize("fam,lh,lw", [("sd15", 32, 128), ("sd3", 48, 64)])
+def test_non_square_latents_vs_oracle(lbx, fam, lh, lw):
+    """Non-square latents (256x1024 and 384x512 outputs): rows and columns of different lengths at
+    every resolution, an attention of L = lh*lw keys (sampled at stride L/256), batch 2 against the
+    oracle and against the same latents decoded alone."""
+    import vae_ref
+    import weights_ref
+    z = weights_ref.make_latents(fam, 2, lh, lw, seed=23)
+    ref = vae_ref.decode(z, weights_ref.make_weights(fam, 0), fam)
+    dec = lbx.Decoder(fam, (lh, lw), seed=0, max_batch=2)
+    got = dec.reconstruct_latents(z)
+    assert got.shape == (2, 8 * lh, 8 * lw, 3)
+    _check(_stats(got, ref), f"{fam} {lh}x{lw} -> {8 * lh}x{8 * lw}, batch 2")
+    assert np.array_equal(dec.reconstruct_latents(z[1:2])[0], got[1])
+
+
 def test_decode_device_pointers_and_graph_reuse(lbx):
     """lbx_decode on device buffers; repeated calls (graph replay) are bit-identical."""
     import torch
