@@ -137,8 +137,8 @@ typedef struct {
   uint64_t peer_copies;    /* blobs fetched from another GPU (lbx_reconstruct_submit_dev) */
   uint64_t peer_bytes;     /* their bytes */
   double peer_ms;          /* device time of the batches' peer-copy phases, summed (CUDA events) */
-  uint64_t attn_fallbacks; /* attention groups whose sampled-maximum softmax could overflow fp16 and
-                              were recomputed against the exact row maximum (normally 0) */
+  uint64_t attn_fallbacks; /* images whose sampled-maximum attention softmax could overflow fp16 and
+                              was recomputed against the exact row maximum (normally 0) */
 } lbx_decoder_counters;
 LBX_API lbx_status lbx_decoder_get_counters(lbx_decoder* dec, lbx_decoder_counters* out);
 

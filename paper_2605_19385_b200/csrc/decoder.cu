@@ -99,8 +99,8 @@ class Decoder {
   float* rowscale = nullptr;
   float* rowmax = nullptr;    // fused-exp attention: sampled row maxima, 2 per row of a group
   float* rowpart = nullptr;   // fused-exp attention: row partial sums, 2 per (row, 256-key tile)
-  int* attn_flag = nullptr;   // fused-exp attention: per-group overflow flags (fallback runs if set)
-  unsigned long long* attn_fallbacks = nullptr;  // flagged groups so far (never reset; counters API)
+  int* attn_flag = nullptr;   // fused-exp attention: per-image overflow flags (fallback runs if set)
+  unsigned long long* attn_fallbacks = nullptr;  // flagged images so far (never reset; counters API)
   unsigned long long* stats = nullptr;  // GroupNorm sites, gnfix.cuh layout
   float2* ss = nullptr;
   uint8_t* rgb = nullptr;
@@ -731,7 +731,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
     // (batched plain GEMMs; the P.V of a single image is only 128 pair-tiles, < 2 waves)
     const int gsz = v_transpose_legacy() ? 1 : s_imgs;
     const bool fused_exp = attn_fused_exp() && L % 256 == 0 && L >= 256;
-    if (fused_exp) LBX_STEP(cudaMemsetAsync(attn_flag, 0, sizeof(int) * (size_t)((n + gsz - 1) / gsz), s), "memset attn flags");
+    if (fused_exp) LBX_STEP(cudaMemsetAsync(attn_flag, 0, sizeof(int) * (size_t)n, s), "memset attn flags");
     for (int i0 = 0; i0 < n; i0 += gsz) {
       const int g = std::min(gsz, n - i0);
       const __half* base = Hb + (size_t)i0 * L * 1536;
@@ -750,7 +750,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
         // overflow fp16 (a score ~11 above r_m) flags the group; the fallback below -- launched
         // always, running only when flagged -- takes the exact row maximum over all keys (the same
         // GEMM with N = L) and recomputes E against it, so every E <= 1.
-        int* flag = attn_flag + i0 / gsz;
+        int* flag = attn_flag + i0;  // one flag per image: a flagged image never changes another's pixels
         const int nparts = 2 * (L / 256);
         GemmArgs mx = sq;
         mx.N = 256;
@@ -766,13 +766,13 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
         LBX_LAUNCH(launch_attn_rowsum(rowpart, nparts, rowscale, g * L, s), "attn.rowsum",
                    4.0 * g * L * nparts + 4.0 * g * L);
         GemmArgs fmx = sq;  // fallback: exact row maxima over all keys (nothing stored)
-        fmx.rowred = 1; fmx.row_part = rowpart; fmx.run_if = flag;
+        fmx.rowred = 1; fmx.row_part = rowpart; fmx.run_if = flag; fmx.run_if_n = g;
         if ((st = gemm(fmx, "attn.score_max(fallback)")) != LBX_OK) return st;
-        LBX_LAUNCH(launch_attn_rowmax(rowpart, nparts, rowmax, g * L, s, flag), "attn.rowmax(fallback)", 0.0);
+        LBX_LAUNCH(launch_attn_rowmax(rowpart, nparts, rowmax, g * L, s, flag, L), "attn.rowmax(fallback)", 0.0);
         GemmArgs fex = ex;
-        fex.exp_force = 0; fex.run_if = flag;
+        fex.exp_force = 0; fex.run_if = flag; fex.run_if_n = g;
         if ((st = gemm(fex, "attn.scores+exp(fallback)")) != LBX_OK) return st;
-        LBX_LAUNCH(launch_attn_rowsum(rowpart, nparts, rowscale, g * L, s, flag), "attn.rowsum(fallback)", 0.0);
+        LBX_LAUNCH(launch_attn_rowsum(rowpart, nparts, rowscale, g * L, s, flag, L), "attn.rowsum(fallback)", 0.0);
       } else {
         if ((st = gemm(sq, "attn.scores")) != LBX_OK) return st;
         LBX_LAUNCH(launch_softmax_rows(S, rowscale, g * L, L, s), "attn.softmax", 4.0 * g * L * (double)L);
@@ -793,7 +793,7 @@ lbx_status Decoder::plan(int n, const __half* lat_in, uint8_t* rgb_out, cudaStre
       if ((st = gemm(pv, "attn.pv")) != LBX_OK) return st;
     }
     if (fused_exp)
-      LBX_LAUNCH(launch_attn_count(attn_flag, (n + gsz - 1) / gsz, attn_fallbacks, s), "attn.count", 0.0);
+      LBX_LAUNCH(launch_attn_count(attn_flag, n, attn_fallbacks, s), "attn.count", 0.0);
     GemmArgs o;
     o.mode = GEMM_PLAIN;
     o.M = n * L; o.N = 512; o.K = 512;

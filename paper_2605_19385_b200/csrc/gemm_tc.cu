@@ -88,7 +88,8 @@ struct KParams {
   int* exp_flag;
   int exp_force;       // tests: flag every group (the exact-softmax fallback always runs)
   int exp_h2;          // rowred 2: fp16 exponent, two E per MUFU op (ex2.approx.f16x2)
-  const int* run_if;   // skip the launch unless *run_if != 0
+  const int* run_if;   // per-image guards (GemmArgs::run_if): skip the tiles of unflagged images
+  int run_if_n;
   int ld_skip;         // diagnostics (bits 27 / 28): after a CTA's first tile the B / A producer only
                        // arrives on the full barrier (no TMA; stale operands, wrong results) -- the
                        // energy and time of the operand traffic
@@ -156,6 +157,17 @@ __device__ __forceinline__ int tile_row0(const KParams& p, int m_tile, int rank,
   const int yp = fdiv(r, p.fd_segs);
   const int x0 = (r - yp * p.segs) * 128 * CG + rank * 128;
   return (img * p.H + yp * p.msub + sub) * p.W + x0;
+}
+
+// Guarded launches (run_if): the tile belongs to an image whose flag is clear -- every warp role
+// skips it, so the tile sequences of producers, MMA issuer and epilogue stay in step.
+__device__ __forceinline__ bool tile_off(const KParams& p, int t, int CG) {
+  if (!p.run_if) return false;
+  int m_tile, n_tile, phase;
+  tile_coords(p, t, m_tile, n_tile, phase);
+  const long long m0 = (long long)m_tile * (128 * p.msub * CG);
+  const int img = p.batch_m ? (int)(m0 / p.batch_m) : 0;
+  return reinterpret_cast<const volatile int*>(p.run_if)[img] == 0;
 }
 
 // Per-lane GroupNorm partials of one chunk: NV = 2 * (groups per chunk) values -- the group sums,
@@ -250,9 +262,11 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
   const int n_a = p.halo ? p.cblocks : p.num_kb;
   const int per_a = p.halo ? p.taps : 1;
 
-  if (p.run_if) {  // uniform across the grid: every CTA reads the same flag before any barrier
+  if (p.run_if) {  // uniform across the grid: every CTA reads the same flags before any barrier
     if (p.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (*reinterpret_cast<const volatile int*>(p.run_if) == 0) return;
+    int any = 0;
+    for (int i = 0; i < p.run_if_n; ++i) any |= reinterpret_cast<const volatile int*>(p.run_if)[i];
+    if (!any) return;
   }
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch(&tmA);
@@ -293,6 +307,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       const int tot_taps = n_a * per_a;
       const uint64_t a_pol = p.a_hint ? ptx::l2_policy_evict_last() : 0ull;
       for (int t = t_first; t < t_end; t += t_step) {
+        if (tile_off(p, t, CG)) continue;
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int rows_cta = 128 * p.msub;
@@ -392,6 +407,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       int st = 0;
       uint32_t ph = 0;
       for (int t = t_first; t < t_end; t += t_step) {
+        if (tile_off(p, t, CG)) continue;
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         const int bimg = p.batch_m ? (m_tile * 128 * p.msub * CG) / p.batch_m : 0;  // batched: image of the tile
@@ -467,6 +483,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       const uint32_t rb = (p.rbuf && p.n_extra) ? 1u : 0u;  // the tile's first MMA is an extra k-block's
       const int tot_taps = n_a * per_a;
       for (int t = t_first; t < t_end; t += t_step) {
+        if (tile_off(p, t, CG)) continue;
         int m_tile, n_tile, phs;
         tile_coords(p, t, m_tile, n_tile, phs);
         // rpf: every use of a buffer (the first included) waits for the epilogue's residual preload
@@ -571,6 +588,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     int st = 0;
     uint32_t ph = 0;
     for (int t = t_first; t < t_end; t += t_step) {
+      if (tile_off(p, t, CG)) continue;
       int m_tile, n_tile, phs;
       tile_coords(p, t, m_tile, n_tile, phs);
       const int m0 = tile_row0(p, m_tile, (int)rank, CG, 0);
@@ -781,6 +799,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
     uint32_t acc_phase = 0;
     uint32_t ochunk = 0;  // tstore: staged chunks so far (selects the staging buffer)
     for (int t = t_first; t < t_end; t += t_step) {
+      if (tile_off(p, t, CG)) continue;
       int m_tile, n_tile, ph;
       tile_coords(p, t, m_tile, n_tile, ph);
       const int n0 = n_tile * BN;
@@ -1000,7 +1019,7 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
       }
       if (RR && p.rowred) {
         p.row_part[(size_t)m * (2 * p.n_tiles) + n_tile * 2 + hsel] = racc;
-        if (p.rowred == 2 && (rbig || p.exp_force)) atomicOr(p.exp_flag, 1);
+        if (p.rowred == 2 && (rbig || p.exp_force)) atomicOr(p.exp_flag + (p.batch_m ? m / p.batch_m : 0), 1);
       }
       }  // sub-tiles
       if (p.rpf) {
@@ -1358,6 +1377,7 @@ cudaError_t gemm_tc_launch(const GemmArgs& a, cudaStream_t stream, int force_cg,
   kp.rres = (kp.rpf && g_rres_policy && !kp.tstore && a.ldr % 8 == 0) ? 1 : 0;
   kp.row_scale = a.row_scale; kp.alpha = a.alpha;
   kp.run_if = a.run_if;
+  kp.run_if_n = a.run_if ? std::max(1, a.run_if_n) : 0;
   if (a.rowred) {  // plain GEMM, 256-wide tiles (two column halves per tile), nothing else in the epilogue
     if (a.mode != GEMM_PLAIN || a.bias || a.resid || a.gn_stats || a.row_scale || !a.row_part ||
         (a.rowred == 2 && (!a.row_max || !a.exp_flag)) || a.rowred > 2 || a.N % 256 || force_bn == 128)

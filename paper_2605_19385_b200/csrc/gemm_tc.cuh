@@ -55,15 +55,19 @@ struct GemmArgs {
   //   rowred 1: the maximum of the scaled values; nothing is stored
   //   rowred 2: E = exp(v - r_m) is stored (fp16), r_m = max(row_max[2m], row_max[2m + 1]) (a
   //             rowred-1 pass over a sample of the keys); row_part gets the fp32 sums of E.  A
-  //             32-column chunk whose sum reaches 65504 (an E may overflow fp16) sets *exp_flag,
-  //             and the caller reruns the exact softmax for the group (exp_force: always).
+  //             32-column chunk whose sum reaches 65504 (an E may overflow fp16) sets the flag of
+  //             its image, exp_flag[m / batch_m], and the caller recomputes that image's softmax
+  //             (exp_force: every image).
   int rowred = 0;
   const float* row_max = nullptr;
   float* row_part = nullptr;
   int* exp_flag = nullptr;
   int exp_force = 0;
-  // if set, the launch does nothing unless *run_if != 0 (the exact-softmax fallback of a group)
+  // per-image guard (the fallback of the fused softmax): run_if[i] for the launch's images
+  // i < run_if_n (rows m / batch_m); tiles of images whose flag is 0 are skipped, and a launch with
+  // no flag set exits at once
   const int* run_if = nullptr;
+  int run_if_n = 1;
 };
 
 // Launch on `stream`.  Returns cudaSuccess or the launch error.  Chooses tile / CTA-pair config.

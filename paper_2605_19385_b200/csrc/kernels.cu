@@ -429,10 +429,16 @@ void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaSt
 // wave of row-looping warps that exit at once unless the group was flagged.
 template <bool MAX>
 __global__ void __launch_bounds__(256) attn_rowred_kernel(const float* __restrict__ part, int nparts,
-                                                          float* __restrict__ out, int rows, const int* run_if) {
-  if (run_if && *reinterpret_cast<const volatile int*>(run_if) == 0) return;
+                                                          float* __restrict__ out, int rows, const int* run_if,
+                                                          int rows_per_img) {
   const int lane = threadIdx.x & 31;
+  if (run_if) {  // per-image guards: nothing to do unless some image of the launch is flagged
+    int any = 0;
+    for (int i = 0; i < rows / rows_per_img; ++i) any |= reinterpret_cast<const volatile int*>(run_if)[i];
+    if (!any) return;
+  }
   for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += gridDim.x * 8) {
+    if (run_if && reinterpret_cast<const volatile int*>(run_if)[r / rows_per_img] == 0) continue;
     const float* pr = part + (size_t)r * nparts;
     float t = MAX ? -INFINITY : 0.f;
     for (int i = lane; i < nparts; i += 32) t = MAX ? fmaxf(t, pr[i]) : t + pr[i];
@@ -452,12 +458,13 @@ __global__ void __launch_bounds__(256) attn_rowred_kernel(const float* __restric
   }
 }
 
-void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s, const int* run_if) {
+void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s, const int* run_if,
+                        int rows_per_img) {
   const int grid = run_if ? std::min((rows + 7) / 8, num_sms() * 8) : (rows + 7) / 8;
-  attn_rowred_kernel<false><<<grid, 256, 0, s>>>(part, nparts, row_scale, rows, run_if);
+  attn_rowred_kernel<false><<<grid, 256, 0, s>>>(part, nparts, row_scale, rows, run_if, rows_per_img);
 }
 
-// counter += number of flagged attention groups (the decoder's lbx_decoder_counters.attn_fallbacks)
+// counter += number of flagged images (the decoder's lbx_decoder_counters.attn_fallbacks)
 __global__ void attn_count_kernel(const int* __restrict__ flags, int groups, unsigned long long* counter) {
   unsigned long long c = 0;
   for (int i = 0; i < groups; ++i) c += flags[i] != 0;
@@ -468,9 +475,10 @@ void launch_attn_count(const int* flags, int groups, unsigned long long* counter
   attn_count_kernel<<<1, 1, 0, s>>>(flags, groups, counter);
 }
 
-void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s, const int* run_if) {
+void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s, const int* run_if,
+                        int rows_per_img) {
   const int grid = run_if ? std::min((rows + 7) / 8, num_sms() * 8) : (rows + 7) / 8;
-  attn_rowred_kernel<true><<<grid, 256, 0, s>>>(part, nparts, row_max2, rows, run_if);
+  attn_rowred_kernel<true><<<grid, 256, 0, s>>>(part, nparts, row_max2, rows, run_if, rows_per_img);
 }
 
 // ----------------------------------------------------------------------------- transpose

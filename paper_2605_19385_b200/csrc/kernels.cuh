@@ -36,12 +36,12 @@ void launch_gn_apply(const __half* x, __half* y, const GnSrc& g, long long rows,
 // With run_if set the launch does nothing unless *run_if != 0 (the fused-exp path's fallback).
 void launch_softmax_rows(__half* S, float* row_scale, int rows, int cols, cudaStream_t s, const int* run_if = nullptr);
 // Fused-exp attention scores: row_scale[r] = 1 / sum(part[r][0 .. nparts)) in a fixed order, and
-// (fallback) row_max2[2r] = max(part[r][..]), row_max2[2r + 1] = -inf.  With run_if set the launch
-// does nothing unless *run_if != 0.
+// (fallback) row_max2[2r] = max(part[r][..]), row_max2[2r + 1] = -inf.  With run_if set only the
+// rows of flagged images (run_if[r / rows_per_img] != 0) are computed.
 void launch_attn_rowsum(const float* part, int nparts, float* row_scale, int rows, cudaStream_t s,
-                        const int* run_if = nullptr);
+                        const int* run_if = nullptr, int rows_per_img = 1);
 void launch_attn_rowmax(const float* part, int nparts, float* row_max2, int rows, cudaStream_t s,
-                        const int* run_if = nullptr);
+                        const int* run_if = nullptr, int rows_per_img = 1);
 void launch_attn_count(const int* flags, int groups, unsigned long long* counter, cudaStream_t s);
 
 // out[c][r] = in[r][c] for an R x Cc block with input row stride ldi and output row stride ldo.

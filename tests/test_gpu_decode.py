@@ -146,7 +146,7 @@ def test_attention_overflow_fallback_peaked_scores(lbx):
         lbx.check(lbx.lib().lbx_op_set_debug(1, 0))
         dec = lbx.Decoder("sd15", (64, 64), weights=blob, max_batch=1)
         natural = dec.reconstruct_latents(z)
-        assert dec.counters()["attn_fallbacks"] >= 1  # the one attention group was flagged
+        assert dec.counters()["attn_fallbacks"] >= 1  # the one image was flagged
         plain = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=1)
         plain.reconstruct_latents(z)
         assert plain.counters()["attn_fallbacks"] == 0
@@ -216,6 +216,25 @@ def test_config_errors(lbx):
     with pytest.raises(lbx.LbxError) as e:
         dec.reconstruct_latents(z)  # n > max_batch
     assert e.value.status == lbx.E_CONFIG
+
+
+def test_non_finite_latents_are_contained(lbx):
+    """A latent holding NaN / inf (a corrupt blob that still unpacks) decodes without an error or a
+    hang, deterministically, and does not touch the other image of its batch: NaN spreads through
+    its own image (GroupNorm statistics and attention are per image) and flags only that image for
+    the attention fallback (per-image flags), which the fallback counter shows."""
+    import weights_ref
+    z = weights_ref.make_latents("sd15", 2, 64, 64, seed=29)
+    clean = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=1).reconstruct_latents(z[1:2])[0]
+    bad = z.copy()
+    bad[0, 0, 5, 7] = np.float16(np.nan)
+    bad[0, 2, 40, 3] = np.float16(np.inf)
+    dec = lbx.Decoder("sd15", (64, 64), seed=0, max_batch=2)
+    a = dec.reconstruct_latents(bad)
+    b = dec.reconstruct_latents(bad)
+    assert np.array_equal(a, b)
+    assert np.array_equal(a[1], clean)  # the finite image of the batch is unaffected
+    assert dec.counters()["attn_fallbacks"] >= 1
 
 
 def test_flux_family_vs_oracle(lbx):
