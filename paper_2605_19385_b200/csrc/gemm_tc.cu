@@ -754,8 +754,17 @@ __global__ void __launch_bounds__(XF ? 512 : 352, 1)
 #pragma unroll
           for (int j = 0; j < NCH; ++j) {
             uint4 u[4];
+            if (p.ld_skip & 4) {  // diagnostics (bit 4 of ld_skip): preload zeros, no residual loads
 #pragma unroll
-            for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(rb + j * 32 * cstep) + i);
+              for (int i = 0; i < 4; ++i) u[i] = make_uint4(0, 0, 0, 0);
+            } else if (p.ld_skip & 8) {  // diagnostics: the residual rows of tile 0 (L2-resident)
+              const __half* r0 = p.resid + (long long)row * p.ldr + cbase * 32;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(r0 + j * 32 * cstep) + i);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) u[i] = __ldg(reinterpret_cast<const uint4*>(rb + j * 32 * cstep) + i);
+            }
             uint32_t r[32];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -1159,6 +1168,7 @@ void gemm_tc_set_debug(int halo_policy, int desc_base_mode) {
   g_attn_exp = ((halo_policy >> 3) & 1) ? 0 : ((halo_policy >> 30) & 1) ? 2 : 1;  // bit 30: f16x2 exp
   g_attn_fallback = (halo_policy >> 11) & 1;
   g_ld_skip = ((halo_policy >> 27) & 1) | (((halo_policy >> 28) & 1) << 1);
+  if (const char* e = std::getenv("LBX_RESID_DIAG")) g_ld_skip |= (std::atoi(e) & 3) << 2;  // 1 zeros, 2 L2 rows
   g_store_mode = ((halo_policy >> 16) & 3) ? (((halo_policy >> 16) & 3) - 1) : 1;
   g_epi_skip = ((halo_policy >> 12) & 1) ? 1 : ((halo_policy >> 13) & 1) ? 2 : ((halo_policy >> 14) & 1) ? 3
                                                                      : ((halo_policy >> 15) & 1) ? 4 : 0;
