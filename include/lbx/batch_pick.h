@@ -11,20 +11,31 @@
 #include <stdint.h>
 
 /* cost_ms[b-1] = GPU time of a batch of b (b = 1..n_cost, linear past n_cost).  Returns the batch
- * size in [1, min(queued, max_batch)] with the lowest time per request; a larger batch must beat
- * the best smaller one by 2%.  No curve: min(queued, max_batch). */
+ * size b in [1, min(queued, max_batch)] that minimises the mean completion time of the `queued`
+ * requests if they were all served FIFO in batches of b (the last one partial).  With a short
+ * queue a batch must be much cheaper per request to pay for holding its first requests back until
+ * the whole batch finishes; under a backlog (queued >> b) the rule tends to the lowest time per
+ * request, i.e. throughput.  No curve: min(queued, max_batch). */
+static inline double lbx_batch_cost_at(const double* cost_ms, uint32_t n_cost, uint32_t b) {
+  return b <= n_cost ? cost_ms[b - 1] : cost_ms[n_cost - 1] * b / n_cost;
+}
 static inline uint32_t lbx_batch_pick_rule(const double* cost_ms, uint32_t n_cost, uint32_t queued,
                                            uint32_t max_batch) {
   const uint32_t lim = queued < max_batch ? queued : max_batch;
   if (lim == 0) return 0;
   if (!cost_ms || n_cost == 0) return lim;
   uint32_t best = 1;
-  double per = cost_ms[0];
-  for (uint32_t b = 2; b <= lim; ++b) {
-    const double c = (b <= n_cost ? cost_ms[b - 1] : cost_ms[n_cost - 1] * b / n_cost) / b;
-    if (c < per * 0.98) {
+  double best_mean = 0.0;
+  for (uint32_t b = 1; b <= lim; ++b) {
+    const double mb = lbx_batch_cost_at(cost_ms, n_cost, b);
+    const uint32_t k = queued / b, r = queued - k * b;  /* k full batches, then one of r */
+    /* sum of completion times: b requests finish at i * mb for i = 1..k, r at k * mb + m(r) */
+    double sum = (double)b * mb * (double)k * (double)(k + 1) / 2.0;
+    if (r) sum += (double)r * ((double)k * mb + lbx_batch_cost_at(cost_ms, n_cost, r));
+    const double mean = sum / (double)queued;
+    if (b == 1 || mean < best_mean * (1.0 - 1e-9)) {
       best = b;
-      per = c;
+      best_mean = mean;
     }
   }
   return best;
