@@ -92,10 +92,11 @@ LBX_API uint64_t lbx_batcher_pending(lbx_batcher* b);
 
 /* Batch size to close from `queued` waiting requests, 1 <= result <= min(queued, max_batch) (0 if
  * queued == 0), given a service curve cost_ms[b-1] = GPU time of a batch of b, b = 1..n_cost
- * (extended linearly past n_cost): the size with the lowest GPU time per request, where a larger
- * batch must beat the best smaller one by 2%.  cost_ms == NULL: min(queued, max_batch) (greedy).
- * On B200 the decode's time per image is flat in the batch size, so this returns 1 and batching
- * adds only latency; on engines with a fixed per-launch cost it batches. */
+ * (extended linearly past n_cost): the size that minimises the mean completion time of the queued
+ * requests served FIFO in batches of that size.  cost_ms == NULL: min(queued, max_batch) (greedy).
+ * On B200 the decode's time per image is nearly flat in the batch size, so this returns 1 until a
+ * deep backlog (batching would make early requests wait for late ones); on engines with a fixed
+ * per-launch cost it batches. */
 LBX_API uint32_t lbx_batch_pick(const double* cost_ms, uint32_t n_cost, uint32_t queued, uint32_t max_batch);
 
 /* Steady-clock microseconds, the time base of lbx_completion. */
