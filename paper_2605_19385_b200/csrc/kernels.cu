@@ -185,19 +185,44 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
       bulk_load(ring + k * kApChunk, src + (first + k * step) * kApChunk, kApChunk, &full[k]);
     }
   }
-  int cur_img = -1;
-  float a[8], b[8];
+  int cur_img = -1, pf_img = -1;
+  float a[8], b[8], na[8], nb[8];
+  // the next image's statistics: loaded while the current chunk is rewritten, finalized after it,
+  // so an image change no longer stalls on dependent L2 loads (small images change every few chunks)
+  unsigned long long pw[8][4];
+  float pg[8], pb[8];
+  // chunk -> image with 32-bit arithmetic (a 64-bit divide per chunk was a measurable share of the
+  // issue slots): the chunk count stays far below 2^32 and an image is a whole number of chunks
+  const uint32_t cpi = (uint32_t)(img_bytes / kApChunk);
   for (long long k = 0; k < mine; ++k) {
     const int st = (int)(k % kApStages);
     const long long c = first + k * step;
-    const int img = (int)(c * kApChunk / img_bytes);
-    if (img != cur_img) {  // finalize this thread's 8 channels of the new image
+    const int img = (int)((uint32_t)c / cpi);
+    if (img != cur_img) {  // this thread's 8 channels of the new image
+      if (img == pf_img) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) { a[j] = na[j]; b[j] = nb[j]; }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 t = site_affine(g, img, cvec * 8 + j, CV / 4);
+          a[j] = (SILU && H2) ? 0.5f * t.x : t.x;  // halved for gn_silu8_h2_half
+          b[j] = (SILU && H2) ? 0.5f * t.y : t.y;
+        }
+      }
       cur_img = img;
+    }
+    const int img_n = k + 1 < mine ? (int)((uint32_t)(c + step) / cpi) : -1;
+    const bool pf = img_n >= 0 && img_n != img && img_n != pf_img;
+    if (pf) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float2 t = site_affine(g, img, cvec * 8 + j, CV / 4);
-        a[j] = (SILU && H2) ? 0.5f * t.x : t.x;  // halved for gn_silu8_h2_half
-        b[j] = (SILU && H2) ? 0.5f * t.y : t.y;
+        const int ch = cvec * 8 + j;
+        const unsigned long long* stp = g.stats + ((size_t)img_n * 32 + ch / (CV / 4)) * kGnStatWords;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) pw[j][w] = __ldg(stp + w);
+        pg[j] = __ldg(g.gamma + ch);
+        pb[j] = __ldg(g.beta + ch);
       }
     }
     ptx::mbar_wait(&full[st], (uint32_t)((k / kApStages) & 1));
@@ -206,6 +231,15 @@ __global__ void __launch_bounds__(256, 1) gn_apply_bulk_kernel(const __half* x, 
     for (int i = 0; i < kApChunk / 16 / 256; ++i) {
       const uint4 u = q[tid + 256 * i];
       q[tid + 256 * i] = (SILU && H2) ? gn_silu8_h2_half(u, a, b) : gn_act8<SILU>(u, a, b);
+    }
+    if (pf) {  // the same gn_affine arithmetic as site_affine (bit-identical)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 t = gn_affine(gnfix_value(pw[j]), gnfix_value(pw[j] + 2), g.inv_count, pg[j], pb[j], g.eps);
+        na[j] = (SILU && H2) ? 0.5f * t.x : t.x;
+        nb[j] = (SILU && H2) ? 0.5f * t.y : t.y;
+      }
+      pf_img = img_n;
     }
     ptx::fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk store
     __syncthreads();
